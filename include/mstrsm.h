@@ -1,0 +1,171 @@
+/*
+ * mstrsm.h -- C ABI of libmstrsm.so: the B200-native (sm_100a) blocked, optionally
+ * overflow-safe, multi-shift triangular solve of Moon & Poulson, arXiv 1607.01477
+ * ("Accelerating eigenvector and pseudospectra computation using blocked multi-shift
+ * triangular solves"), plus the two drivers the paper builds on it.
+ *
+ * Citations: P:n = line n of the paper text.  R# = reading in DESIGN.md §3.
+ *
+ * Conventions for every call
+ *   - Column-major (LAPACK) storage with leading dimensions; element (i,j) of a matrix A
+ *     with leading dimension lda is A[i + j*lda] (0-based).
+ *   - Complex numbers are interleaved (re, im) doubles: mstrsm_dcomplex has the layout of C99
+ *     double _Complex, std::complex<double>, cuDoubleComplex and torch.complex128.
+ *   - Unless stated otherwise, every array argument is a DEVICE pointer, owned by the
+ *     caller, and must stay valid until the work enqueued by the call has completed.
+ *     B / Z are overwritten in place.  U, T, shifts are read-only.
+ *   - The strictly lower triangle of U / T is never read.
+ *   - Calls are ASYNCHRONOUS on the library's current stream (mstrsm_set_stream; default
+ *     the legacy default stream): they enqueue kernels and return.  Device workspace is
+ *     allocated stream-ordered (cudaMallocAsync) and released stream-ordered.
+ *   - nb is the block size n_b of Alg. 2/3/5.  nb = 0 selects the default
+ *     (64).  1 <= nb <= 128.  nb is part of the semantics of the safe variants (it sets
+ *     the granularity of the growth-bound updates, R10).
+ *
+ * Return codes (LAPACK INFO style)
+ *     0   success (possibly with rescaling, reported through scales / scale_exp)
+ *    -i   argument i is invalid (1-based position in the C prototype)
+ *     1   CUDA launch / runtime error (message: mstrsm_error_string(1))
+ *     2   non-finite entry in U or the shifts (safe variants; reported by
+ *         mstrsm_status(), which synchronises -- the solve itself stays asynchronous)
+ *     3   communication error (multi-GPU helpers)
+ *   m == 0 or n == 0 returns 0 immediately.  A zero right-hand-side column yields x = 0,
+ *   c = 1 (R13).  The unsafe variants do not replace zero pivots: Inf/NaN propagate.
+ */
+#ifndef MSTRSM_H
+#define MSTRSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } mstrsm_dcomplex;
+
+typedef enum {
+    MSTRSM_OP_N = 0,   /* (U - s_j I)   x_j = c_j b_j : back substitution, blocks bottom-up   */
+    MSTRSM_OP_C = 1    /* (U - s_j I)^H x_j = c_j b_j : forward substitution, blocks top-down
+                          (P:58-62 footnote: the lower-triangular case)                      */
+} mstrsm_op;
+
+/* ------------------------------------------------------------------------------------
+ * Multi-shift triangular solve, Alg. 3: for j = 0..n-1 solve
+ *     (U - shifts[j] I) x_j = b_j          (B(:,j) = b_j on entry, x_j on exit)
+ * U: m x m upper triangular (ldu >= max(1,m)); shifts: n scalars; B: m x n (ldb >= max(1,m)).
+ * scales (nullable, n doubles) is set to 1.0 (the plain solve never rescales).
+ * Work: per block one diagonal-block solve per column + one shift-free update GEMM
+ * B(I0,:) -= U(I0,I1) X(I1,:) shared by every shift.
+ */
+int mstrsm_d(const double *U, int64_t ldu, int64_t m, const double *shifts,
+             double *B, int64_t ldb, int64_t n, double *scales, int nb);
+int mstrsm_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts,
+             mstrsm_dcomplex *B, int64_t ldb, int64_t n, double *scales, int nb);
+
+/* ------------------------------------------------------------------------------------
+ * Safe multi-shift triangular solve, Alg. 5 with Alg. 4 on the
+ * diagonal blocks: find x_j and c_j in [0,1] with (U - s_j I) x_j = c_j b_j
+ * such that no intermediate reaches Omega = 2^970 (R1).  c_j = 2^{e_j} exactly (R2);
+ * scales (required, n doubles) receives c_j, which may underflow to 0 (R12).
+ * Zero pivots U(i,i) - s_j == 0 are replaced by delta = 2^-52 ||U||_inf (R4).
+ */
+int mstrsm_d_safe(const double *U, int64_t ldu, int64_t m, const double *shifts,
+                  double *B, int64_t ldb, int64_t n, double *scales, int nb);
+int mstrsm_z_safe(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts,
+                  mstrsm_dcomplex *B, int64_t ldb, int64_t n, double *scales, int nb);
+
+/* ------------------------------------------------------------------------------------
+ * Extended form of both solves.
+ *   safe          0: Alg. 3, 1: Alg. 5
+ *   op            MSTRSM_OP_N or MSTRSM_OP_C (C: (U - s I)^H, i.e. L = U^H - conj(s) I)
+ *   shift_stride  stride between consecutive shifts (ldu + 1 reads diag(U) in place)
+ *   row_end_host  HOST pointer (nullable, op N only): n values r_j in [0, m]; column j is
+ *                 solved on rows [0, r_j) and rows [r_j, m) are set to 0 (R26; the eigen
+ *                 shortcut of P:503-508 is r_k = k).  If the values are non-decreasing the
+ *                 library skips inactive columns per block.  Copied before return.
+ *   scales        nullable for safe = 0; required for safe = 1
+ *   scale_exp     nullable: n int32 receiving e_j (c_j = 2^{e_j}); 0 for safe = 0
+ */
+int mstrsm_d_ex(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m,
+                const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
+                const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb);
+int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
+                const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb,
+                int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
+                int nb);
+
+/* ------------------------------------------------------------------------------------
+ * Triangular eigenvectors, Alg. 6 TriangEig: lambda = diag(T); Z := -T with
+ * diag(Z) := 0; safe multi-shift solve with shifts lambda, shortcut to the strictly upper
+ * RHS (R11); diag(Z) := s.  T Z = Z diag(lambda) backward-stably.
+ *   T      m x m upper triangular (ldt >= max(1,m)), read-only
+ *   Z      m x m output (ldz >= max(1,m)); Z(k,k) = c_k = 2^{e_k}, rows > k are 0
+ *   scales nullable (m doubles, = diag Z); scale_exp nullable (m int32)
+ */
+int trevc_d(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz,
+            double *scales, int32_t *scale_exp, int nb);
+int trevc_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, mstrsm_dcomplex *Z, int64_t ldz,
+            double *scales, int32_t *scale_exp, int nb);
+
+/* Column subset (the shard of one GPU when shifts are partitioned across GPUs):
+ *   cols_host  HOST pointer, ncols strictly increasing eigenvector indices in [0, m)
+ *   Z          m x ncols output: Z(:,q) is eigenvector cols_host[q]; scales/scale_exp
+ *              have ncols entries.  Results are bit-identical to the corresponding columns
+ *              of trevc_* (columns are independent).                         */
+int trevc_d_cols(const double *T, int64_t ldt, int64_t m, const int64_t *cols_host,
+                 int64_t ncols, double *Z, int64_t ldz, double *scales, int32_t *scale_exp,
+                 int nb);
+int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t *cols_host,
+                 int64_t ncols, mstrsm_dcomplex *Z, int64_t ldz, double *scales,
+                 int32_t *scale_exp, int nb);
+
+/* End-to-end entry with HOST buffers: copies T (pinned or pageable host memory) to the
+ * device, runs trevc_z, copies Z, scales and scale_exp back, and synchronises.
+ * All pointers are HOST pointers (scales / scale_exp nullable).  Blocking.            */
+int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *Z_host,
+                 int64_t ldz, double *scales_host, int32_t *scale_exp_host, int nb);
+
+/* ------------------------------------------------------------------------------------
+ * Pseudospectra, Van Loan / Lui with multi-shift batching: for
+ * every point z_p, sigma_min(U - z_p I) = 1/sqrt(lambda_max((U - zI)^{-H}(U - zI)^{-1}))
+ * (P:600-604), lambda_max by `iters` Lanczos steps (R14) from the
+ * shared unit-2-norm start vector v0 (m complex, device).  Each step is one op-N and one
+ * op-C safe multi-shift solve over all points at once.
+ *   z          npts complex shifts (device)
+ *   sigma_min  npts doubles (device, output)
+ *   flags      nullable npts int32: bit0 = a solve rescaled (near-singular point); sigma
+ *              is then the upper bound c_1/||y||_2 of that step (R25)
+ */
+int pseudospectra_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z,
+                    int64_t npts, int iters, const mstrsm_dcomplex *v0, double *sigma_min,
+                    int32_t *flags, int nb);
+
+/* ------------------------------------------------------------------------------------
+ * Runtime helpers */
+int         mstrsm_set_stream(void *cuda_stream);  /* cudaStream_t; NULL = legacy stream */
+void       *mstrsm_get_stream(void);
+const char *mstrsm_error_string(int code);
+/* Synchronises the current stream; returns 0, 1 (sticky CUDA error) or 2 (a safe call
+ * since the last mstrsm_status saw a non-finite U entry or shift); clears the flag.   */
+int         mstrsm_status(void);
+/* Number of kernels libmstrsm.so has launched since the last reset (for bench/gpu_launches). */
+int64_t     mstrsm_launch_count(int reset);
+
+/* Live kernel timing for the bench: mstrsm_profile(1) clears and starts bracketing every
+ * library launch with CUDA events on the launching stream; mstrsm_profile(0) stops.
+ * mstrsm_profile_read synchronises and returns, for one kernel kind (0 = update GEMM,
+ * 1 = diagonal-block kernel, 2 = other), the summed device time, the launch count and the
+ * algorithmic flops of those launches (GEMM: 2 M N K real / 8 M N K complex).            */
+int         mstrsm_profile(int enable);
+int         mstrsm_profile_read(int kind, double *total_ms, int64_t *launches, double *flops);
+
+/* FP64 roofline probe: a register-resident DMMA (mma.sync.m8n8k4.f64) loop and a DFMA loop
+ * on every SM for about `ms` milliseconds each; returns achieved TFLOP/s (2 flops/FMA).
+ * Synchronous.                                                                          */
+int mstrsm_fp64_peak(double ms, double *dmma_tflops, double *dfma_tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSTRSM_H */

@@ -1,5 +1,274 @@
-"""ctypes binding for libmstrsm.so (filled in with the CUDA library)."""
+"""ctypes binding for libmstrsm.so (C ABI in include/mstrsm.h).
+
+Argument marshalling only: every step of the solve runs in the library's sm_100a kernels.
+Functions carry the C names (``mstrsm_d``, ``mstrsm_z_safe``, ``trevc_z``, ``pseudospectra_z``,
+...) and take torch CUDA tensors; a few convenience wrappers (``solve``, ``trevc``,
+``pseudospectra``) allocate outputs.  The library runs on torch's current CUDA stream.
+
+There is no CPU fallback: if the library is missing or CUDA is unavailable, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmstrsm.so")
+_lib = None
+
+c_i64, c_int, c_dbl, c_vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+
+__all__ = [
+    "load", "LIB_PATH", "MstrsmError",
+    "mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
+    "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
+    "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
+    "mstrsm_profile", "mstrsm_profile_read",
+    "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count",
+]
+
+
+class MstrsmError(RuntimeError):
+    pass
 
 
 def load():
-    raise RuntimeError("libmstrsm.so not built yet")
+    """Load libmstrsm.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise MstrsmError(f"{LIB_PATH} not built; run `make` or __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = c_vp
+    sig = {
+        "mstrsm_d": [P, c_i64, c_i64, P, P, c_i64, c_i64, P, c_int],
+        "mstrsm_z": [P, c_i64, c_i64, P, P, c_i64, c_i64, P, c_int],
+        "mstrsm_d_safe": [P, c_i64, c_i64, P, P, c_i64, c_i64, P, c_int],
+        "mstrsm_z_safe": [P, c_i64, c_i64, P, P, c_i64, c_i64, P, c_int],
+        "mstrsm_d_ex": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
+        "mstrsm_z_ex": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
+        "trevc_d": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
+        "trevc_z": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
+        "trevc_d_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
+        "trevc_z_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
+        "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
+        "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
+        "mstrsm_set_stream": [P],
+        "mstrsm_status": [],
+        "mstrsm_launch_count": [c_int],
+        "mstrsm_fp64_peak": [c_dbl, P, P],
+        "mstrsm_error_string": [c_int],
+        "mstrsm_profile": [c_int],
+        "mstrsm_profile_read": [c_int, P, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = c_int
+    lib.mstrsm_launch_count.restype = c_i64
+    lib.mstrsm_error_string.restype = ctypes.c_char_p
+    lib.mstrsm_get_stream.restype = c_vp
+    _lib = lib
+    return lib
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise MstrsmError("CUDA is not available: libmstrsm has no CPU path")
+    return torch
+
+
+def _bind_stream(lib):
+    torch = _torch()
+    lib.mstrsm_set_stream(c_vp(torch.cuda.current_stream().cuda_stream))
+
+
+def _check(rc: int, name: str):
+    if rc != 0:
+        msg = _lib.mstrsm_error_string(rc).decode()
+        raise MstrsmError(f"{name} returned {rc}: {msg}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return c_vp(t.data_ptr())
+
+
+def _ld(t) -> int:
+    """Leading dimension of a column-major (Fortran-strided) 2-D tensor."""
+    if t.dim() == 1:
+        return max(1, t.shape[0])
+    if t.stride(0) != 1:
+        raise ValueError("matrices must be column-major: use tensor.t().contiguous().t() "
+                         "or allocate with torch.empty(n, m).t()")
+    return max(1, t.stride(1), t.shape[0])
+
+
+def _host_i64(a):
+    if a is None:
+        return None, None
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+    return arr, arr.ctypes.data_as(c_vp)
+
+
+# ------------------------------------------------------------------ C-named entry points
+def _call(name, *args):
+    lib = load()
+    _bind_stream(lib)
+    _check(getattr(lib, name)(*args), name)
+
+
+def mstrsm_d(U, ldu, m, shifts, B, ldb, n, scales, nb):
+    _call("mstrsm_d", _ptr(U), ldu, m, _ptr(shifts), _ptr(B), ldb, n, _ptr(scales), nb)
+
+
+def mstrsm_z(U, ldu, m, shifts, B, ldb, n, scales, nb):
+    _call("mstrsm_z", _ptr(U), ldu, m, _ptr(shifts), _ptr(B), ldb, n, _ptr(scales), nb)
+
+
+def mstrsm_d_safe(U, ldu, m, shifts, B, ldb, n, scales, nb):
+    _call("mstrsm_d_safe", _ptr(U), ldu, m, _ptr(shifts), _ptr(B), ldb, n, _ptr(scales), nb)
+
+
+def mstrsm_z_safe(U, ldu, m, shifts, B, ldb, n, scales, nb):
+    _call("mstrsm_z_safe", _ptr(U), ldu, m, _ptr(shifts), _ptr(B), ldb, n, _ptr(scales), nb)
+
+
+def mstrsm_d_ex(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
+    arr, p = _host_i64(row_end_host)
+    _call("mstrsm_d_ex", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
+          _ptr(scales), _ptr(scale_exp), nb)
+
+
+def mstrsm_z_ex(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
+    arr, p = _host_i64(row_end_host)
+    _call("mstrsm_z_ex", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
+          _ptr(scales), _ptr(scale_exp), nb)
+
+
+def trevc_d(T, ldt, m, Z, ldz, scales, scale_exp, nb):
+    _call("trevc_d", _ptr(T), ldt, m, _ptr(Z), ldz, _ptr(scales), _ptr(scale_exp), nb)
+
+
+def trevc_z(T, ldt, m, Z, ldz, scales, scale_exp, nb):
+    _call("trevc_z", _ptr(T), ldt, m, _ptr(Z), ldz, _ptr(scales), _ptr(scale_exp), nb)
+
+
+def trevc_d_cols(T, ldt, m, cols_host, ncols, Z, ldz, scales, scale_exp, nb):
+    arr, p = _host_i64(cols_host)
+    _call("trevc_d_cols", _ptr(T), ldt, m, p, ncols, _ptr(Z), ldz, _ptr(scales), _ptr(scale_exp), nb)
+
+
+def trevc_z_cols(T, ldt, m, cols_host, ncols, Z, ldz, scales, scale_exp, nb):
+    arr, p = _host_i64(cols_host)
+    _call("trevc_z_cols", _ptr(T), ldt, m, p, ncols, _ptr(Z), ldz, _ptr(scales), _ptr(scale_exp), nb)
+
+
+def trevc_z_host(T_host: np.ndarray, m: int, Z_host: np.ndarray, scales_host=None, exp_host=None, nb=0):
+    """Host-buffer end-to-end entry (numpy complex128 Fortran arrays, blocking)."""
+    lib = load()
+    _bind_stream(lib)
+    ptr = lambda a: a.ctypes.data_as(c_vp) if a is not None else None
+    _check(lib.trevc_z_host(ptr(T_host), T_host.shape[0], m, ptr(Z_host), Z_host.shape[0],
+                            ptr(scales_host), ptr(exp_host), nb), "trevc_z_host")
+
+
+def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
+    _call("pseudospectra_z", _ptr(U), ldu, m, _ptr(z), npts, iters, _ptr(v0), _ptr(sigma_min),
+          _ptr(flags), nb)
+
+
+def mstrsm_status() -> int:
+    lib = load()
+    _bind_stream(lib)
+    return int(lib.mstrsm_status())
+
+
+def mstrsm_launch_count(reset: int = 0) -> int:
+    return int(load().mstrsm_launch_count(reset))
+
+
+def mstrsm_fp64_peak(ms: float = 50.0):
+    lib = load()
+    _bind_stream(lib)
+    a, b = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib.mstrsm_fp64_peak(ms, ctypes.byref(a), ctypes.byref(b)), "mstrsm_fp64_peak")
+    return a.value, b.value
+
+
+def mstrsm_profile(enable: int):
+    lib = load()
+    _bind_stream(lib)
+    _check(lib.mstrsm_profile(enable), "mstrsm_profile")
+
+
+def mstrsm_profile_read(kind: int):
+    """(total device ms, launches, algorithmic flops) of one kernel kind since mstrsm_profile(1):
+    0 = update GEMM, 1 = diagonal-block kernel, 2 = other."""
+    lib = load()
+    _bind_stream(lib)
+    t, c, f = ctypes.c_double(0), ctypes.c_int64(0), ctypes.c_double(0)
+    _check(lib.mstrsm_profile_read(kind, ctypes.byref(t), ctypes.byref(c), ctypes.byref(f)),
+           "mstrsm_profile_read")
+    return t.value, c.value, f.value
+
+
+def mstrsm_error_string(code: int) -> str:
+    return load().mstrsm_error_string(code).decode()
+
+
+# ------------------------------------------------------------------ convenience wrappers
+status = mstrsm_status
+launch_count = mstrsm_launch_count
+fp64_peak = mstrsm_fp64_peak
+
+
+def colmajor(t):
+    """Column-major copy of a 2-D tensor (same device / dtype)."""
+    return t.t().contiguous().t()
+
+
+def solve(U, shifts, B, *, safe: bool = True, op: str = "N", nb: int = 64, row_end=None,
+          shift_stride: int = 1):
+    """In-place multi-shift solve on column-major CUDA tensors; returns (B, scales, scale_exp)."""
+    torch = _torch()
+    m, n = B.shape
+    cplx = B.dtype == torch.complex128
+    scales = torch.empty(n, dtype=torch.float64, device=B.device)
+    exps = torch.empty(n, dtype=torch.int32, device=B.device)
+    f = mstrsm_z_ex if cplx else mstrsm_d_ex
+    f(1 if safe else 0, 0 if op == "N" else 1, U, _ld(U), m, shifts, shift_stride, B, _ld(B), n,
+      row_end, scales, exps, nb)
+    return B, scales, exps
+
+
+def trevc(T, *, nb: int = 64, cols=None):
+    """Triangular eigenvectors of column-major CUDA tensor T; returns (Z, scales, scale_exp)."""
+    torch = _torch()
+    m = T.shape[0]
+    ncols = m if cols is None else len(cols)
+    Z = torch.empty((ncols, m), dtype=T.dtype, device=T.device).t()
+    scales = torch.empty(ncols, dtype=torch.float64, device=T.device)
+    exps = torch.empty(ncols, dtype=torch.int32, device=T.device)
+    cplx = T.dtype == torch.complex128
+    if cols is None:
+        (trevc_z if cplx else trevc_d)(T, _ld(T), m, Z, _ld(Z), scales, exps, nb)
+    else:
+        (trevc_z_cols if cplx else trevc_d_cols)(T, _ld(T), m, cols, ncols, Z, _ld(Z), scales, exps, nb)
+    return Z, scales, exps
+
+
+def pseudospectra(U, z, v0, *, iters: int = 15, nb: int = 64):
+    """sigma_min(U - z_p I) for all points; returns (sigma, flags)."""
+    torch = _torch()
+    m = U.shape[0]
+    npts = z.shape[0]
+    sigma = torch.empty(npts, dtype=torch.float64, device=U.device)
+    flags = torch.empty(npts, dtype=torch.int32, device=U.device)
+    pseudospectra_z(U, _ld(U), m, z, npts, iters, v0, sigma, flags, nb)
+    return sigma, flags

@@ -1,0 +1,235 @@
+// aux_kernels.cuh -- the memory-bound steps of the path (HBM-roofline kernels):
+//   a.1 RHS / state init  (eigen: P:519-525)
+//   a.2 norm pass          (delta: P:231-234)
+//   a.6 finalize           (lazy form of the xSCAL rescales P:378-380; diag Z P:530)
+#pragma once
+#include "common.cuh"
+
+namespace mstrsm {
+
+// ------------------------------------------------------------------------------------------
+// a.2 norm pass, op N.  One warp per column k (grid-stride):
+//   cnl[k]  = max_{lo(k) <= l < k} |U(l,k)|   (block-local off-diagonal column norm, R5)
+//   pcol[k] = max_{l < lo(k)} |U(l,k)|          (panel part of P_b, R6)
+// and flags a non-finite entry in U(0:k, k) (diagonal included).  max is order-free, so the
+// results are bit-identical to a sequential evaluation.
+template <typename T>
+__global__ void norm_cols_n_kernel(const T *__restrict__ U, int64_t ldu, int64_t m, int nb,
+                                   double *__restrict__ cnl, double *__restrict__ pcol,
+                                   int *__restrict__ nonfinite) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w; k < m; k += nw) {
+        int64_t b = (m - 1 - k) / nb;
+        Blk bl = block_rows(0, m, nb, b);
+        const T *col = U + k * ldu;
+        double c = 0.0, p = 0.0;
+        bool bad = false;
+        for (int64_t l = lane; l <= k; l += 32) {
+            T v = col[l];
+            double a = S<T>::mod(v);
+            bad |= !(a <= 1.7976931348623157e308);
+            if (l < bl.lo) p = fmax(p, a);
+            else if (l < k) c = fmax(c, a);
+        }
+        c = warp_max(c);
+        p = warp_max(p);
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            cnl[k] = c;
+            pcol[k] = p;
+            if (bad) atomicExch(nonfinite, 1);
+        }
+    }
+}
+
+// a.2 norm pass, op C (L = U^H).  One thread per row l of U; the warp walks the columns i of U
+// in lockstep so that every load is coalesced (consecutive rows of one column):
+//   cnl[l]  = max_{l < i < hi(l)} |U(l,i)|     (block-local column norm of L)
+//   prow[l] = max_{i >= hi(l)} |U(l,i)|
+template <typename T>
+__global__ void norm_rows_c_kernel(const T *__restrict__ U, int64_t ldu, int64_t m, int nb,
+                                   double *__restrict__ cnl, double *__restrict__ prow,
+                                   int *__restrict__ nonfinite) {
+    int64_t l = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t l0 = (int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31));   // first row of the warp
+    if (l0 >= m) return;
+    int64_t hi = l < m ? block_rows(1, m, nb, l / nb).hi : m;
+    double c = 0.0, p = 0.0;
+    bool bad = false;
+    for (int64_t i = l0; i < m; i++) {
+        if (l < m && i >= l) {
+            double a = S<T>::mod(U[l + i * ldu]);
+            bad |= !(a <= 1.7976931348623157e308);
+            if (i > l) {
+                if (i < hi) c = fmax(c, a); else p = fmax(p, a);
+            }
+        }
+    }
+    if (l < m) {
+        cnl[l] = c;
+        prow[l] = p;
+        if (bad) atomicExch(nonfinite, 1);
+    }
+}
+
+// Panel sums P_b, one thread per block, in the fixed order of R6 (op N: k ascending; op C:
+// l descending), sequential -> bit-identical to the oracle given bit-identical inputs.
+__global__ void panel_sum_kernel(int op, int64_t m, int nb, int64_t nblk,
+                                 const double *__restrict__ part, double *__restrict__ P) {
+    int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= nblk) return;
+    Blk bl = block_rows(op, m, nb, b);
+    double s = 0.0;
+    if (op == 0) for (int64_t k = bl.lo; k < bl.hi; k++) s = __dadd_rn(s, part[k]);
+    else for (int64_t l = bl.hi - 1; l >= bl.lo; l--) s = __dadd_rn(s, part[l]);
+    P[b] = s;
+}
+
+// ||U||_inf for delta (R4).  op N: row sums sum_{k >= i} |U(i,k)|, ascending k, one thread per
+// row, warp walks columns in lockstep (coalesced).  op C: column sums sum_{l = i..0} |U(l,i)|
+// (= rows of U^H), descending l, one thread per column.
+template <typename T>
+__global__ void rowsum_n_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
+                                double *__restrict__ rs) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t i0 = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+    if (i0 >= m) return;
+    double s = 0.0;
+    for (int64_t k = i0; k < m; k++)
+        if (i < m && k >= i) s = __dadd_rn(s, S<T>::mod(U[i + k * ldu]));
+    if (i < m) rs[i] = s;
+}
+
+template <typename T>
+__global__ void colsum_c_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
+                                double *__restrict__ rs) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double s = 0.0;
+    for (int64_t l = i; l >= 0; l--) s = __dadd_rn(s, S<T>::mod(U[l + i * ldu]));
+    rs[i] = s;
+}
+
+// delta = 2^-52 max(rs) (or DBL_MIN when U == 0), one block.
+__global__ void delta_kernel(int64_t m, const double *__restrict__ rs, double *__restrict__ delta) {
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) v = fmax(v, rs[i]);
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        v = warp_max(v);
+        if (threadIdx.x == 0) *delta = v > 0.0 ? ldexp(v, -52) : 2.2250738585072014e-308;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// a.1 init (general RHS).  One warp per column j: G_j = max_{l < r_j} |B(l,j)|,
+// e_j = 0, rows [r_j, m) zeroed (R26); flags non-finite shifts.
+template <typename T>
+__global__ void init_rhs_kernel(T *__restrict__ B, int64_t ldb, int64_t m, int64_t n,
+                                const int64_t *__restrict__ rowend, const T *__restrict__ shifts,
+                                int64_t sstride, double *__restrict__ G, int *__restrict__ e,
+                                int *__restrict__ nonfinite) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t j = w; j < n; j += nw) {
+        int64_t r = rowend ? rowend[j] : m;
+        r = r < 0 ? 0 : (r > m ? m : r);
+        T *x = B + j * ldb;
+        double g = 0.0;
+        for (int64_t l = lane; l < m; l += 32) {
+            if (l < r) g = fmax(g, S<T>::mod(x[l]));
+            else x[l] = S<T>::zero();
+        }
+        g = warp_max(g);
+        if (lane == 0) {
+            if (G) G[j] = g;
+            if (e) e[j] = 0;
+            if (shifts && nonfinite && !(S<T>::mod(shifts[j * sstride]) <= 1.7976931348623157e308))
+                atomicExch(nonfinite, 1);
+        }
+    }
+}
+
+// a.1 init for TriangEig (Alg. 6).  Column q holds eigenvector k = cols[q]:
+//   Z(l,q) = -T(l,k) for l < k, 0 for l >= k;  G_q = max_{l<k} |T(l,k)|;  shift_q = T(k,k);
+//   row_end_q = k (the P:503-508 shortcut).
+template <typename T>
+__global__ void init_trevc_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t m,
+                                  const int64_t *__restrict__ cols, int64_t ncols,
+                                  T *__restrict__ Z, int64_t ldz, T *__restrict__ shifts,
+                                  int64_t *__restrict__ rowend, double *__restrict__ G,
+                                  int *__restrict__ e, int *__restrict__ nonfinite) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = w; q < ncols; q += nw) {
+        int64_t k = cols ? cols[q] : q;
+        const T *tc = Tm + k * ldt;
+        T *z = Z + q * ldz;
+        double g = 0.0;
+        for (int64_t l = lane; l < m; l += 32) {
+            if (l < k) {
+                T v = tc[l];
+                g = fmax(g, S<T>::mod(v));
+                z[l] = S<T>::neg(v);
+            } else {
+                z[l] = S<T>::zero();
+            }
+        }
+        g = warp_max(g);
+        if (lane == 0) {
+            T d = tc[k];
+            shifts[q] = d;
+            rowend[q] = k;
+            G[q] = g;
+            e[q] = 0;
+            if (!(S<T>::mod(d) <= 1.7976931348623157e308)) atomicExch(nonfinite, 1);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// a.6 finalize.  Block b finalised rows I1(b) of column j in the frame E[b][j]; the final frame
+// is e_j, so X(I1(b), j) *= 2^{e_j - E[b][j]} (exact powers of two; the lazy form of the
+// eager xSCAL of rows I2 in P:378-380 / P:398).  Then c_j = 2^{e_j} -> scales, e_j -> exp,
+// and for TriangEig Z(k,q) = c_q.
+template <typename T>
+__global__ void finalize_kernel(int op, T *__restrict__ B, int64_t ldb, int64_t m, int64_t n,
+                                int nb, int64_t nblk, const int64_t *__restrict__ rowend,
+                                const int *__restrict__ e, const int *__restrict__ Etab,
+                                double *__restrict__ scales, int *__restrict__ scale_exp,
+                                const int64_t *__restrict__ diag_row) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t j = w; j < n; j += nw) {
+        int ej = e ? e[j] : 0;
+        int64_t r = rowend ? rowend[j] : m;
+        T *x = B + j * ldb;
+        if (Etab) {
+            for (int64_t b = 0; b < nblk; b++) {
+                Blk bl = block_rows(op, m, nb, b);
+                if (bl.lo >= r) continue;
+                int d = ej - Etab[b * n + j];
+                if (d == 0) continue;
+                int64_t hh = bl.hi < r ? bl.hi : r;
+                for (int64_t l = bl.lo + lane; l < hh; l += 32) x[l] = S<T>::ldx(x[l], d);
+            }
+        }
+        if (lane == 0) {
+            double c = ldexp(1.0, ej);
+            if (scales) scales[j] = c;
+            if (scale_exp) scale_exp[j] = ej;
+            if (diag_row) x[diag_row[j]] = S<T>::real(c);
+        }
+    }
+}
+
+}  // namespace mstrsm

@@ -1,0 +1,242 @@
+// gemm_kernel.cuh -- a.5, the shift-free substitution step shared by every shift:
+//
+//     C(i,j) <- 2^{d_j} C(i,j) - sum_k A(i,k) X(k,j)
+//
+//   op N: C = B(0:lo, cols), A = U(0:lo, lo:hi),         X = B(lo:hi, cols)
+//   op C: C = B(hi:m, cols), A = U(lo:hi, hi:m)^H,       X = B(lo:hi, cols)
+//
+// d_j <= 0 is the exponent change of column j in this block (safe variant, lazy form of the
+// xSCAL rescales of P:378-380 and P:398 applied to rows I0); d = 0 / null for the plain solve.
+//
+// FP64 tensor cores: sm_100a has no tcgen05 f64 kind, so the contraction is the warp-level
+// mma.sync.aligned.m8n8k4.f64 (SASS DMMA.8x8x4).  Complex = 4 real DMMA sub-products sharing
+// the A/X fragments (Cr += Ar Xr - Ai Xi, Ci += Ar Xi + Ai Xr).  Operand tiles are staged by
+// cp.async (LDGSTS) into a 3-stage shared-memory ring with XOR swizzles that make every fragment
+// load conflict-free; 4 warps (2x2) per CTA, 2 CTAs per SM.
+#pragma once
+#include "common.cuh"
+
+namespace mstrsm {
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// cp.async with zero fill when !valid (src-size 0).
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *dst, const void *src, bool valid) {
+    unsigned d = smem_u32(dst);
+    int sz = valid ? BYTES : 0;
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(BYTES), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <typename T>
+struct GemmArgs {
+    const T *U; int64_t ldu;
+    T *B; int64_t ldb;
+    int64_t M, N; int K;
+    int64_t a_r0, a_c0;    // op N: A(i,k) = U(a_r0+i, a_c0+k); op C: A(i,k) = conj(U(a_r0+k, a_c0+i))
+    int64_t c_r0, x_r0;    // C rows start, X rows start
+    int64_t col0;          // first column
+    const int *dblk;       // per-column exponent delta (nullable)
+};
+
+// Tile geometry.  Complex: CTA 64 (rows) x 64 (cols), warp 32x32, BK = 16.
+//                 Real:    CTA 128 x 64, warp 64x32, BK = 16.
+template <typename T> struct GemmCfg;
+template <> struct GemmCfg<cplx> { static constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32; };
+template <> struct GemmCfg<double> { static constexpr int BM = 128, BN = 64, BK = 16, WM = 64, WN = 32; };
+constexpr int kGemmStages = 3;
+constexpr int kGemmThreads = 128;
+
+template <typename T>
+__host__ __device__ constexpr int gemm_stage_elems() {
+    return GemmCfg<T>::BM * GemmCfg<T>::BK + GemmCfg<T>::BN * GemmCfg<T>::BK;
+}
+template <typename T>
+__host__ __device__ constexpr int gemm_smem_bytes() {
+    return kGemmStages * gemm_stage_elems<T>() * int(sizeof(T));
+}
+
+// Swizzled smem offsets (in elements).
+//  A, op N ("k-major", m contiguous): element (k, m) of a BK x BM tile.
+//  A, op C and X ("row-major over the BM/BN index", k contiguous): element (r, k) of BMxBK / BNxBK.
+template <typename T>
+__device__ __forceinline__ int offA_kmajor(int k, int mm) {
+    constexpr int BM = GemmCfg<T>::BM;
+    if (S<T>::cplx_) return k * BM + (mm ^ ((k & 3) << 1));      // 16-B elements: 8 per 128 B
+    else return k * BM + (mm ^ ((k & 3) << 2));                  // 8-B elements: 16 per 128 B
+}
+template <typename T>
+__device__ __forceinline__ int offRK(int r, int k) {
+    constexpr int BK = GemmCfg<T>::BK;
+    if (S<T>::cplx_) return r * BK + (k ^ ((r & 1) << 2));
+    else return r * BK + (k ^ ((r & 3) << 2));
+}
+
+template <typename T, bool OPC>
+__global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T> g) {
+    constexpr int BM = GemmCfg<T>::BM, BN = GemmCfg<T>::BN, BK = GemmCfg<T>::BK;
+    constexpr int WM = GemmCfg<T>::WM, WN = GemmCfg<T>::WN;
+    constexpr int MI = WM / 8, NI = WN / 8;
+    constexpr bool CPX = S<T>::cplx_;
+    constexpr int ESZ = sizeof(T);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *smem = reinterpret_cast<T *>(smem_raw);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int64_t m0 = int64_t(blockIdx.x) * BM;
+    const int64_t n0 = int64_t(blockIdx.y) * BN;
+    const int nk = (g.K + BK - 1) / BK;
+
+    auto stageA = [&](int s) { return smem + s * gemm_stage_elems<T>(); };
+    auto stageX = [&](int s) { return smem + s * gemm_stage_elems<T>() + BM * BK; };
+
+    auto load_stage = [&](int s, int kt) {
+        T *As = stageA(s), *Xs = stageX(s);
+        const int k0 = kt * BK;
+        // A tile
+        if (!OPC) {
+            // BK columns of U, BM contiguous rows each
+#pragma unroll
+            for (int it = 0; it < (BM * BK) / kGemmThreads; it++) {
+                int idx = it * kGemmThreads + tid;
+                int mm = idx % BM, k = idx / BM;
+                int64_t gi = m0 + mm;
+                int gk = k0 + k;
+                bool v = gi < g.M && gk < g.K;
+                const T *src = g.U + (v ? (g.a_r0 + gi) + (g.a_c0 + gk) * g.ldu : 0);
+                cp_async<ESZ>(As + offA_kmajor<T>(k, mm), src, v);
+            }
+        } else {
+            // A(i,k) = conj(U(a_r0+k, a_c0+i)): BM columns of U, BK contiguous rows each
+#pragma unroll
+            for (int it = 0; it < (BM * BK) / kGemmThreads; it++) {
+                int idx = it * kGemmThreads + tid;
+                int k = idx % BK, mm = idx / BK;
+                int64_t gi = m0 + mm;
+                int gk = k0 + k;
+                bool v = gi < g.M && gk < g.K;
+                const T *src = g.U + (v ? (g.a_r0 + gk) + (g.a_c0 + gi) * g.ldu : 0);
+                cp_async<ESZ>(As + offRK<T>(mm, k), src, v);
+            }
+        }
+        // X tile: BN columns of B, BK contiguous rows each
+#pragma unroll
+        for (int it = 0; it < (BN * BK) / kGemmThreads; it++) {
+            int idx = it * kGemmThreads + tid;
+            int k = idx % BK, nn = idx / BK;
+            int64_t gj = n0 + nn;
+            int gk = k0 + k;
+            bool v = gj < g.N && gk < g.K;
+            const T *src = g.B + (v ? (g.x_r0 + gk) + (g.col0 + gj) * g.ldb : 0);
+            cp_async<ESZ>(Xs + offRK<T>(nn, k), src, v);
+        }
+    };
+
+    // accumulators: real part (and imaginary part for complex), 2 doubles per 8x8 sub-tile
+    double accR[MI][NI][2], accI[CPX ? MI : 1][CPX ? NI : 1][2];
+#pragma unroll
+    for (int i = 0; i < MI; i++)
+#pragma unroll
+        for (int jn = 0; jn < NI; jn++) {
+            accR[i][jn][0] = accR[i][jn][1] = 0.0;
+            if (CPX) accI[CPX ? i : 0][CPX ? jn : 0][0] = accI[CPX ? i : 0][CPX ? jn : 0][1] = 0.0;
+        }
+
+#pragma unroll
+    for (int s = 0; s < kGemmStages - 1; s++) {
+        if (s < nk) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    for (int kt = 0; kt < nk; kt++) {
+        cp_async_wait<kGemmStages - 2>();
+        __syncthreads();
+        {
+            int nxt = kt + kGemmStages - 1;
+            if (nxt < nk) load_stage(nxt % kGemmStages, nxt);
+            cp_async_commit();
+        }
+        const T *As = stageA(kt % kGemmStages);
+        const T *Xs = stageX(kt % kGemmStages);
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; kk++) {
+            const int k = kk * 4 + tq;
+            double ar[MI], ai[MI], br[NI], bi[NI];
+#pragma unroll
+            for (int i = 0; i < MI; i++) {
+                int mm = wm * WM + i * 8 + gq;
+                T v = OPC ? As[offRK<T>(mm, k)] : As[offA_kmajor<T>(k, mm)];
+                if constexpr (CPX) { ar[i] = v.x; ai[i] = OPC ? -v.y : v.y; }
+                else { ar[i] = v; ai[i] = 0.0; }
+            }
+#pragma unroll
+            for (int jn = 0; jn < NI; jn++) {
+                int nn = wn * WN + jn * 8 + gq;
+                T v = Xs[offRK<T>(nn, k)];
+                if constexpr (CPX) { br[jn] = v.x; bi[jn] = v.y; }
+                else { br[jn] = v; bi[jn] = 0.0; }
+            }
+#pragma unroll
+            for (int i = 0; i < MI; i++) {
+                double nai = -ai[i];
+#pragma unroll
+                for (int jn = 0; jn < NI; jn++) {
+                    dmma(accR[i][jn][0], accR[i][jn][1], ar[i], br[jn]);
+                    if constexpr (CPX) {
+                        dmma(accR[i][jn][0], accR[i][jn][1], nai, bi[jn]);
+                        dmma(accI[i][jn][0], accI[i][jn][1], ar[i], bi[jn]);
+                        dmma(accI[i][jn][0], accI[i][jn][1], ai[i], br[jn]);
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+
+    // ---- epilogue: C = 2^d C - acc ----
+#pragma unroll
+    for (int jn = 0; jn < NI; jn++) {
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            int64_t gj = n0 + wn * WN + jn * 8 + tq * 2 + c;
+            if (gj >= g.N) continue;
+            int d = g.dblk ? g.dblk[g.col0 + gj] : 0;
+            double sc = d >= -1022 ? ldexp(1.0, d) : 0.0;
+            T *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
+#pragma unroll
+            for (int i = 0; i < MI; i++) {
+                int64_t gi = m0 + wm * WM + i * 8 + gq;
+                if (gi >= g.M) continue;
+                T old = colp[gi];
+                T nv;
+                if constexpr (CPX) {
+                    if (d == 0) { nv.x = old.x - accR[i][jn][c]; nv.y = old.y - accI[i][jn][c]; }
+                    else if (d >= -1022) { nv.x = fma(old.x, sc, -accR[i][jn][c]); nv.y = fma(old.y, sc, -accI[i][jn][c]); }
+                    else { nv.x = ldexp(old.x, d) - accR[i][jn][c]; nv.y = ldexp(old.y, d) - accI[i][jn][c]; }
+                } else {
+                    if (d == 0) nv = old - accR[i][jn][c];
+                    else if (d >= -1022) nv = fma(old, sc, -accR[i][jn][c]);
+                    else nv = ldexp(old, d) - accR[i][jn][c];
+                }
+                colp[gi] = nv;
+            }
+        }
+    }
+}
+
+}  // namespace mstrsm

@@ -1,0 +1,649 @@
+// mstrsm.cu -- libmstrsm.so: C ABI (include/mstrsm.h) + host orchestration of the blocked
+// (safe) multi-shift triangular solve (arXiv 1607.01477, Alg. 3 / Alg. 5) on sm_100a.
+//
+// Per solve, all on the library stream, no host synchronisation:
+//   a.2 norm pass (safe)            norm_cols_n / norm_rows_c, panel_sum, rowsum, delta
+//   a.1 init                        init_rhs / init_trevc
+//   for every block b (op N bottom-up, op C top-down; P:162-180 / P:362-411):
+//     a.3+a.4 diag_kernel           per-column diagonal-block solve, bounds, rescale decision
+//     a.5     gemm_update_kernel    B(I0,act) = 2^d B(I0,act) - U(I0,I1) X(I1,act)  (DMMA)
+//   a.6 finalize                    lazy exponent fix-up, scales, diag(Z)
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "../../include/mstrsm.h"
+#include "aux_kernels.cuh"
+#include "diag_kernel.cuh"
+#include "gemm_kernel.cuh"
+#include "lanczos_kernels.cuh"
+
+using namespace mstrsm;
+
+namespace {
+
+cudaStream_t g_stream = nullptr;
+std::atomic<int64_t> g_launches{0};
+int *g_flag = nullptr;                 // device: non-finite input seen
+char g_errmsg[512] = "no error";
+int g_num_sms = 0;
+std::mutex g_mu;
+
+int set_cuda_error(cudaError_t e, const char *where) {
+    snprintf(g_errmsg, sizeof(g_errmsg), "CUDA error in %s: %s", where, cudaGetErrorString(e));
+    return 1;
+}
+
+#define CK(call)                                               \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return set_cuda_error(e_, #call); \
+    } while (0)
+#define CK_LAUNCH(name)                                        \
+    do {                                                       \
+        g_launches.fetch_add(1, std::memory_order_relaxed);    \
+        cudaError_t e_ = cudaGetLastError();                   \
+        if (e_ != cudaSuccess) return set_cuda_error(e_, name); \
+    } while (0)
+
+int ensure_init() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_flag) return 0;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaMalloc(&g_flag, sizeof(int)));
+    CK(cudaMemset(g_flag, 0, sizeof(int)));
+    return 0;
+}
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- live kernel profiling
+// When enabled (mstrsm_profile(1)), every launch is bracketed by CUDA events recorded on the
+// launching stream; mstrsm_profile_read sums the elapsed times per kernel kind.
+enum { PK_GEMM = 0, PK_DIAG = 1, PK_OTHER = 2, PK_N = 3 };
+struct ProfRec { int kind; cudaEvent_t e0, e1; double flops; };
+bool g_prof = false;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_ev_pool;
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+struct ProfScope {
+    ProfRec r{};
+    bool on;
+    ProfScope(int kind, double flops) : on(g_prof) {
+        if (!on) return;
+        r.kind = kind; r.flops = flops; r.e0 = ev_get(); r.e1 = ev_get();
+        cudaEventRecord(r.e0, g_stream);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(r.e1, g_stream);
+        g_prof_recs.push_back(r);
+    }
+};
+
+// Device workspace for one solve, carved out of one stream-ordered allocation.
+struct Work {
+    void *base = nullptr;
+    double *cnl = nullptr, *part = nullptr, *P = nullptr, *delta = nullptr, *G = nullptr;
+    int *e = nullptr, *dblk = nullptr, *Etab = nullptr;
+    int64_t *rowend = nullptr;
+    void *shifts = nullptr;            // trevc: gathered diag(T)
+    cudaStream_t st = nullptr;
+    ~Work() { if (base) cudaFreeAsync(base, st); }
+};
+
+template <typename T>
+int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool need_shifts) {
+    int64_t nblk = cdiv(m, nb);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    size_t o_cnl = take(m * 8), o_part = take(m * 8), o_P = take(std::max<int64_t>(nblk, 1) * 8),
+           o_delta = take(8), o_G = take(n * 8), o_e = take(n * 4), o_d = take(n * 4),
+           o_E = take(std::max<int64_t>(nblk, 1) * n * 4), o_r = take(need_rowend ? n * 8 : 0),
+           o_s = take(need_shifts ? n * sizeof(T) : 0);
+    w.st = g_stream;
+    CK(cudaMallocAsync(&w.base, off, g_stream));
+    char *b = static_cast<char *>(w.base);
+    w.cnl = (double *)(b + o_cnl); w.part = (double *)(b + o_part); w.P = (double *)(b + o_P);
+    w.delta = (double *)(b + o_delta); w.G = (double *)(b + o_G); w.e = (int *)(b + o_e);
+    w.dblk = (int *)(b + o_d); w.Etab = (int *)(b + o_E);
+    w.rowend = need_rowend ? (int64_t *)(b + o_r) : nullptr;
+    w.shifts = need_shifts ? (void *)(b + o_s) : nullptr;
+    return 0;
+}
+
+template <typename K>
+int occupancy(K kern, int threads, size_t smem) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess) nb = 1;
+    return std::max(nb, 1);
+}
+
+// ---------------------------------------------------------------- norm pass (a.2)
+template <typename T>
+int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w) {
+    int64_t nblk = cdiv(m, nb);
+    if (op == 0) {
+        int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
+        norm_cols_n_kernel<T><<<blocks, 256, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
+        CK_LAUNCH("norm_cols_n_kernel");
+        panel_sum_kernel<<<int(cdiv(nblk, 128)), 128, 0, g_stream>>>(0, m, nb, nblk, w.part, w.P);
+        CK_LAUNCH("panel_sum_kernel");
+        rowsum_n_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, w.part);
+        CK_LAUNCH("rowsum_n_kernel");
+    } else {
+        norm_rows_c_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
+        CK_LAUNCH("norm_rows_c_kernel");
+        panel_sum_kernel<<<int(cdiv(nblk, 128)), 128, 0, g_stream>>>(1, m, nb, nblk, w.part, w.P);
+        CK_LAUNCH("panel_sum_kernel");
+        colsum_c_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, w.part);
+        CK_LAUNCH("colsum_c_kernel");
+    }
+    delta_kernel<<<1, 1024, 0, g_stream>>>(m, w.part, w.delta);
+    CK_LAUNCH("delta_kernel");
+    return 0;
+}
+
+// ---------------------------------------------------------------- diag launch (a.3/a.4)
+template <typename T, int RPL, bool SAFE, int OP>
+int launch_diag_t(const DiagArgs<T> &a) {
+    auto kern = diag_kernel<T, RPL, SAFE, OP>;
+    int nfull = int(a.hi - a.lo);
+    size_t smem = size_t(diag_smem_bytes(RPL * 32 >= nfull ? nfull : nfull, sizeof(T)));
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    int threads = smem > 96 * 1024 ? 512 : 256;
+    int occ = occupancy(kern, threads, smem);
+    int64_t warps = threads / 32;
+    int grid = int(std::min<int64_t>(cdiv(a.ncols, warps), int64_t(occ) * g_num_sms));
+    if (grid < 1) grid = 1;
+    double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
+    ProfScope ps(PK_DIAG, fl);
+    kern<<<grid, threads, smem, g_stream>>>(a);
+    CK_LAUNCH("diag_kernel");
+    return 0;
+}
+
+template <typename T, bool SAFE, int OP>
+int launch_diag(const DiagArgs<T> &a, int nb) {
+    if (nb <= 32) return launch_diag_t<T, 1, SAFE, OP>(a);
+    if (nb <= 64) return launch_diag_t<T, 2, SAFE, OP>(a);
+    return launch_diag_t<T, 4, SAFE, OP>(a);
+}
+
+// ---------------------------------------------------------------- GEMM launch (a.5)
+template <typename T, bool OPC>
+int launch_gemm(const GemmArgs<T> &g) {
+    auto kern = gemm_update_kernel<T, OPC>;
+    static bool attr_set = false;
+    constexpr int smem = gemm_smem_bytes<T>();
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_set = true;
+    }
+    dim3 grid(unsigned(cdiv(g.M, GemmCfg<T>::BM)), unsigned(cdiv(g.N, GemmCfg<T>::BN)));
+    ProfScope ps(PK_GEMM, double(g.M) * g.N * g.K * (S<T>::cplx_ ? 8.0 : 2.0));
+    kern<<<grid, kGemmThreads, smem, g_stream>>>(g);
+    CK_LAUNCH("gemm_update_kernel");
+    return 0;
+}
+
+// ---------------------------------------------------------------- the blocked solve
+// State (G, e) must be initialised by the caller (init kernels).  active_from(b) gives the first
+// active column of block b when row ends are known on the host and sorted.
+template <typename T, bool SAFE>
+int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride,
+                  T *B, int64_t ldb, int64_t n, const int64_t *rowend_dev,
+                  const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w) {
+    int64_t nblk = cdiv(m, nb);
+    for (int64_t b = 0; b < nblk; b++) {
+        Blk bl = block_rows(op, m, nb, b);
+        int64_t c0 = 0;
+        if (op == 0 && rowend_sorted_host) {
+            const auto &re = *rowend_sorted_host;
+            c0 = std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();   // first r > lo
+        }
+        int64_t ncols = n - c0;
+        if (ncols <= 0) continue;
+        DiagArgs<T> a;
+        a.U = U; a.ldu = ldu; a.m = m; a.shifts = shifts; a.sstride = sstride;
+        a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
+        a.rowend = op == 0 ? rowend_dev : nullptr;
+        a.lo = bl.lo; a.hi = bl.hi; a.b = b;
+        a.cnl = w.cnl; a.P = w.P; a.delta = w.delta;
+        a.G = w.G; a.e = w.e; a.dblk = w.dblk; a.Etab = w.Etab;
+        int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
+        if (rc) return rc;
+        int64_t M = op == 0 ? bl.lo : m - bl.hi;
+        if (M <= 0) continue;
+        GemmArgs<T> g;
+        g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
+        g.M = M; g.N = ncols; g.K = int(bl.hi - bl.lo);
+        if (op == 0) { g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0; }
+        else { g.a_r0 = bl.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
+        g.x_r0 = bl.lo; g.col0 = c0;
+        g.dblk = SAFE ? w.dblk : nullptr;
+        rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+template <typename T>
+int finalize(int op, int safe, T *B, int64_t ldb, int64_t m, int64_t n, int nb,
+             const int64_t *rowend_dev, double *scales, int *scale_exp, const int64_t *diag_row,
+             Work &w) {
+    int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
+    if (blocks < 1) blocks = 1;
+    finalize_kernel<T><<<blocks, 256, 0, g_stream>>>(op, B, ldb, m, n, nb, cdiv(m, nb), rowend_dev,
+                                                      safe ? w.e : nullptr, safe ? w.Etab : nullptr,
+                                                      scales, scale_exp, diag_row);
+    CK_LAUNCH("finalize_kernel");
+    return 0;
+}
+
+bool is_sorted_nondecreasing(const int64_t *v, int64_t n) {
+    for (int64_t i = 1; i < n; i++)
+        if (v[i] < v[i - 1]) return false;
+    return true;
+}
+
+template <typename T>
+int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *shifts,
+                   int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                   double *scales, int32_t *scale_exp, int nb) {
+    if (safe != 0 && safe != 1) return -1;
+    if (op != 0 && op != 1) return -2;
+    if (m < 0) return -5;
+    if (ldu < std::max<int64_t>(1, m)) return -4;
+    if (sstride < 0) return -7;
+    if (ldb < std::max<int64_t>(1, m)) return -9;
+    if (n < 0) return -10;
+    if (nb == 0) nb = 64;
+    if (nb < 1 || nb > 128) return -14;
+    if (op == 1 && row_end_host) return -11;
+    if (m == 0 || n == 0) return 0;
+    if (!U) return -3;
+    if (!shifts) return -6;
+    if (!B) return -8;
+    if (safe && !scales) return -12;
+    if (int rc = ensure_init()) return rc;
+
+    Work w;
+    if (int rc = alloc_work<T>(w, m, n, nb, row_end_host != nullptr, false)) return rc;
+    std::vector<int64_t> re_host;
+    bool sorted = false;
+    if (row_end_host) {
+        re_host.assign(row_end_host, row_end_host + n);
+        for (auto &v : re_host) v = v < 0 ? 0 : (v > m ? m : v);
+        sorted = is_sorted_nondecreasing(re_host.data(), n);
+        CK(cudaMemcpyAsync(w.rowend, re_host.data(), n * 8, cudaMemcpyHostToDevice, g_stream));
+    }
+    int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
+    if (safe) {
+        if (int rc = norm_pass<T>(op, U, ldu, m, nb, w)) return rc;
+        init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, shifts, sstride, w.G, w.e, g_flag);
+        CK_LAUNCH("init_rhs_kernel");
+        int rc = blocked_solve<T, true>(op, U, ldu, m, shifts, sstride, B, ldb, n, w.rowend,
+                                        sorted ? &re_host : nullptr, nb, w);
+        if (rc) return rc;
+    } else {
+        if (w.rowend) {
+            init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, nullptr, 0, nullptr, nullptr, nullptr);
+            CK_LAUNCH("init_rhs_kernel");
+        }
+        int rc = blocked_solve<T, false>(op, U, ldu, m, shifts, sstride, B, ldb, n, w.rowend,
+                                         sorted ? &re_host : nullptr, nb, w);
+        if (rc) return rc;
+    }
+    if (scales || scale_exp || safe)
+        if (int rc = finalize<T>(op, safe, B, ldb, m, n, nb, w.rowend, scales, scale_exp, nullptr, w)) return rc;
+    return 0;
+}
+
+template <typename T>
+int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
+               T *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
+    if (m < 0) return -3;
+    if (ldt < std::max<int64_t>(1, m)) return -2;
+    if (ncols < 0) return -5;
+    if (ldz < std::max<int64_t>(1, m)) return -7;
+    if (nb == 0) nb = 64;
+    if (nb < 1 || nb > 128) return -10;
+    if (m == 0 || ncols == 0) return 0;
+    if (!Tm) return -1;
+    if (!Z) return -6;
+    std::vector<int64_t> cols(ncols);
+    for (int64_t q = 0; q < ncols; q++) {
+        cols[q] = cols_host ? cols_host[q] : q;
+        if (cols[q] < 0 || cols[q] >= m || (q > 0 && cols[q] <= cols[q - 1])) return -4;
+    }
+    if (int rc = ensure_init()) return rc;
+    Work w;
+    if (int rc = alloc_work<T>(w, m, ncols, nb, true, true)) return rc;
+    int64_t *cols_dev = nullptr;
+    if (cols_host) {
+        CK(cudaMallocAsync(&cols_dev, ncols * 8, g_stream));
+        CK(cudaMemcpyAsync(cols_dev, cols.data(), ncols * 8, cudaMemcpyHostToDevice, g_stream));
+    }
+    T *sh = static_cast<T *>(w.shifts);
+    if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w)) return rc;
+    int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
+    init_trevc_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, cols_dev, ncols, Z, ldz, sh,
+                                                        w.rowend, w.G, w.e, g_flag);
+    CK_LAUNCH("init_trevc_kernel");
+    // row_end_q = cols[q] (the P:503-508 shortcut), sorted ascending
+    int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w);
+    if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
+    if (cols_dev) cudaFreeAsync(cols_dev, g_stream);
+    return rc;
+}
+
+// ---------------------------------------------------------------- pseudospectra driver (a.7)
+int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int64_t npts, int iters,
+                       const cplx *v0, double *sigma, int32_t *flags, int nb) {
+    if (m < 0) return -3;
+    if (ldu < std::max<int64_t>(1, m)) return -2;
+    if (npts < 0) return -5;
+    if (iters < 1) return -6;
+    if (nb == 0) nb = 64;
+    if (nb < 1 || nb > 128) return -10;
+    if (m == 0 || npts == 0) return 0;
+    if (!U) return -1;
+    if (!z) return -4;
+    if (!v0) return -7;
+    if (!sigma) return -8;
+    if (int rc = ensure_init()) return rc;
+    Work wN, wC;
+    if (int rc = alloc_work<cplx>(wN, m, npts, nb, false, false)) return rc;
+    if (int rc = alloc_work<cplx>(wC, m, npts, nb, false, false)) return rc;
+    if (int rc = norm_pass<cplx>(0, U, ldu, m, nb, wN)) return rc;
+    if (int rc = norm_pass<cplx>(1, U, ldu, m, nb, wC)) return rc;
+    size_t vec = size_t(m) * npts * sizeof(cplx);
+    size_t small = size_t(npts) * 8;
+    size_t total = 4 * vec + 2 * size_t(iters) * small + 8 * small + 1024;
+    char *buf = nullptr;
+    CK(cudaMallocAsync(&buf, total, g_stream));
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char *p = buf + off; off += (bytes + 255) & ~size_t(255); return p; };
+    LanczosState st;
+    st.V = (cplx *)take(vec); st.Vp = (cplx *)take(vec); st.W = (cplx *)take(vec); st.Y = (cplx *)take(vec);
+    st.alpha = (double *)take(iters * small); st.beta = (double *)take(iters * small);
+    st.kdone = (int *)take(npts * 4); st.active = (int *)take(npts * 4);
+    st.flags = flags ? (int *)flags : (int *)take(npts * 4);
+    st.amax = (double *)take(small); st.beta_prev = (double *)take(small); st.sigma = sigma;
+    int *e1 = (int *)take(npts * 4), *e2 = (int *)take(npts * 4);
+    st.e1 = e1; st.e2 = e2;
+    int blocks = int(std::min<int64_t>(cdiv(npts, 8), int64_t(g_num_sms) * 16));
+    if (blocks < 1) blocks = 1;
+    lanczos_init_kernel<<<blocks, 256, 0, g_stream>>>(v0, st, m, npts);
+    CK_LAUNCH("lanczos_init_kernel");
+    int rc = 0;
+    for (int it = 0; it < iters && !rc; it++) {
+        copy_cols_kernel<<<blocks, 256, 0, g_stream>>>(st.V, st.Y, m, npts);
+        CK_LAUNCH("copy_cols_kernel");
+        init_rhs_kernel<cplx><<<blocks, 256, 0, g_stream>>>(st.Y, m, m, npts, nullptr, z, 1, wN.G, wN.e, g_flag);
+        CK_LAUNCH("init_rhs_kernel");
+        rc = blocked_solve<cplx, true>(0, U, ldu, m, z, 1, st.Y, m, npts, nullptr, nullptr, nb, wN);
+        if (!rc) rc = finalize<cplx>(0, 1, st.Y, m, m, npts, nb, nullptr, nullptr, e1, nullptr, wN);
+        if (rc) break;
+        copy_cols_kernel<<<blocks, 256, 0, g_stream>>>(st.Y, st.W, m, npts);
+        CK_LAUNCH("copy_cols_kernel");
+        init_rhs_kernel<cplx><<<blocks, 256, 0, g_stream>>>(st.W, m, m, npts, nullptr, nullptr, 0, wC.G, wC.e, nullptr);
+        CK_LAUNCH("init_rhs_kernel");
+        rc = blocked_solve<cplx, true>(1, U, ldu, m, z, 1, st.W, m, npts, nullptr, nullptr, nb, wC);
+        if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, npts, nb, nullptr, nullptr, e2, nullptr, wC);
+        if (rc) break;
+        lanczos_step_kernel<<<blocks, 256, 0, g_stream>>>(st, m, npts, it, iters);
+        CK_LAUNCH("lanczos_step_kernel");
+    }
+    if (!rc) {
+        bisect_sigma_kernel<<<int(cdiv(npts, 128)), 128, 0, g_stream>>>(st, npts);
+        CK_LAUNCH("bisect_sigma_kernel");
+    }
+    cudaFreeAsync(buf, g_stream);
+    return rc;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+// Map an invalid-argument position of mstrsm_*_ex to the short prototypes
+// (U, ldu, m, shifts, B, ldb, n, scales, nb).
+static int short_pos(int rc) {
+    if (rc >= 0) return rc;
+    switch (-rc) {
+        case 3: return -1; case 4: return -2; case 5: return -3; case 6: return -4; case 8: return -5;
+        case 9: return -6; case 10: return -7; case 12: return -8; case 14: return -9; default: return rc;
+    }
+}
+
+extern "C" {
+
+int mstrsm_d(const double *U, int64_t ldu, int64_t m, const double *shifts, double *B, int64_t ldb,
+             int64_t n, double *scales, int nb) {
+    return short_pos(mstrsm_ex_impl<double>(0, 0, U, ldu, m, shifts, 1, B, ldb, n, nullptr, scales, nullptr, nb));
+}
+int mstrsm_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts, mstrsm_dcomplex *B,
+             int64_t ldb, int64_t n, double *scales, int nb) {
+    return short_pos(mstrsm_ex_impl<cplx>(0, 0, (const cplx *)U, ldu, m, (const cplx *)shifts, 1, (cplx *)B, ldb, n,
+                                nullptr, scales, nullptr, nb));
+}
+int mstrsm_d_safe(const double *U, int64_t ldu, int64_t m, const double *shifts, double *B,
+                  int64_t ldb, int64_t n, double *scales, int nb) {
+    return short_pos(mstrsm_ex_impl<double>(1, 0, U, ldu, m, shifts, 1, B, ldb, n, nullptr, scales, nullptr, nb));
+}
+int mstrsm_z_safe(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts, mstrsm_dcomplex *B,
+                  int64_t ldb, int64_t n, double *scales, int nb) {
+    return short_pos(mstrsm_ex_impl<cplx>(1, 0, (const cplx *)U, ldu, m, (const cplx *)shifts, 1, (cplx *)B, ldb, n,
+                                nullptr, scales, nullptr, nb));
+}
+int mstrsm_d_ex(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
+                int64_t shift_stride, double *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                double *scales, int32_t *scale_exp, int nb) {
+    return mstrsm_ex_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host,
+                                  scales, scale_exp, nb);
+}
+int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts,
+                int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                double *scales, int32_t *scale_exp, int nb) {
+    return mstrsm_ex_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride,
+                                (cplx *)B, ldb, n, row_end_host, scales, scale_exp, nb);
+}
+
+int trevc_d(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,
+            int32_t *scale_exp, int nb) {
+    int rc = trevc_impl<double>(T, ldt, m, nullptr, m, Z, ldz, scales, scale_exp, nb);
+    return rc < 0 ? (rc == -4 ? -1 : (rc <= -6 ? rc + 2 : rc)) : rc;
+}
+int trevc_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, mstrsm_dcomplex *Z, int64_t ldz, double *scales,
+            int32_t *scale_exp, int nb) {
+    int rc = trevc_impl<cplx>((const cplx *)T, ldt, m, nullptr, m, (cplx *)Z, ldz, scales, scale_exp, nb);
+    return rc < 0 ? (rc == -4 ? -1 : (rc <= -6 ? rc + 2 : rc)) : rc;
+}
+int trevc_d_cols(const double *T, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
+                 double *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
+    return trevc_impl<double>(T, ldt, m, cols_host, ncols, Z, ldz, scales, scale_exp, nb);
+}
+int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
+                 mstrsm_dcomplex *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
+    return trevc_impl<cplx>((const cplx *)T, ldt, m, cols_host, ncols, (cplx *)Z, ldz, scales, scale_exp, nb);
+}
+
+int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *Z_host, int64_t ldz,
+                 double *scales_host, int32_t *scale_exp_host, int nb) {
+    if (m < 0) return -3;
+    if (ldt < std::max<int64_t>(1, m)) return -2;
+    if (ldz < std::max<int64_t>(1, m)) return -5;
+    if (m == 0) return 0;
+    if (!T_host) return -1;
+    if (!Z_host) return -4;
+    if (int rc = ensure_init()) return rc;
+    cplx *dT = nullptr, *dZ = nullptr;
+    double *ds = nullptr;
+    int *de = nullptr;
+    size_t bytes = size_t(m) * m * sizeof(cplx);
+    CK(cudaMallocAsync(&dT, bytes, g_stream));
+    CK(cudaMallocAsync(&dZ, bytes, g_stream));
+    CK(cudaMallocAsync(&ds, m * 8, g_stream));
+    CK(cudaMallocAsync(&de, m * 4, g_stream));
+    if (ldt == m) CK(cudaMemcpyAsync(dT, T_host, bytes, cudaMemcpyHostToDevice, g_stream));
+    else CK(cudaMemcpy2DAsync(dT, m * sizeof(cplx), T_host, ldt * sizeof(cplx), m * sizeof(cplx), m,
+                              cudaMemcpyHostToDevice, g_stream));
+    int rc = trevc_impl<cplx>(dT, m, m, nullptr, m, dZ, m, ds, de, nb);
+    if (rc == 0) {
+        if (ldz == m) CK(cudaMemcpyAsync(Z_host, dZ, bytes, cudaMemcpyDeviceToHost, g_stream));
+        else CK(cudaMemcpy2DAsync(Z_host, ldz * sizeof(cplx), dZ, m * sizeof(cplx), m * sizeof(cplx), m,
+                                  cudaMemcpyDeviceToHost, g_stream));
+        if (scales_host) CK(cudaMemcpyAsync(scales_host, ds, m * 8, cudaMemcpyDeviceToHost, g_stream));
+        if (scale_exp_host) CK(cudaMemcpyAsync(scale_exp_host, de, m * 4, cudaMemcpyDeviceToHost, g_stream));
+    }
+    cudaFreeAsync(dT, g_stream);
+    cudaFreeAsync(dZ, g_stream);
+    cudaFreeAsync(ds, g_stream);
+    cudaFreeAsync(de, g_stream);
+    CK(cudaStreamSynchronize(g_stream));
+    return rc;
+}
+
+int pseudospectra_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z, int64_t npts, int iters,
+                    const mstrsm_dcomplex *v0, double *sigma_min, int32_t *flags, int nb) {
+    return pseudospectra_impl((const cplx *)U, ldu, m, (const cplx *)z, npts, iters, (const cplx *)v0,
+                              sigma_min, flags, nb);
+}
+
+int mstrsm_set_stream(void *s) {
+    g_stream = static_cast<cudaStream_t>(s);
+    return 0;
+}
+void *mstrsm_get_stream(void) { return g_stream; }
+
+const char *mstrsm_error_string(int code) {
+    switch (code) {
+        case 0: return "success";
+        case 1: return g_errmsg;
+        case 2: return "non-finite entry in U or the shifts";
+        case 3: return "communication error";
+        default: return code < 0 ? "invalid argument" : "unknown error";
+    }
+}
+
+int mstrsm_status(void) {
+    if (int rc = ensure_init()) return rc;
+    CK(cudaStreamSynchronize(g_stream));
+    int h = 0;
+    CK(cudaMemcpy(&h, g_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(g_flag, 0, sizeof(int)));
+    return h ? 2 : 0;
+}
+
+int64_t mstrsm_launch_count(int reset) {
+    return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+int mstrsm_profile(int enable) {
+    for (auto &r : g_prof_recs) { g_ev_pool.push_back(r.e0); g_ev_pool.push_back(r.e1); }
+    g_prof_recs.clear();
+    g_prof = enable != 0;
+    return 0;
+}
+
+int mstrsm_profile_read(int kind, double *total_ms, int64_t *launches, double *flops) {
+    CK(cudaStreamSynchronize(g_stream));
+    double t = 0.0, f = 0.0;
+    int64_t c = 0;
+    for (auto &r : g_prof_recs) {
+        if (r.kind != kind) continue;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.e0, r.e1));
+        t += ms; f += r.flops; c++;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = c;
+    if (flops) *flops = f;
+    return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- FP64 roofline probe
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double *out, int iters, double seed) {
+    double a = seed * (threadIdx.x + 1), b = 1.0 - seed * threadIdx.x;
+    double c[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; q++) c[q][0] = c[q][1] = 0.0;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) dmma(c[q][0], c[q][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) s += c[q][0] + c[q][1];
+    if (s == 1234.5) out[0] = s;
+}
+
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double *out, int iters, double seed) {
+    double a = 1.0 - seed, b = seed * threadIdx.x;
+    double c[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) c[q] = q * seed;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) c[q] = fma(c[q], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) s += c[q];
+    if (s == 1234.5) out[0] = s;
+}
+
+extern "C" int mstrsm_fp64_peak(double ms, double *dmma_tflops, double *dfma_tflops) {
+    if (int rc = ensure_init()) return rc;
+    double *out = nullptr;
+    CK(cudaMalloc(&out, 8));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = g_num_sms * 8, threads = 256;
+    for (int which = 0; which < 2; which++) {
+        int iters = 1000;
+        double tf = 0.0;
+        for (int rep = 0; rep < 6; rep++) {
+            CK(cudaEventRecord(e0, g_stream));
+            if (which == 0) dmma_peak_kernel<<<blocks, threads, 0, g_stream>>>(out, iters, 1e-3);
+            else dfma_peak_kernel<<<blocks, threads, 0, g_stream>>>(out, iters, 1e-3);
+            CK_LAUNCH("fp64_peak_kernel");
+            CK(cudaEventRecord(e1, g_stream));
+            CK(cudaEventSynchronize(e1));
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, e0, e1));
+            double flops = which == 0 ? double(blocks) * (threads / 32) * iters * 8.0 * 512.0
+                                      : double(blocks) * threads * iters * 8.0 * 2.0;
+            if (rep >= 2) tf = std::max(tf, flops / (t * 1e-3) / 1e12);
+            if (t > 0.f && t < ms) iters = int(std::min(1e9, iters * (ms / t)));
+        }
+        if (which == 0 && dmma_tflops) *dmma_tflops = tf;
+        if (which == 1 && dfma_tflops) *dfma_tflops = tf;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return 0;
+}

@@ -1,0 +1,99 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol that
+include/mstrsm.h declares, and rejects invalid arguments (LAPACK INFO style, -i) or returns 0 for
+empty problems before touching CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1607_01477_b200 as ms
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mstrsm.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\**\s*([A-Za-z_][A-Za-z0-9_]*)\s*\(",
+                       src, flags=re.M)
+    return sorted(set(n for n in names if n not in ("if", "while")))
+
+
+def test_header_declares_the_survey_boundary():
+    names = declared_functions()
+    for required in ["mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
+                     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
+                     "mstrsm_set_stream", "mstrsm_get_stream", "mstrsm_error_string", "mstrsm_status",
+                     "mstrsm_launch_count", "mstrsm_fp64_peak"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(ms.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_library_is_sm100a():
+    """The shipped cubin targets sm_100a (cuobjdump lists the ELF arch)."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", ms.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _lib():
+    return ms.load()
+
+
+def test_invalid_arguments_are_rejected_without_cuda():
+    lib = _lib()
+    P = None
+    # mstrsm_d(U, ldu, m, shifts, B, ldb, n, scales, nb)
+    assert lib.mstrsm_d(P, 1, -1, P, P, 1, 1, P, 32) == -3      # m < 0
+    assert lib.mstrsm_d(P, 3, 4, P, P, 4, 1, P, 32) == -2       # ldu < m
+    assert lib.mstrsm_d(P, 4, 4, P, P, 3, 1, P, 32) == -6       # ldb < m
+    assert lib.mstrsm_d(P, 4, 4, P, P, 4, -2, P, 32) == -7      # n < 0
+    assert lib.mstrsm_d(P, 4, 4, P, P, 4, 1, P, 129) == -9      # nb > 128
+    assert lib.mstrsm_d(P, 4, 4, P, P, 4, 1, P, -1) == -9       # nb < 0
+    assert lib.mstrsm_d(P, 4, 4, P, P, 4, 1, P, 0) == -1        # U NULL
+    assert lib.mstrsm_d_safe(ctypes.c_void_p(8), 4, 4, ctypes.c_void_p(8), ctypes.c_void_p(8), 4, 1, P, 32) == -8
+    # mstrsm_z_ex(safe, op, U, ldu, m, shifts, stride, B, ldb, n, row_end, scales, exp, nb)
+    assert lib.mstrsm_z_ex(2, 0, P, 4, 4, P, 1, P, 4, 1, P, P, P, 0) == -1
+    assert lib.mstrsm_z_ex(0, 5, P, 4, 4, P, 1, P, 4, 1, P, P, P, 0) == -2
+    re_ = (ctypes.c_int64 * 1)(3)
+    assert lib.mstrsm_z_ex(0, 1, P, 4, 4, P, 1, P, 4, 1, re_, P, P, 0) == -11   # row_end with op C
+    # trevc_z(T, ldt, m, Z, ldz, scales, exp, nb)
+    assert lib.trevc_z(P, 2, 3, P, 3, P, P, 0) == -2
+    assert lib.trevc_z(P, 3, 3, P, 2, P, P, 0) == -5
+    assert lib.trevc_z(P, 3, 3, P, 3, P, P, 200) == -8
+    # pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma, flags, nb)
+    assert lib.pseudospectra_z(P, 4, 4, P, 1, 0, P, P, P, 0) == -6
+
+
+def test_empty_problems_return_zero_without_cuda():
+    lib = _lib()
+    P = None
+    assert lib.mstrsm_z(P, 1, 0, P, P, 1, 5, P, 0) == 0
+    assert lib.mstrsm_d_safe(P, 4, 4, P, P, 4, 0, P, 0) == 0
+    assert lib.trevc_d(P, 1, 0, P, 1, P, P, 0) == 0
+    assert lib.pseudospectra_z(P, 1, 0, P, 0, 15, P, P, P, 0) == 0
+
+
+def test_error_strings():
+    lib = _lib()
+    assert lib.mstrsm_error_string(0) == b"success"
+    assert b"non-finite" in lib.mstrsm_error_string(2)
+    assert b"invalid" in lib.mstrsm_error_string(-3)
+
+
+def test_no_cpu_fallback_without_cuda():
+    """Calling the product path without a GPU raises; it never computes on the CPU."""
+    import numpy as np
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    U = torch.from_numpy(np.eye(4))
+    with pytest.raises(ms.MstrsmError):
+        ms.solve(U, torch.zeros(1, dtype=torch.float64), torch.ones(4, 1, dtype=torch.float64))
