@@ -1,20 +1,27 @@
 # Builds the product library (sm_100a) and the CPU oracle (test infrastructure).
+#   make -j8        (translation units compile in parallel)
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -shared --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr
 PKG := paper_1607_01477_b200
-SRCS := $(PKG)/csrc/mstrsm.cu
-HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/mstrsm.h
+CSRC := $(PKG)/csrc
+UNITS := mstrsm runtime gemm_launch diag_dN diag_dC diag_zN diag_zC
+OBJS := $(addprefix build/,$(addsuffix .o,$(UNITS)))
+HDRS := $(wildcard $(CSRC)/*.cuh) include/mstrsm.h
 
 all: $(PKG)/libmstrsm.so oracle/liboracle.so
 
-$(PKG)/libmstrsm.so: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -Xptxas -v -o $@ $(SRCS) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+
+$(PKG)/libmstrsm.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 oracle/liboracle.so: oracle/mstrsm_oracle.c oracle/oracle_algo.inc oracle/oracle_scalar.h
 	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread -o $@ oracle/mstrsm_oracle.c -lm
 
 clean:
-	rm -f $(PKG)/libmstrsm.so oracle/liboracle.so
+	rm -rf build $(PKG)/libmstrsm.so oracle/liboracle.so
 
 .PHONY: all clean

@@ -90,16 +90,34 @@ __global__ void panel_sum_kernel(int op, int64_t m, int nb, int64_t nblk,
 // ||U||_inf for delta (R4).  op N: row sums sum_{k >= i} |U(i,k)|, ascending k, one thread per
 // row, warp walks columns in lockstep (coalesced).  op C: column sums sum_{l = i..0} |U(l,i)|
 // (= rows of U^H), descending l, one thread per column.
+constexpr int kRowsumChunk = 256;   // columns per partial sum
+
 template <typename T>
 __global__ void rowsum_n_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
-                                double *__restrict__ rs) {
+                                double *__restrict__ part) {
+    // grid (row blocks of 128, column chunks); partial sum of row i over the chunk's columns
+    // k >= i, ascending k.  A second pass adds the chunks in ascending order (fixed order,
+    // deterministic; differs from a single sequential sum only in rounding, which moves delta
+    // by ulps).
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    int64_t i0 = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
-    if (i0 >= m) return;
+    int64_t i0 = int64_t(blockIdx.x) * blockDim.x;
+    int64_t k0 = int64_t(blockIdx.y) * kRowsumChunk, k1 = k0 + kRowsumChunk < m ? k0 + kRowsumChunk : m;
     double s = 0.0;
-    for (int64_t k = i0; k < m; k++)
-        if (i < m && k >= i) s = __dadd_rn(s, S<T>::mod(U[i + k * ldu]));
-    if (i < m) rs[i] = s;
+    if (k1 > i0) {
+        int64_t kb = k0 > i0 ? k0 : i0;
+        for (int64_t k = kb; k < k1; k++)
+            if (i < m && k >= i) s = __dadd_rn(s, S<T>::mod(U[i + k * ldu]));
+    }
+    if (i < m) part[int64_t(blockIdx.y) * m + i] = s;
+}
+
+__global__ void rowsum_reduce_kernel(int64_t m, int64_t nchunks, const double *__restrict__ part,
+                                     double *__restrict__ rs) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double s = 0.0;
+    for (int64_t c = 0; c < nchunks; c++) s = __dadd_rn(s, part[c * m + i]);
+    rs[i] = s;
 }
 
 template <typename T>

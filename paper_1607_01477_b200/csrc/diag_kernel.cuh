@@ -10,11 +10,14 @@
 // the GEMM epilogue (rows I0, still pending) and E[b][j] = e_j records the frame of the rows
 // finalised here (rows I2 are fixed up once at the end by finalize_kernel).
 //
-// Layout: one warp per column (persistent CTAs loop over columns).  The diagonal block is
-// staged once per CTA in shared memory as a packed strictly-upper triangle in "solve
-// coordinates" sc (op N: sc = row - lo; op C: sc = hi-1-row, the flip of DESIGN §4 / R9), so
-// the same loop serves back substitution (op N) and forward substitution with L = U^H (op C).
-// Lane `lane` owns solve rows sc = rr*32 + lane, rr < RPL.
+// Layout.  A warp holds G = 32/LPC columns; LPC lanes share one column and lane r of a group
+// owns the solve rows sc = r + LPC*t, t < RPL (LPC*RPL >= n_b).  The per-row scalar chain of
+// Alg. 4 (|y_l|, the division, |x_l|, the bound checks) is therefore executed once per group and
+// serves G columns per warp instruction, while the substitution within the block is spread over
+// the LPC lanes.  The diagonal block is staged once per CTA in shared memory as a packed
+// strictly-upper triangle in "solve coordinates" sc (op N: sc = row - lo; op C: sc = hi-1-row,
+// the flip of R9), so one loop serves back substitution (op N) and forward substitution with
+// L = U^H (op C).  Persistent CTAs loop over column groups.
 #pragma once
 #include "common.cuh"
 
@@ -39,9 +42,56 @@ __host__ __device__ inline int64_t diag_smem_bytes(int nfull, int esize) {
     return pk * esize + int64_t(nfull) * esize + int64_t(nfull) * 8;
 }
 
-template <typename T, int RPL, bool SAFE, int OP>
+// 1/d for the division x = y/d, computed once per row and group (Smith's scaling, R7).
+template <typename T> struct Recip;
+template <> struct Recip<double> {
+    double v;
+    __device__ __forceinline__ void make(double d) { v = d; }
+    __device__ __forceinline__ double apply(double y) const { return __ddiv_rn(y, v); }   // exact IEEE division
+};
+template <> struct Recip<cplx> {
+    double r, inv; bool sw;
+    __device__ __forceinline__ void make(cplx d) {
+        sw = fabs(d.y) > fabs(d.x);
+        if (!sw) { r = __ddiv_rn(d.y, d.x); inv = __drcp_rn(__dadd_rn(d.x, __dmul_rn(d.y, r))); }
+        else { r = __ddiv_rn(d.x, d.y); inv = __drcp_rn(__dadd_rn(d.y, __dmul_rn(d.x, r))); }
+    }
+    // Smith's numerators times the rounded reciprocal of the denominator (<= 1.5 ulp from the
+    // oracle's Smith quotient; R24 covers the difference).
+    __device__ __forceinline__ cplx apply(cplx a) const {
+        if (!sw) return make_double2(__dmul_rn(__dadd_rn(a.x, __dmul_rn(a.y, r)), inv),
+                                     __dmul_rn(__dsub_rn(a.y, __dmul_rn(a.x, r)), inv));
+        return make_double2(__dmul_rn(__dadd_rn(__dmul_rn(a.x, r), a.y), inv),
+                            __dmul_rn(__dsub_rn(__dmul_rn(a.y, r), a.x), inv));
+    }
+};
+
+// 2^k as a double for -1022 <= k <= 1023 (exact, built from the exponent bits).
+__device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(1023 + k) << 52); }
+__device__ __forceinline__ double maxabs(double v) { return fabs(v); }
+__device__ __forceinline__ double maxabs(cplx v) { return fmax(fabs(v.x), fabs(v.y)); }
+__device__ __forceinline__ double scale_pw(double v, double p) { return __dmul_rn(v, p); }
+__device__ __forceinline__ cplx scale_pw(cplx v, double p) { return make_double2(__dmul_rn(v.x, p), __dmul_rn(v.y, p)); }
+
+template <int LPC>
+__device__ __forceinline__ double group_max(double v) {
+#pragma unroll
+    for (int o = 1; o < LPC; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o, LPC));
+    return v;
+}
+
+template <typename T, int LPC>
+__device__ __forceinline__ T group_shfl(T v, int src) {
+    if constexpr (S<T>::cplx_)
+        return make_double2(__shfl_sync(0xffffffffu, v.x, src, LPC), __shfl_sync(0xffffffffu, v.y, src, LPC));
+    else
+        return __shfl_sync(0xffffffffu, v, src, LPC);
+}
+
+template <typename T, int LPC, int RPL, bool SAFE, int OP>
 __global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
     typedef S<T> ST;
+    constexpr int G = 32 / LPC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nfull = int(a.hi - a.lo);
     const int64_t npk = int64_t(nfull) * (nfull - 1) / 2 + 128;
@@ -52,14 +102,13 @@ __global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
     // ---- stage U(I1,I1) (packed, solve coordinates), its diagonal and cnl ----
     const int tid = threadIdx.x, nth = blockDim.x;
     {
-        const int rl = tid & 127, cstep = nth >> 7;
-        for (int cq = tid >> 7; cq < nfull; cq += cstep) {
+        for (int idx = tid; idx < nfull * 128; idx += nth) {       // any blockDim
+            const int cq = idx >> 7, rl = idx & 127;
             if (rl < cq) {
                 if (OP == 0) {      // U~(i,c) = U(lo+i, lo+c)
                     pk[int64_t(cq) * (cq - 1) / 2 + rl] = a.U[(a.lo + rl) + (a.lo + cq) * a.ldu];
-                } else {            // U~(i,c) = conj(U(hi-1-c, hi-1-i)); read U column q = lo+cq, row r = lo+rl
-                    int ci = nfull - 1 - cq;          // solve index of the U column
-                    int cc = nfull - 1 - rl;          // solve index of the U row
+                } else {            // U~(i,c) = conj(U(hi-1-c, hi-1-i)); U column lo+cq, row lo+rl
+                    int ci = nfull - 1 - cq, cc = nfull - 1 - rl;
                     pk[int64_t(cc) * (cc - 1) / 2 + ci] = ST::conj(a.U[(a.lo + rl) + (a.lo + cq) * a.ldu]);
                 }
             }
@@ -73,141 +122,186 @@ __global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
     }
     __syncthreads();
 
-    const int lane = tid & 31;
+    const int lane = tid & 31, grp = lane / LPC, rl = lane % LPC;
     const int64_t wid = (int64_t(blockIdx.x) * nth + tid) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * nth) >> 5;
     const double delta = SAFE ? *a.delta : 0.0;
     const double Pb = SAFE ? a.P[a.b] : 0.0;
 
-    for (int64_t q = wid; q < a.ncols; q += nw) {
-        const int64_t j = a.c0 + q;
-        const int64_t r = (OP == 0 && a.rowend) ? a.rowend[j] : a.m;
-        if (r <= a.lo) {                      // column not active in this block
-            if (SAFE && lane == 0) a.dblk[j] = 0;
-            continue;
-        }
-        const int nrow = OP == 0 ? int((a.hi < r ? a.hi : r) - a.lo) : nfull;
-        T sh = a.shifts[j * a.sstride];
+    for (int64_t base = wid * G; base < a.ncols; base += nw * G) {
+        const int64_t q = base + grp;
+        const bool valid = q < a.ncols;
+        const int64_t j = a.c0 + (valid ? q : 0);
+        const int64_t r = valid ? ((OP == 0 && a.rowend) ? a.rowend[j] : a.m) : 0;
+        const bool active = valid && r > a.lo;
+        if (SAFE && valid && !active && rl == 0) a.dblk[j] = 0;     // inactive column: no rescale
+        const int nrow = active ? (OP == 0 ? int((a.hi < r ? a.hi : r) - a.lo) : nfull) : 0;
+        int nmax = nrow;
+#pragma unroll
+        for (int o = LPC; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        if (nmax == 0) continue;                                      // warp-uniform
+        T sh = active ? a.shifts[j * a.sstride] : ST::zero();
         if (OP == 1) sh = ST::conj(sh);
         T *x = a.B + j * a.ldb;
-
-        T y[RPL], d[RPL];
-#pragma unroll
-        for (int rr = 0; rr < RPL; rr++) {
-            int sc = rr * 32 + lane;
-            if (sc < nrow) {
-                int64_t row = OP == 0 ? a.lo + sc : a.hi - 1 - sc;
-                y[rr] = x[row];
-                T dd = ST::sub(dg[sc], sh);
-                if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
-                d[rr] = dd;
-            } else {
-                y[rr] = ST::zero();
-                d[rr] = ST::real(1.0);
-            }
-        }
+        auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
+        auto dof = [&](int sc) -> T {
+            T dd = ST::sub(dg[sc], sh);
+            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
+            return dd;
+        };
 
         bool guarded = false;
         double g = 0.0;
-        int kt = 0;
         if (SAFE) {
-            // ---- precheck, eqs. (4)-(5): M = max(g/|d_l|, M); g = g (1 + cnl/|d_l|),
-            // evaluated in the oracle's order: the product chain is sequential, the quotients
-            // use the value of g before each step. ----
-            double ad[RPL], tf[RPL], gb[RPL];
+            // ---- precheck, eqs. (4)-(5), in the oracle's order:
+            //      M = max_l g_l/|d_l|,  g_{l-1} = g_l * (1 + cnl_l/|d_l|),  g_top = ||y(I1)||_inf ----
             double g0 = 0.0;
 #pragma unroll
-            for (int rr = 0; rr < RPL; rr++) {
-                int sc = rr * 32 + lane;
-                g0 = fmax(g0, ST::mod(y[rr]));
-                ad[rr] = ST::mod(d[rr]);
-                tf[rr] = __dadd_rn(1.0, __ddiv_rn(sc < nrow ? cn[sc] : 0.0, ad[rr]));
-                gb[rr] = 0.0;
+            for (int t = 0; t < RPL; t++) {
+                int sc = rl + LPC * t;
+                if (sc < nrow) g0 = fmax(g0, ST::mod(x[rowof(sc)]));
             }
-            g0 = warp_max(g0);
-            double gg = g0;
+            g0 = group_max<LPC>(g0);
+            double ad[RPL], tf[RPL], gb[RPL];
 #pragma unroll
-            for (int rr = RPL - 1; rr >= 0; rr--) {
-                for (int t = 31; t >= 0; t--) {
-                    if (rr * 32 + t >= nrow) continue;
-                    if (lane == t) gb[rr] = gg;
-                    gg = __dmul_rn(gg, __shfl_sync(0xffffffffu, tf[rr], t));
+            for (int t = 0; t < RPL; t++) {
+                int sc = rl + LPC * t;
+                ad[t] = 1.0; tf[t] = 1.0; gb[t] = 0.0;
+                if (sc < nrow) {
+                    ad[t] = ST::mod(dof(sc));
+                    tf[t] = __dadd_rn(1.0, __ddiv_rn(cn[sc], ad[t]));
+                }
+            }
+            double gg = g0;
+            for (int sc = nmax - 1; sc >= 0; sc--) {
+                const int t = sc / LPC, rr = sc % LPC;
+                double own = 1.0;
+#pragma unroll
+                for (int t2 = 0; t2 < RPL; t2++)
+                    if (t2 == t) own = tf[t2];
+                double tfv = __shfl_sync(0xffffffffu, own, rr, LPC);
+                if (sc < nrow) {
+#pragma unroll
+                    for (int t2 = 0; t2 < RPL; t2++)
+                        if (t2 == t && rl == rr) gb[t2] = gg;
+                    gg = __dmul_rn(gg, tfv);
                 }
             }
             double M = 0.0;
 #pragma unroll
-            for (int rr = 0; rr < RPL; rr++)
-                if (rr * 32 + lane < nrow) M = fmax(M, __ddiv_rn(gb[rr], ad[rr]));
-            M = warp_max(M);
-            guarded = !(M < kOmega && gg < kOmega);
+            for (int t = 0; t < RPL; t++)
+                if (rl + LPC * t < nrow) M = fmax(M, __ddiv_rn(gb[t], ad[t]));
+            M = group_max<LPC>(M);
+            guarded = active && !(M < kOmega && gg < kOmega);
             g = g0;
         }
 
-        // ---- Trsv / guarded loop, solve coordinate sc = nrow-1 .. 0 ----
+        T y[RPL];
 #pragma unroll
-        for (int rr = RPL - 1; rr >= 0; rr--) {
-            for (int t = 31; t >= 0; t--) {
-                const int sc = rr * 32 + t;
-                if (sc >= nrow) continue;
-                T yl = ST::shfl(y[rr], t);
-                T dl = ST::shfl(d[rr], t);
+        for (int t = 0; t < RPL; t++) {
+            int sc = rl + LPC * t;
+            y[t] = sc < nrow ? x[rowof(sc)] : ST::zero();
+        }
+
+        // ---- Trsv / guarded loop over solve rows sc = nmax-1 .. 0 ----
+        // Rescales "y := t y" of the guarded loop are applied LAZILY to the rows
+        // held in registers: y[] lives in a frame 2^pend above the true (oracle) frame; the
+        // chain values are brought to the true frame exactly (power-of-two scaling commutes
+        // with rounding), and the registers are flushed once pend reaches 12 bits, which keeps
+        // |y|, |x u| below DBL_MAX for max|U| <= 2^40 (R8).
+        // The step loop is a runtime loop (compact code: the I-cache, not the ALUs, bounded an
+        // unrolled version); the lane-local row slot t = sc / LPC is selected with predicates.
+        int kt = 0, pend = 0;
+        for (int sc = nmax - 1; sc >= 0; sc--) {
+            const int t = sc / LPC, rr = sc % LPC;
+            T own = ST::zero();
+#pragma unroll
+            for (int t2 = 0; t2 < RPL; t2++)
+                if (t2 == t) own = y[t2];
+            T yl = group_shfl<T, LPC>(own, rr);
+            if (sc < nrow) {
+                T dl = dof(sc);
+                Recip<T> rd;
+                rd.make(dl);
+                T xl;
                 if (SAFE && guarded) {
-                    double ay = ST::mod(yl), adl = ST::mod(dl);
-                    double lim = __dmul_rn(kOmega, adl);
-                    if (ay >= lim) {                                   // P:282-295 (R8)
-                        int k = minpow2(ay, lim);
-#pragma unroll
-                        for (int q2 = 0; q2 < RPL; q2++) y[q2] = ST::ldx(y[q2], -k);
-                        yl = ST::ldx(yl, -k);
-                        kt += k;
-                        g = ldexp(g, -k);
+                    if (pend) yl = scale_pw(yl, pow2i(-pend));         // true frame (exact)
+                    xl = rd.apply(yl);                                 // P:297 diagonal step
+                    // P:282-295 (R8): |y_l| >= Omega |d_l|.  Cheap conservative pre-test:
+                    // |y| <= 1.4143 max|y_c|, |d| >= max|d_c|.
+                    if (!(1.5 * maxabs(yl) < kOmega * maxabs(dl))) {
+                        double ay = ST::mod(yl), lim = __dmul_rn(kOmega, ST::mod(dl));
+                        if (ay >= lim) {
+                            int k = minpow2(ay, lim);
+                            pend += k;
+                            yl = ST::ldx(yl, -k);
+                            xl = rd.apply(yl);
+                            kt += k;
+                            g = ldexp(g, -k);
+                        }
                     }
-                }
-                T xl = ST::div(yl, dl);                                // P:297 diagonal step
-                if (SAFE && guarded) {
                     double M = ST::mod(xl);
                     g = __dadd_rn(g, __dmul_rn(M, cn[sc]));
                     if (g >= kOmega) {
                         int k = minpow2(g, kOmega);
-#pragma unroll
-                        for (int q2 = 0; q2 < RPL; q2++) y[q2] = ST::ldx(y[q2], -k);
+                        pend += k;
                         xl = ST::ldx(xl, -k);
                         kt += k;
                         g = ldexp(g, -k);
                     }
+                    if (pend >= 12) {                                  // flush registers -> true frame
+                        if (pend < 1000) {
+                            double p = pow2i(-pend);
+#pragma unroll
+                            for (int t2 = 0; t2 < RPL; t2++) y[t2] = scale_pw(y[t2], p);
+                        } else {
+#pragma unroll
+                            for (int t2 = 0; t2 < RPL; t2++) y[t2] = ST::ldx(y[t2], -pend);
+                        }
+                        pend = 0;
+                    } else if (pend) {
+                        xl = scale_pw(xl, pow2i(pend));                // register frame for the update
+                    }
+                } else {
+                    xl = rd.apply(yl);                                 // P:297 / P:82
                 }
-                if (lane == t) y[rr] = xl;
-                // substitution within the block (P:315 / P:84): rows sc' < sc
+                // owner stores x_l; substitution within the block (P:315 / P:84): rows sc' < sc
                 const T *col = pk + int64_t(sc) * (sc - 1) / 2;
 #pragma unroll
-                for (int q2 = 0; q2 <= rr; q2++) {
-                    int i = q2 * 32 + lane;
-                    if (i < sc) y[q2] = ST::fnms(y[q2], xl, col[i]);
+                for (int t2 = 0; t2 < RPL; t2++) {
+                    int i = rl + LPC * t2;
+                    if (i < sc) y[t2] = ST::fnms(y[t2], xl, col[i]);
+                    else if (i == sc) y[t2] = xl;
                 }
             }
         }
+        if (SAFE && pend) {
+#pragma unroll
+            for (int t2 = 0; t2 < RPL; t2++) y[t2] = ST::ldx(y[t2], -pend);
+        }
 
         if (SAFE) {
-            int ej = a.e[j];
-            double Gj = a.G[j];
+            int ej = 0;
+            double Gj = 0.0;
+            if (active) { ej = a.e[j]; Gj = a.G[j]; }
             if (kt > 0) {                                              // P:376-386, step (ii)
                 ej -= kt;
                 Gj = ldexp(Gj, -kt);
             }
             double xm = 0.0;
 #pragma unroll
-            for (int rr = 0; rr < RPL; rr++) xm = fmax(xm, ST::mod(y[rr]));
-            xm = warp_max(xm);
+            for (int t = 0; t < RPL; t++) xm = fmax(xm, ST::mod(y[t]));
+            xm = group_max<LPC>(xm);
             Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
             int k3 = 0;
             if (Gj >= kOmega) {
                 k3 = minpow2(Gj, kOmega);
 #pragma unroll
-                for (int rr = 0; rr < RPL; rr++) y[rr] = ST::ldx(y[rr], -k3);
+                for (int t = 0; t < RPL; t++) y[t] = ST::ldx(y[t], -k3);
                 ej -= k3;
                 Gj = ldexp(Gj, -k3);
             }
-            if (lane == 0) {
+            if (active && rl == 0) {
                 a.e[j] = ej;
                 a.G[j] = Gj;
                 a.dblk[j] = -(kt + k3);
@@ -215,9 +309,9 @@ __global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
             }
         }
 #pragma unroll
-        for (int rr = 0; rr < RPL; rr++) {
-            int sc = rr * 32 + lane;
-            if (sc < nrow) x[OP == 0 ? a.lo + sc : a.hi - 1 - sc] = y[rr];
+        for (int t = 0; t < RPL; t++) {
+            int sc = rl + LPC * t;
+            if (sc < nrow) x[rowof(sc)] = y[t];
         }
     }
 }

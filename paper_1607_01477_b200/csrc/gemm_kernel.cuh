@@ -18,10 +18,12 @@
 
 namespace mstrsm {
 
+// Not volatile: the MMA is a pure function of its operands, so the compiler may interleave the
+// independent accumulator chains.
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -53,10 +55,10 @@ struct GemmArgs {
 };
 
 // Tile geometry.  Complex: CTA 64 (rows) x 64 (cols), warp 32x32, BK = 16.
-//                 Real:    CTA 128 x 64, warp 64x32, BK = 16.
+//                 Real:    CTA 64 x 64, warp 32x32, BK = 16.
 template <typename T> struct GemmCfg;
 template <> struct GemmCfg<cplx> { static constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32; };
-template <> struct GemmCfg<double> { static constexpr int BM = 128, BN = 64, BK = 16, WM = 64, WN = 32; };
+template <> struct GemmCfg<double> { static constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32; };
 constexpr int kGemmStages = 3;
 constexpr int kGemmThreads = 128;
 
@@ -163,12 +165,36 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
         cp_async_commit();
     }
 
+    // C tile prefetch: half h (columns [32h, 32h+32) of the tile) goes to the pipeline stage
+    // (nk + h) % S, issued at iteration max(0, nk - 2 + h), when that stage is no longer needed by
+    // the mainloop; the epilogue then reads C from shared memory.
+    static_assert(kGemmStages == 3, "C prefetch assumes 3 stages");
+    static_assert(BM * (BN / 2) <= gemm_stage_elems<T>(), "C half must fit in one stage");
+    auto offC = [&](int row, int colh) {                  // swizzled [col][row] within a half
+        if constexpr (CPX) return colh * BM + (row ^ (((colh >> 1) & 3) << 1));
+        else return colh * BM + (row ^ (((colh >> 1) & 3) << 2));
+    };
+    auto load_c_half = [&](int h) {
+        T *Cs = smem + ((nk + h) % kGemmStages) * gemm_stage_elems<T>();
+#pragma unroll
+        for (int it = 0; it < (BM * (BN / 2)) / kGemmThreads; it++) {
+            int idx = it * kGemmThreads + tid;
+            int row = idx % BM, colh = idx / BM;
+            int64_t gi = m0 + row, gj = n0 + h * (BN / 2) + colh;
+            bool v = gi < g.M && gj < g.N;
+            const T *src = g.B + (v ? (g.c_r0 + gi) + (g.col0 + gj) * g.ldb : 0);
+            cp_async<ESZ>(Cs + offC(row, colh), src, v);
+        }
+    };
+
     for (int kt = 0; kt < nk; kt++) {
         cp_async_wait<kGemmStages - 2>();
         __syncthreads();
         {
             int nxt = kt + kGemmStages - 1;
             if (nxt < nk) load_stage(nxt % kGemmStages, nxt);
+            if (kt == (nk - 2 > 0 ? nk - 2 : 0)) load_c_half(0);
+            if (kt == nk - 1) load_c_half(1);
             cp_async_commit();
         }
         const T *As = stageA(kt % kGemmStages);
@@ -176,13 +202,14 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
 #pragma unroll
         for (int kk = 0; kk < BK / 4; kk++) {
             const int k = kk * 4 + tq;
-            double ar[MI], ai[MI], br[NI], bi[NI];
+            double ar[MI], ai[MI], nai[MI], br[NI], bi[NI];
 #pragma unroll
             for (int i = 0; i < MI; i++) {
                 int mm = wm * WM + i * 8 + gq;
                 T v = OPC ? As[offRK<T>(mm, k)] : As[offA_kmajor<T>(k, mm)];
                 if constexpr (CPX) { ar[i] = v.x; ai[i] = OPC ? -v.y : v.y; }
                 else { ar[i] = v; ai[i] = 0.0; }
+                nai[i] = -ai[i];
             }
 #pragma unroll
             for (int jn = 0; jn < NI; jn++) {
@@ -191,38 +218,50 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
                 if constexpr (CPX) { br[jn] = v.x; bi[jn] = v.y; }
                 else { br[jn] = v; bi[jn] = 0.0; }
             }
+            // four passes over independent accumulators: consecutive DMMAs never depend on
+            // each other (dependency distance MI*NI*2 instructions)
 #pragma unroll
-            for (int i = 0; i < MI; i++) {
-                double nai = -ai[i];
+            for (int i = 0; i < MI; i++)
 #pragma unroll
-                for (int jn = 0; jn < NI; jn++) {
-                    dmma(accR[i][jn][0], accR[i][jn][1], ar[i], br[jn]);
-                    if constexpr (CPX) {
-                        dmma(accR[i][jn][0], accR[i][jn][1], nai, bi[jn]);
-                        dmma(accI[i][jn][0], accI[i][jn][1], ar[i], bi[jn]);
-                        dmma(accI[i][jn][0], accI[i][jn][1], ai[i], br[jn]);
-                    }
-                }
+                for (int jn = 0; jn < NI; jn++) dmma(accR[i][jn][0], accR[i][jn][1], ar[i], br[jn]);
+            if constexpr (CPX) {
+#pragma unroll
+                for (int i = 0; i < MI; i++)
+#pragma unroll
+                    for (int jn = 0; jn < NI; jn++) dmma(accI[i][jn][0], accI[i][jn][1], ar[i], bi[jn]);
+#pragma unroll
+                for (int i = 0; i < MI; i++)
+#pragma unroll
+                    for (int jn = 0; jn < NI; jn++) dmma(accR[i][jn][0], accR[i][jn][1], nai[i], bi[jn]);
+#pragma unroll
+                for (int i = 0; i < MI; i++)
+#pragma unroll
+                    for (int jn = 0; jn < NI; jn++) dmma(accI[i][jn][0], accI[i][jn][1], ai[i], br[jn]);
             }
         }
     }
+    if (nk == 0) { load_c_half(0); load_c_half(1); cp_async_commit(); }
     cp_async_wait<0>();
+    __syncthreads();
 
-    // ---- epilogue: C = 2^d C - acc ----
+    // ---- epilogue: C = 2^d C - acc (C from shared memory) ----
+    const T *Cs = smem + ((nk + wn) % kGemmStages) * gemm_stage_elems<T>();   // this warp's half
 #pragma unroll
     for (int jn = 0; jn < NI; jn++) {
 #pragma unroll
         for (int c = 0; c < 2; c++) {
-            int64_t gj = n0 + wn * WN + jn * 8 + tq * 2 + c;
+            const int colh = jn * 8 + tq * 2 + c;
+            int64_t gj = n0 + wn * WN + colh;
             if (gj >= g.N) continue;
             int d = g.dblk ? g.dblk[g.col0 + gj] : 0;
             double sc = d >= -1022 ? ldexp(1.0, d) : 0.0;
             T *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
 #pragma unroll
             for (int i = 0; i < MI; i++) {
-                int64_t gi = m0 + wm * WM + i * 8 + gq;
+                const int row = wm * WM + i * 8 + gq;
+                int64_t gi = m0 + row;
                 if (gi >= g.M) continue;
-                T old = colp[gi];
+                T old = Cs[offC(row, colh)];
                 T nv;
                 if constexpr (CPX) {
                     if (d == 0) { nv.x = old.x - accR[i][jn][c]; nv.y = old.y - accI[i][jn][c]; }

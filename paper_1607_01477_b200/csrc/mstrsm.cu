@@ -20,80 +20,13 @@
 
 #include "../../include/mstrsm.h"
 #include "aux_kernels.cuh"
-#include "diag_kernel.cuh"
-#include "gemm_kernel.cuh"
+#include "runtime.cuh"
 #include "lanczos_kernels.cuh"
 
 using namespace mstrsm;
+using namespace mstrsm::rt;
 
 namespace {
-
-cudaStream_t g_stream = nullptr;
-std::atomic<int64_t> g_launches{0};
-int *g_flag = nullptr;                 // device: non-finite input seen
-char g_errmsg[512] = "no error";
-int g_num_sms = 0;
-std::mutex g_mu;
-
-int set_cuda_error(cudaError_t e, const char *where) {
-    snprintf(g_errmsg, sizeof(g_errmsg), "CUDA error in %s: %s", where, cudaGetErrorString(e));
-    return 1;
-}
-
-#define CK(call)                                               \
-    do {                                                       \
-        cudaError_t e_ = (call);                               \
-        if (e_ != cudaSuccess) return set_cuda_error(e_, #call); \
-    } while (0)
-#define CK_LAUNCH(name)                                        \
-    do {                                                       \
-        g_launches.fetch_add(1, std::memory_order_relaxed);    \
-        cudaError_t e_ = cudaGetLastError();                   \
-        if (e_ != cudaSuccess) return set_cuda_error(e_, name); \
-    } while (0)
-
-int ensure_init() {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (g_flag) return 0;
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaMalloc(&g_flag, sizeof(int)));
-    CK(cudaMemset(g_flag, 0, sizeof(int)));
-    return 0;
-}
-
-inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
-
-// ---------------------------------------------------------------- live kernel profiling
-// When enabled (mstrsm_profile(1)), every launch is bracketed by CUDA events recorded on the
-// launching stream; mstrsm_profile_read sums the elapsed times per kernel kind.
-enum { PK_GEMM = 0, PK_DIAG = 1, PK_OTHER = 2, PK_N = 3 };
-struct ProfRec { int kind; cudaEvent_t e0, e1; double flops; };
-bool g_prof = false;
-std::vector<ProfRec> g_prof_recs;
-std::vector<cudaEvent_t> g_ev_pool;
-
-cudaEvent_t ev_get() {
-    if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    return e;
-}
-struct ProfScope {
-    ProfRec r{};
-    bool on;
-    ProfScope(int kind, double flops) : on(g_prof) {
-        if (!on) return;
-        r.kind = kind; r.flops = flops; r.e0 = ev_get(); r.e1 = ev_get();
-        cudaEventRecord(r.e0, g_stream);
-    }
-    ~ProfScope() {
-        if (!on) return;
-        cudaEventRecord(r.e1, g_stream);
-        g_prof_recs.push_back(r);
-    }
-};
 
 // Device workspace for one solve, carved out of one stream-ordered allocation.
 struct Work {
@@ -143,8 +76,14 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w) {
         CK_LAUNCH("norm_cols_n_kernel");
         panel_sum_kernel<<<int(cdiv(nblk, 128)), 128, 0, g_stream>>>(0, m, nb, nblk, w.part, w.P);
         CK_LAUNCH("panel_sum_kernel");
-        rowsum_n_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, w.part);
+        int64_t nch = cdiv(m, kRowsumChunk);
+        double *part2 = nullptr;
+        CK(cudaMallocAsync(&part2, size_t(nch) * m * 8, g_stream));
+        rowsum_n_kernel<T><<<dim3(unsigned(cdiv(m, 128)), unsigned(nch)), 128, 0, g_stream>>>(U, ldu, m, part2);
         CK_LAUNCH("rowsum_n_kernel");
+        rowsum_reduce_kernel<<<int(cdiv(m, 128)), 128, 0, g_stream>>>(m, nch, part2, w.part);
+        CK_LAUNCH("rowsum_reduce_kernel");
+        CK(cudaFreeAsync(part2, g_stream));
     } else {
         norm_rows_c_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
         CK_LAUNCH("norm_rows_c_kernel");
@@ -155,53 +94,6 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w) {
     }
     delta_kernel<<<1, 1024, 0, g_stream>>>(m, w.part, w.delta);
     CK_LAUNCH("delta_kernel");
-    return 0;
-}
-
-// ---------------------------------------------------------------- diag launch (a.3/a.4)
-template <typename T, int RPL, bool SAFE, int OP>
-int launch_diag_t(const DiagArgs<T> &a) {
-    auto kern = diag_kernel<T, RPL, SAFE, OP>;
-    int nfull = int(a.hi - a.lo);
-    size_t smem = size_t(diag_smem_bytes(RPL * 32 >= nfull ? nfull : nfull, sizeof(T)));
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
-    }
-    int threads = smem > 96 * 1024 ? 512 : 256;
-    int occ = occupancy(kern, threads, smem);
-    int64_t warps = threads / 32;
-    int grid = int(std::min<int64_t>(cdiv(a.ncols, warps), int64_t(occ) * g_num_sms));
-    if (grid < 1) grid = 1;
-    double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
-    ProfScope ps(PK_DIAG, fl);
-    kern<<<grid, threads, smem, g_stream>>>(a);
-    CK_LAUNCH("diag_kernel");
-    return 0;
-}
-
-template <typename T, bool SAFE, int OP>
-int launch_diag(const DiagArgs<T> &a, int nb) {
-    if (nb <= 32) return launch_diag_t<T, 1, SAFE, OP>(a);
-    if (nb <= 64) return launch_diag_t<T, 2, SAFE, OP>(a);
-    return launch_diag_t<T, 4, SAFE, OP>(a);
-}
-
-// ---------------------------------------------------------------- GEMM launch (a.5)
-template <typename T, bool OPC>
-int launch_gemm(const GemmArgs<T> &g) {
-    auto kern = gemm_update_kernel<T, OPC>;
-    static bool attr_set = false;
-    constexpr int smem = gemm_smem_bytes<T>();
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
-    }
-    dim3 grid(unsigned(cdiv(g.M, GemmCfg<T>::BM)), unsigned(cdiv(g.N, GemmCfg<T>::BN)));
-    ProfScope ps(PK_GEMM, double(g.M) * g.N * g.K * (S<T>::cplx_ ? 8.0 : 2.0));
-    kern<<<grid, kGemmThreads, smem, g_stream>>>(g);
-    CK_LAUNCH("gemm_update_kernel");
     return 0;
 }
 

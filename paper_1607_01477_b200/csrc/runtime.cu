@@ -1,0 +1,45 @@
+// runtime.cu -- definitions of the library-wide runtime state (see runtime.cuh).
+#include <stdio.h>
+
+#include <mutex>
+
+#include "runtime.cuh"
+
+namespace mstrsm {
+namespace rt {
+
+cudaStream_t g_stream = nullptr;
+std::atomic<int64_t> g_launches{0};
+int *g_flag = nullptr;                 // device: non-finite input seen
+char g_errmsg[512] = "no error";
+int g_num_sms = 0;
+static std::mutex g_mu;
+bool g_prof = false;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_ev_pool;
+
+int set_cuda_error(cudaError_t e, const char *where) {
+    snprintf(g_errmsg, sizeof(g_errmsg), "CUDA error in %s: %s", where, cudaGetErrorString(e));
+    return 1;
+}
+
+int ensure_init() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_flag) return 0;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaMalloc(&g_flag, sizeof(int)));
+    CK(cudaMemset(g_flag, 0, sizeof(int)));
+    return 0;
+}
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+}  // namespace rt
+}  // namespace mstrsm

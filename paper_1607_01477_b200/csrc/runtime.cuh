@@ -1,0 +1,75 @@
+// runtime.cuh -- library-wide runtime state shared by the translation units of libmstrsm:
+// the current stream, launch counter, error string, live profiling (CUDA events on the
+// launching stream) and the launcher prototypes of the kernels compiled in separate units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <vector>
+
+#include "common.cuh"
+#include "diag_kernel.cuh"
+#include "gemm_kernel.cuh"
+
+namespace mstrsm {
+namespace rt {
+
+extern cudaStream_t g_stream;
+extern std::atomic<int64_t> g_launches;
+extern int *g_flag;
+extern char g_errmsg[512];
+extern int g_num_sms;
+
+int set_cuda_error(cudaError_t e, const char *where);
+int ensure_init();
+
+#define CK(call)                                                       \
+    do {                                                               \
+        cudaError_t e_ = (call);                                       \
+        if (e_ != cudaSuccess) return ::mstrsm::rt::set_cuda_error(e_, #call); \
+    } while (0)
+#define CK_LAUNCH(name)                                                \
+    do {                                                               \
+        ::mstrsm::rt::g_launches.fetch_add(1, std::memory_order_relaxed); \
+        cudaError_t e_ = cudaGetLastError();                           \
+        if (e_ != cudaSuccess) return ::mstrsm::rt::set_cuda_error(e_, name); \
+    } while (0)
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// live kernel profiling
+enum { PK_GEMM = 0, PK_DIAG = 1, PK_OTHER = 2, PK_N = 3 };
+struct ProfRec { int kind; cudaEvent_t e0, e1; double flops; };
+extern bool g_prof;
+extern std::vector<ProfRec> g_prof_recs;
+extern std::vector<cudaEvent_t> g_ev_pool;
+cudaEvent_t ev_get();
+struct ProfScope {
+    ProfRec r{};
+    bool on;
+    ProfScope(int kind, double flops) : on(g_prof) {
+        if (!on) return;
+        r.kind = kind; r.flops = flops; r.e0 = ev_get(); r.e1 = ev_get();
+        cudaEventRecord(r.e0, g_stream);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(r.e1, g_stream);
+        g_prof_recs.push_back(r);
+    }
+};
+
+template <typename K>
+int occupancy(K kern, int threads, size_t smem) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess) nb = 1;
+    return nb > 1 ? nb : 1;
+}
+
+// launchers compiled in their own translation units (diag_*.cu, gemm_launch.cu)
+template <typename T, bool SAFE, int OP> int launch_diag(const DiagArgs<T> &a, int nb);
+template <typename T, bool OPC> int launch_gemm(const GemmArgs<T> &g);
+
+}  // namespace rt
+}  // namespace mstrsm
