@@ -1,0 +1,9 @@
+// diag_dC_plain.cu -- instantiation of the diagonal-block kernel for scalar double, op C, plain variant
+// (one translation unit per instantiation set so the build compiles them in parallel).
+#include "diag_launch.cuh"
+
+namespace mstrsm {
+namespace rt {
+template int launch_diag<double, false, 1>(const DiagArgs<double> &, int);
+}  // namespace rt
+}  // namespace mstrsm

@@ -10,14 +10,22 @@
 // the GEMM epilogue (rows I0, still pending) and E[b][j] = e_j records the frame of the rows
 // finalised here (rows I2 are fixed up once at the end by finalize_kernel).
 //
-// Layout.  A warp holds G = 32/LPC columns; LPC lanes share one column and lane r of a group
-// owns the solve rows sc = r + LPC*t, t < RPL (LPC*RPL >= n_b).  The per-row scalar chain of
-// Alg. 4 (|y_l|, the division, |x_l|, the bound checks) is therefore executed once per group and
-// serves G columns per warp instruction, while the substitution within the block is spread over
-// the LPC lanes.  The diagonal block is staged once per CTA in shared memory as a packed
-// strictly-upper triangle in "solve coordinates" sc (op N: sc = row - lo; op C: sc = hi-1-row,
-// the flip of R9), so one loop serves back substitution (op N) and forward substitution with
-// L = U^H (op C).  Persistent CTAs loop over column groups.
+// Layout.  A warp holds G = 32/LPC columns; LPC lanes share one column and lane r of a group owns
+// the solve rows sc = r + LPC*t, t < RPL (LPC*RPL >= n_b), in registers.  The row loop is
+// "for t = RPL-1..0 (unrolled) for r = LPC-1..0 (runtime)", so every register slot index is a
+// compile-time constant and row sc's update touches only the slots t2 <= t that still hold
+// unsolved rows.  The diagonal block is staged once per CTA in shared memory as a packed strictly
+// upper triangle in "solve coordinates" sc (op N: sc = row - lo; op C: sc = hi-1-row, the flip of
+// R9), so one loop serves back substitution (op N) and forward substitution with L = U^H (op C).
+// Persistent CTAs loop over column groups.
+//
+// Per-row pivot data (1/d_l, Omega*|d_l|) depend only on the shift, not on the running solution,
+// so every lane precomputes them for its own rows before the loop and the sequential chain only
+// shuffles them.  In the guarded loop the solution lives in a register frame 2^pend above the
+// true (paper) frame: a rescale "y := 2^-k y" only adds k to pend, which leaves
+// the register values -- and therefore the substitution -- untouched; the registers are brought
+// back to the true frame once pend reaches 12 bits.  The bound chain (|y_l|, |x_l|, g, the
+// rescale exponents) is branch-free and runs beside the substitution instead of in front of it.
 #pragma once
 #include "common.cuh"
 
@@ -42,36 +50,131 @@ __host__ __device__ inline int64_t diag_smem_bytes(int nfull, int esize) {
     return pk * esize + int64_t(nfull) * esize + int64_t(nfull) * 8;
 }
 
-// 1/d for the division x = y/d, computed once per row and group (Smith's scaling, R7).
-template <typename T> struct Recip;
-template <> struct Recip<double> {
-    double v;
-    __device__ __forceinline__ void make(double d) { v = d; }
-    __device__ __forceinline__ double apply(double y) const { return __ddiv_rn(y, v); }   // exact IEEE division
-};
-template <> struct Recip<cplx> {
-    double r, inv; bool sw;
-    __device__ __forceinline__ void make(cplx d) {
-        sw = fabs(d.y) > fabs(d.x);
-        if (!sw) { r = __ddiv_rn(d.y, d.x); inv = __drcp_rn(__dadd_rn(d.x, __dmul_rn(d.y, r))); }
-        else { r = __ddiv_rn(d.x, d.y); inv = __drcp_rn(__dadd_rn(d.y, __dmul_rn(d.x, r))); }
-    }
-    // Smith's numerators times the rounded reciprocal of the denominator (<= 1.5 ulp from the
-    // oracle's Smith quotient; R24 covers the difference).
-    __device__ __forceinline__ cplx apply(cplx a) const {
-        if (!sw) return make_double2(__dmul_rn(__dadd_rn(a.x, __dmul_rn(a.y, r)), inv),
-                                     __dmul_rn(__dsub_rn(a.y, __dmul_rn(a.x, r)), inv));
-        return make_double2(__dmul_rn(__dadd_rn(__dmul_rn(a.x, r), a.y), inv),
-                            __dmul_rn(__dsub_rn(__dmul_rn(a.y, r), a.x), inv));
-    }
+// Threads per CTA of an instantiation (its __launch_bounds__): 8 warps when each lane holds 16
+// rows (up to 255 registers), 12 (complex) or 16 (real) warps when it holds 8.
+template <typename T, int RPL> struct DiagThreads {
+    static constexpr int value = RPL >= 16 ? 256 : (S<T>::cplx_ ? 384 : 512);
 };
 
 // 2^k as a double for -1022 <= k <= 1023 (exact, built from the exponent bits).
 __device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(1023 + k) << 52); }
+// v * 2^-k for k >= 0 as a product with an exact power of two: rounded exactly like ldexp(v, -k)
+// for k <= 1022; beyond that (only after extreme rescales) two products, which can differ from
+// ldexp by the double rounding of a subnormal result.
+__device__ __forceinline__ double mulp2n(double v, int k) {
+    if (k <= 1022) return __dmul_rn(v, pow2i(-k));
+    return __dmul_rn(__dmul_rn(v, pow2i(-1022)), pow2i(-min(k - 1022, 1022)));
+}
+__device__ __forceinline__ cplx mulp2n(cplx v, int k) { return make_double2(mulp2n(v.x, k), mulp2n(v.y, k)); }
+// y := 2^-k y for a whole register array (one scale factor for all elements); k <= 1022 when
+// SMALL, any k >= 0 otherwise.
+template <bool SMALL, typename T, int N>
+__device__ __forceinline__ void scale_all(T (&y)[N], int k) {
+    const double p1 = SMALL || k <= 1022 ? pow2i(-k) : pow2i(-1022);
+#pragma unroll
+    for (int t = 0; t < N; t++) {
+        if constexpr (S<T>::cplx_) y[t] = make_double2(__dmul_rn(y[t].x, p1), __dmul_rn(y[t].y, p1));
+        else y[t] = __dmul_rn(y[t], p1);
+    }
+    if (!SMALL && k > 1022) {
+        const double p2 = pow2i(-min(k - 1022, 1022));
+#pragma unroll
+        for (int t = 0; t < N; t++) {
+            if constexpr (S<T>::cplx_) y[t] = make_double2(__dmul_rn(y[t].x, p2), __dmul_rn(y[t].y, p2));
+            else y[t] = __dmul_rn(y[t], p2);
+        }
+    }
+}
+// v * 2^s for |s| <= 1074 as two exact power-of-two products.
+__device__ __forceinline__ double mulp2s(double v, int s) {
+    const int h = s / 2;
+    return __dmul_rn(__dmul_rn(v, pow2i(h)), pow2i(s - h));
+}
 __device__ __forceinline__ double maxabs(double v) { return fabs(v); }
 __device__ __forceinline__ double maxabs(cplx v) { return fmax(fabs(v.x), fabs(v.y)); }
-__device__ __forceinline__ double scale_pw(double v, double p) { return __dmul_rn(v, p); }
-__device__ __forceinline__ cplx scale_pw(cplx v, double p) { return make_double2(__dmul_rn(v.x, p), __dmul_rn(v.y, p)); }
+
+// |z| of R7 (prescaled sqrt(re^2 + im^2), no FMA) without branches; equal to S<cplx>::mod for
+// finite z.
+__device__ __forceinline__ double modv(double a) { return fabs(a); }
+__device__ __forceinline__ double modv(cplx a) {
+    double x = fabs(a.x), y = fabs(a.y), big = fmax(x, y);
+    double s = big > 0x1p+500 ? 0x1p-600 : (big < 0x1p-500 ? 0x1p+600 : 1.0);
+    double si = big > 0x1p+500 ? 0x1p+600 : (big < 0x1p-500 ? 0x1p-600 : 1.0);
+    x = __dmul_rn(x, s);
+    y = __dmul_rn(y, s);
+    return __dmul_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y))), si);
+}
+
+// R2's minpow2(a, L) (smallest k >= 1 with 2^-k a < L) for positive a >= L from the exponent and
+// mantissa bits: 2^-k a < L  <=>  k > e_a - e_L, or k = e_a - e_L with mant(a) < mant(L).
+__device__ __forceinline__ void exp_mant(double x, int &e, long long &mnt) {
+    long long b = __double_as_longlong(x);
+    e = int(b >> 52);
+    if (e == 0) { b = __double_as_longlong(__dmul_rn(x, 0x1p+64)); e = int(b >> 52) - 64; }   // subnormal
+    mnt = b & 0xFFFFFFFFFFFFFll;
+}
+__device__ __forceinline__ int minpow2_bits(double a, double L) {
+    if (!(a <= 1.7976931348623157e308)) return 1100;
+    int ea, el;
+    long long ma, ml;
+    exp_mant(a, ea, ma);
+    exp_mant(L, el, ml);
+    int k = ea - el + (ma >= ml ? 1 : 0);
+    return k < 1 ? 1 : k;
+}
+
+// Pivot data of one row: x = y / d.
+//   real:    d and its correctly rounded reciprocal; the quotient is q0 = y r, rem = y - q0 d
+//            (exact by FMA), q = q0 + rem r, which is the correctly rounded y / d (Markstein) when
+//            nothing under/overflows -- otherwise the IEEE division itself (bit-exact with the
+//            oracle's y / d).
+//   complex: 1/d from an exactly prescaled conj(d)/|d|^2; x = y * (1/d) differs from the
+//            oracle's Smith quotient by a few ulps (R24).
+template <typename T> struct Piv;
+template <> struct Piv<double> {
+    double d, r;
+    __device__ __forceinline__ void make(double dd) { d = dd; r = __drcp_rn(dd); }
+    __device__ __forceinline__ double apply(double y) const {
+        double q0 = __dmul_rn(y, r);
+        double rem = fma(-q0, d, y);
+        double q = fma(rem, r, q0);
+        double aq = fabs(q), ad = fabs(d);
+        bool ok = (aq < 0x1p+1000 && aq > 0x1p-960 && ad < 0x1p+1000 && ad > 0x1p-1000) || y == 0.0;
+        return ok ? q : __ddiv_rn(y, d);
+    }
+    __device__ __forceinline__ double absd() const { return fabs(d); }
+    template <int W> __device__ __forceinline__ Piv shfl(int src) const {
+        Piv o;
+        o.d = __shfl_sync(0xffffffffu, d, src, W);
+        o.r = __shfl_sync(0xffffffffu, r, src, W);
+        return o;
+    }
+};
+template <> struct Piv<cplx> {
+    cplx r;
+    __device__ __forceinline__ void make(cplx dd) {
+        double big = fmax(fabs(dd.x), fabs(dd.y));
+        if (!(big > 0.0 && big <= 1.7976931348623157e308)) {          // 0 or non-finite pivot
+            r = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+            return;
+        }
+        int e;
+        long long mnt;
+        exp_mant(big, e, mnt);
+        e -= 1023;                                                        // big in [2^e, 2^(e+1))
+        double dx = mulp2s(dd.x, -e), dy = mulp2s(dd.y, -e);              // max component in [1, 2)
+        double inv = __drcp_rn(fma(dx, dx, __dmul_rn(dy, dy)));          // 1 / |d 2^-e|^2
+        r = make_double2(mulp2s(__dmul_rn(dx, inv), -e), mulp2s(-__dmul_rn(dy, inv), -e));
+    }
+    __device__ __forceinline__ cplx apply(cplx y) const {
+        return make_double2(fma(y.x, r.x, -__dmul_rn(y.y, r.y)), fma(y.x, r.y, __dmul_rn(y.y, r.x)));
+    }
+    template <int W> __device__ __forceinline__ Piv shfl(int src) const {
+        Piv o;
+        o.r = make_double2(__shfl_sync(0xffffffffu, r.x, src, W), __shfl_sync(0xffffffffu, r.y, src, W));
+        return o;
+    }
+};
 
 template <int LPC>
 __device__ __forceinline__ double group_max(double v) {
@@ -88,8 +191,81 @@ __device__ __forceinline__ T group_shfl(T v, int src) {
         return __shfl_sync(0xffffffffu, v, src, LPC);
 }
 
+// The row loop of one column group.  GUARD: the guarded loop of Alg. 4 for the groups
+// with `guarded` set (others of the warp run the same substitution without rescales).
+template <typename T, int LPC, int RPL, bool GUARD>
+__device__ __forceinline__ void diag_rows(T (&y)[RPL], const Piv<T> (&pv)[RPL], const double (&oad)[RPL],
+                                          const T *__restrict__ pk, const double *__restrict__ cn,
+                                          int rl, int nrow, int nmax, bool guarded, double &g, int &kt) {
+    typedef S<T> ST;
+    int pend = 0;
+#pragma unroll
+    for (int t = RPL - 1; t >= 0; t--) {
+        if (t * LPC >= nmax) continue;                                     // warp-uniform
+#pragma unroll 1
+        for (int rr = LPC - 1; rr >= 0; rr--) {
+            const int sc = t * LPC + rr;
+            if (sc >= nmax) continue;                                      // warp-uniform
+            const bool in = sc < nrow;
+            const T yl = group_shfl<T, LPC>(y[t], rr);                     // register frame
+            const Piv<T> p = pv[t].template shfl<LPC>(rr);
+            T xv = p.apply(yl);                                            // P:297 / P:82
+            if constexpr (GUARD) {
+                double oadv;                                               // Omega |d_l|
+                if constexpr (ST::cplx_) oadv = __shfl_sync(0xffffffffu, oad[t], rr, LPC);
+                else oadv = __dmul_rn(kOmega, p.absd());
+                const double cnv = cn[sc];
+                const bool live = in && guarded;
+                // P:279-295 (R8): |y_l| >= Omega |d_l| in the true frame (pend <= 11 here: exact)
+                const double ay = __dmul_rn(modv(yl), pow2i(-pend));
+                const bool t1 = live && ay >= oadv;
+                const int k1 = t1 ? minpow2_bits(ay, oadv) : 0;
+                const int pend1 = pend + k1;
+                // the register-frame quotient would overflow (tiny pivot): take x_l in the true
+                // frame and bring the registers there before the substitution (rare)
+                const bool xtrue = t1 && !(maxabs(xv) < 0x1p+1020);
+                if (xtrue) xv = p.apply(mulp2n(yl, pend1));
+                // M = |x_l|, g += M cnl(l), rescale when g >= Omega
+                const double M = xtrue ? modv(xv) : mulp2n(modv(xv), pend1);
+                double gn = __dadd_rn(t1 ? mulp2n(g, k1) : g, __dmul_rn(M, cnv));
+                const bool t2 = live && gn >= kOmega;
+                const int k2 = t2 ? minpow2_bits(gn, kOmega) : 0;
+                if (t2) gn = mulp2n(gn, k2);
+                g = live ? gn : g;
+                kt += k1 + k2;
+                pend = pend1 + k2;
+                if (xtrue || pend >= 48) {
+                    // keep the substitution below overflow (R8): true frame first
+                    scale_all<false>(y, pend);
+                    xv = mulp2n(xv, xtrue ? k2 : pend);
+                    pend = 0;
+                }
+            }
+            const T xr = in ? xv : ST::zero();
+            // owner stores x_l; substitution within the block (P:315 / P:84): rows sc' < sc
+            const T *col = pk + (sc * (sc - 1)) / 2;
+            {
+                const int i = rl + LPC * t;
+                if (rl < rr) y[t] = ST::fnms(y[t], xr, col[i]);
+                else if (rl == rr && in) y[t] = xv;
+            }
+#pragma unroll
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, col[rl + LPC * t2]);
+            if constexpr (GUARD) {
+                if (pend >= 12) {                                          // back to the true frame
+                    scale_all<true>(y, pend);
+                    pend = 0;
+                }
+            }
+        }
+    }
+    if constexpr (GUARD) {
+        if (pend) scale_all<true>(y, pend);
+    }
+}
+
 template <typename T, int LPC, int RPL, bool SAFE, int OP>
-__global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
+__global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(DiagArgs<T> a) {
     typedef S<T> ST;
     constexpr int G = 32 / LPC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -144,141 +320,63 @@ __global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
         if (OP == 1) sh = ST::conj(sh);
         T *x = a.B + j * a.ldb;
         auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
-        auto dof = [&](int sc) -> T {
-            T dd = ST::sub(dg[sc], sh);
-            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);      // P:231-234
-            return dd;
-        };
+
+        // ---- load the rows, per-row pivot data (d_l = U(l,l) - s_j; delta for an exact zero,
+        //      P:231-234), Omega |d_l| ----
+        T y[RPL];
+        Piv<T> pv[RPL];
+        double oad[RPL];
+#pragma unroll
+        for (int t = 0; t < RPL; t++) {
+            const int sc = rl + LPC * t;
+            const bool in = sc < nrow;
+            y[t] = in ? x[rowof(sc)] : ST::zero();
+            T dd = in ? ST::sub(dg[sc], sh) : ST::real(1.0);
+            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
+            pv[t].make(dd);
+            oad[t] = SAFE && ST::cplx_ ? __dmul_rn(kOmega, modv(dd)) : 0.0;
+        }
 
         bool guarded = false;
         double g = 0.0;
         if (SAFE) {
             // ---- precheck, eqs. (4)-(5), in the oracle's order:
-            //      M = max_l g_l/|d_l|,  g_{l-1} = g_l * (1 + cnl_l/|d_l|),  g_top = ||y(I1)||_inf ----
+            //      M = max_l g_l/|d_l| (tested as g_l < Omega |d_l|), g_{l-1} = g_l (1 + cnl_l/|d_l|),
+            //      g_top = ||y(I1)||_inf ----
             double g0 = 0.0;
 #pragma unroll
-            for (int t = 0; t < RPL; t++) {
-                int sc = rl + LPC * t;
-                if (sc < nrow) g0 = fmax(g0, ST::mod(x[rowof(sc)]));
-            }
-            g0 = group_max<LPC>(g0);
-            double ad[RPL], tf[RPL], gb[RPL];
-#pragma unroll
-            for (int t = 0; t < RPL; t++) {
-                int sc = rl + LPC * t;
-                ad[t] = 1.0; tf[t] = 1.0; gb[t] = 0.0;
-                if (sc < nrow) {
-                    ad[t] = ST::mod(dof(sc));
-                    tf[t] = __dadd_rn(1.0, __ddiv_rn(cn[sc], ad[t]));
-                }
-            }
-            double gg = g0;
-            for (int sc = nmax - 1; sc >= 0; sc--) {
-                const int t = sc / LPC, rr = sc % LPC;
-                double own = 1.0;
-#pragma unroll
-                for (int t2 = 0; t2 < RPL; t2++)
-                    if (t2 == t) own = tf[t2];
-                double tfv = __shfl_sync(0xffffffffu, own, rr, LPC);
-                if (sc < nrow) {
-#pragma unroll
-                    for (int t2 = 0; t2 < RPL; t2++)
-                        if (t2 == t && rl == rr) gb[t2] = gg;
-                    gg = __dmul_rn(gg, tfv);
-                }
-            }
-            double M = 0.0;
-#pragma unroll
             for (int t = 0; t < RPL; t++)
-                if (rl + LPC * t < nrow) M = fmax(M, __ddiv_rn(gb[t], ad[t]));
-            M = group_max<LPC>(M);
-            guarded = active && !(M < kOmega && gg < kOmega);
+                if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
+            g0 = group_max<LPC>(g0);
+            double gg = g0;
+            bool okM = true;
+#pragma unroll
+            for (int t = RPL - 1; t >= 0; t--) {
+                if (t * LPC >= nmax) continue;
+#pragma unroll 1
+                for (int rr = LPC - 1; rr >= 0; rr--) {
+                    const int sc = t * LPC + rr;
+                    if (sc >= nmax) continue;
+                    double oadv;
+                    if constexpr (ST::cplx_) oadv = __shfl_sync(0xffffffffu, oad[t], rr, LPC);
+                    else oadv = __dmul_rn(kOmega, fabs(__shfl_sync(0xffffffffu, pv[t].d, rr, LPC)));
+                    const double ad = __dmul_rn(oadv, 0x1p-970);
+                    const double tf = __dadd_rn(1.0, __ddiv_rn(cn[sc], ad));
+                    if (sc < nrow) {
+                        okM = okM && gg < oadv;
+                        gg = __dmul_rn(gg, tf);
+                    }
+                }
+            }
+            guarded = active && !(okM && gg < kOmega);
             g = g0;
         }
 
-        T y[RPL];
-#pragma unroll
-        for (int t = 0; t < RPL; t++) {
-            int sc = rl + LPC * t;
-            y[t] = sc < nrow ? x[rowof(sc)] : ST::zero();
-        }
-
-        // ---- Trsv / guarded loop over solve rows sc = nmax-1 .. 0 ----
-        // Rescales "y := t y" of the guarded loop are applied LAZILY to the rows
-        // held in registers: y[] lives in a frame 2^pend above the true (oracle) frame; the
-        // chain values are brought to the true frame exactly (power-of-two scaling commutes
-        // with rounding), and the registers are flushed once pend reaches 12 bits, which keeps
-        // |y|, |x u| below DBL_MAX for max|U| <= 2^40 (R8).
-        // The step loop is a runtime loop (compact code: the I-cache, not the ALUs, bounded an
-        // unrolled version); the lane-local row slot t = sc / LPC is selected with predicates.
-        int kt = 0, pend = 0;
-        for (int sc = nmax - 1; sc >= 0; sc--) {
-            const int t = sc / LPC, rr = sc % LPC;
-            T own = ST::zero();
-#pragma unroll
-            for (int t2 = 0; t2 < RPL; t2++)
-                if (t2 == t) own = y[t2];
-            T yl = group_shfl<T, LPC>(own, rr);
-            if (sc < nrow) {
-                T dl = dof(sc);
-                Recip<T> rd;
-                rd.make(dl);
-                T xl;
-                if (SAFE && guarded) {
-                    if (pend) yl = scale_pw(yl, pow2i(-pend));         // true frame (exact)
-                    xl = rd.apply(yl);                                 // P:297 diagonal step
-                    // P:282-295 (R8): |y_l| >= Omega |d_l|.  Cheap conservative pre-test:
-                    // |y| <= 1.4143 max|y_c|, |d| >= max|d_c|.
-                    if (!(1.5 * maxabs(yl) < kOmega * maxabs(dl))) {
-                        double ay = ST::mod(yl), lim = __dmul_rn(kOmega, ST::mod(dl));
-                        if (ay >= lim) {
-                            int k = minpow2(ay, lim);
-                            pend += k;
-                            yl = ST::ldx(yl, -k);
-                            xl = rd.apply(yl);
-                            kt += k;
-                            g = ldexp(g, -k);
-                        }
-                    }
-                    double M = ST::mod(xl);
-                    g = __dadd_rn(g, __dmul_rn(M, cn[sc]));
-                    if (g >= kOmega) {
-                        int k = minpow2(g, kOmega);
-                        pend += k;
-                        xl = ST::ldx(xl, -k);
-                        kt += k;
-                        g = ldexp(g, -k);
-                    }
-                    if (pend >= 12) {                                  // flush registers -> true frame
-                        if (pend < 1000) {
-                            double p = pow2i(-pend);
-#pragma unroll
-                            for (int t2 = 0; t2 < RPL; t2++) y[t2] = scale_pw(y[t2], p);
-                        } else {
-#pragma unroll
-                            for (int t2 = 0; t2 < RPL; t2++) y[t2] = ST::ldx(y[t2], -pend);
-                        }
-                        pend = 0;
-                    } else if (pend) {
-                        xl = scale_pw(xl, pow2i(pend));                // register frame for the update
-                    }
-                } else {
-                    xl = rd.apply(yl);                                 // P:297 / P:82
-                }
-                // owner stores x_l; substitution within the block (P:315 / P:84): rows sc' < sc
-                const T *col = pk + int64_t(sc) * (sc - 1) / 2;
-#pragma unroll
-                for (int t2 = 0; t2 < RPL; t2++) {
-                    int i = rl + LPC * t2;
-                    if (i < sc) y[t2] = ST::fnms(y[t2], xl, col[i]);
-                    else if (i == sc) y[t2] = xl;
-                }
-            }
-        }
-        if (SAFE && pend) {
-#pragma unroll
-            for (int t2 = 0; t2 < RPL; t2++) y[t2] = ST::ldx(y[t2], -pend);
-        }
+        int kt = 0;
+        if (SAFE && __any_sync(0xffffffffu, guarded))
+            diag_rows<T, LPC, RPL, true>(y, pv, oad, pk, cn, rl, nrow, nmax, guarded, g, kt);
+        else
+            diag_rows<T, LPC, RPL, false>(y, pv, oad, pk, cn, rl, nrow, nmax, false, g, kt);
 
         if (SAFE) {
             int ej = 0;
@@ -286,20 +384,19 @@ __global__ void __launch_bounds__(512) diag_kernel(DiagArgs<T> a) {
             if (active) { ej = a.e[j]; Gj = a.G[j]; }
             if (kt > 0) {                                              // P:376-386, step (ii)
                 ej -= kt;
-                Gj = ldexp(Gj, -kt);
+                Gj = mulp2n(Gj, kt);
             }
             double xm = 0.0;
 #pragma unroll
-            for (int t = 0; t < RPL; t++) xm = fmax(xm, ST::mod(y[t]));
+            for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
             xm = group_max<LPC>(xm);
             Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
             int k3 = 0;
             if (Gj >= kOmega) {
-                k3 = minpow2(Gj, kOmega);
-#pragma unroll
-                for (int t = 0; t < RPL; t++) y[t] = ST::ldx(y[t], -k3);
+                k3 = minpow2_bits(Gj, kOmega);
+                scale_all<false>(y, k3);
                 ej -= k3;
-                Gj = ldexp(Gj, -k3);
+                Gj = mulp2n(Gj, k3);
             }
             if (active && rl == 0) {
                 a.e[j] = ej;

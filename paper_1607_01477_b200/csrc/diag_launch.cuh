@@ -5,9 +5,10 @@
 
 namespace mstrsm {
 namespace rt {
-template <typename T, int LPC, bool SAFE, int OP>
+template <typename T, int LPC, int RPL, bool SAFE, int OP>
 int launch_diag_t(const DiagArgs<T> &a) {
-    auto kern = diag_kernel<T, LPC, 16, SAFE, OP>;
+    auto kern = diag_kernel<T, LPC, RPL, SAFE, OP>;
+    constexpr int kMaxThreads = DiagThreads<T, RPL>::value;
     int nfull = int(a.hi - a.lo);
     size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T)));
     static bool attr_set = false;
@@ -16,12 +17,11 @@ int launch_diag_t(const DiagArgs<T> &a) {
         attr_set = true;
     }
     // warps per CTA chosen so that the grid covers every SM when there are enough columns
-    // (one CTA per SM when the staged block is large), at most 16 warps.
     const int G = 32 / LPC;
-    int occ1 = occupancy(kern, 512, smem);                 // CTAs per SM at 512 threads
+    int occ1 = occupancy(kern, kMaxThreads, smem);          // CTAs per SM at full size
     int64_t groups = cdiv(a.ncols, G);
     int64_t wpc = cdiv(groups, int64_t(g_num_sms) * std::max(occ1, 1));
-    wpc = std::max<int64_t>(1, std::min<int64_t>(16, wpc));
+    wpc = std::max<int64_t>(1, std::min<int64_t>(kMaxThreads / 32, wpc));
     int threads = int(wpc * 32);
     int occ = occupancy(kern, threads, smem);
     int grid = int(std::min<int64_t>(cdiv(groups, wpc), int64_t(occ) * g_num_sms));
@@ -33,12 +33,18 @@ int launch_diag_t(const DiagArgs<T> &a) {
     return 0;
 }
 
+// Lane layout: LPC lanes per column, RPL rows per lane (LPC * RPL >= n_b).  RPL = 16 packs
+// 32/LPC columns into a warp (the per-row scalar chain is shared by more columns); when the block
+// has too few active columns to give every SM a full CTA of such warps, RPL = 8 spreads each
+// column over twice the lanes instead (shorter substitution per lane, more warps).
 template <typename T, bool SAFE, int OP>
 int launch_diag(const DiagArgs<T> &a, int nb) {
-    if (nb <= 16) return launch_diag_t<T, 1, SAFE, OP>(a);
-    if (nb <= 32) return launch_diag_t<T, 2, SAFE, OP>(a);
-    if (nb <= 64) return launch_diag_t<T, 4, SAFE, OP>(a);
-    return launch_diag_t<T, 8, SAFE, OP>(a);
+    const int64_t full_wave = int64_t(g_num_sms) * (DiagThreads<T, 16>::value / 32);
+    auto few = [&](int lpc16) { return cdiv(a.ncols, 32 / lpc16) < full_wave; };
+    if (nb <= 16) return launch_diag_t<T, 1, 16, SAFE, OP>(a);
+    if (nb <= 32) return launch_diag_t<T, 2, 16, SAFE, OP>(a);
+    if (nb <= 64) return few(4) ? launch_diag_t<T, 8, 8, SAFE, OP>(a) : launch_diag_t<T, 4, 16, SAFE, OP>(a);
+    return few(8) ? launch_diag_t<T, 16, 8, SAFE, OP>(a) : launch_diag_t<T, 8, 16, SAFE, OP>(a);
 }
 
 }  // namespace rt
