@@ -111,6 +111,23 @@ __device__ __forceinline__ double warp_sum(double v) {
 // 2^d as a double for d >= -1074 (exact); callers handle smaller d via ldexp on the value.
 __device__ __forceinline__ double pow2(int d) { return ldexp(1.0, d); }
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// cp.async with zero fill when !valid (src-size 0).
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *dst, const void *src, bool valid) {
+    unsigned d = smem_u32(dst);
+    int sz = valid ? BYTES : 0;
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(BYTES), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // Block partition (R9).  op N: block b covers rows [max(0, m-(b+1)nb), m-b*nb).
 //                        op C: block b covers rows [b*nb, min(m, (b+1)nb)).
 struct Blk { int64_t lo, hi; };

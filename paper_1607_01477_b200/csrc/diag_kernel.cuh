@@ -43,17 +43,20 @@ struct DiagArgs {
     const double *P;               // panel sums, P[b]
     const double *delta;           // device scalar (R4)
     double *G; int *e; int *dblk; int *Etab;
+    int *fb_list; int *fb_count;   // columns handed to the synchronous fallback (safe variants)
+    int force_fb;                  // testing: hand every guarded column to the fallback
 };
 
+// Shared memory: the packed strictly upper triangle, the diagonal and cnl.
 __host__ __device__ inline int64_t diag_smem_bytes(int nfull, int esize) {
     int64_t pk = int64_t(nfull) * (nfull - 1) / 2 + 128;
     return pk * esize + int64_t(nfull) * esize + int64_t(nfull) * 8;
 }
 
-// Threads per CTA of an instantiation (its __launch_bounds__): 8 warps when each lane holds 16
-// rows (up to 255 registers), 12 (complex) or 16 (real) warps when it holds 8.
+// Threads per CTA of an instantiation (its __launch_bounds__): 10 warps when each lane holds 16
+// rows (up to 204 registers), 14 warps when it holds 8 (up to 146).
 template <typename T, int RPL> struct DiagThreads {
-    static constexpr int value = RPL >= 16 ? 256 : (S<T>::cplx_ ? 384 : 512);
+    static constexpr int value = RPL >= 16 ? 320 : 448;
 };
 
 // 2^k as a double for -1022 <= k <= 1023 (exact, built from the exponent bits).
@@ -89,6 +92,27 @@ __device__ __forceinline__ void scale_all(T (&y)[N], int k) {
 __device__ __forceinline__ double mulp2s(double v, int s) {
     const int h = s / 2;
     return __dmul_rn(__dmul_rn(v, pow2i(h)), pow2i(s - h));
+}
+// v * 2^s for any integer s as (at most) three exact power-of-two products.
+__device__ __forceinline__ double mulp2_any(double v, int s) {
+    const int s1 = max(-1022, min(1023, s));
+    const int s2 = max(-1022, min(1023, s - s1));
+    const int s3 = max(-1022, min(1023, s - s1 - s2));
+    return __dmul_rn(__dmul_rn(__dmul_rn(v, pow2i(s1)), pow2i(s2)), pow2i(s3));
+}
+template <typename T, int N>
+__device__ __forceinline__ void scale_all_any(T (&y)[N], int s) {
+    const int s1 = max(-1022, min(1023, s));
+    const int s2 = max(-1022, min(1023, s - s1));
+    const int s3 = max(-1022, min(1023, s - s1 - s2));
+    const double p1 = pow2i(s1), p2 = pow2i(s2), p3 = pow2i(s3);
+#pragma unroll
+    for (int t = 0; t < N; t++) {
+        if constexpr (S<T>::cplx_)
+            y[t] = make_double2(__dmul_rn(__dmul_rn(__dmul_rn(y[t].x, p1), p2), p3),
+                                __dmul_rn(__dmul_rn(__dmul_rn(y[t].y, p1), p2), p3));
+        else y[t] = __dmul_rn(__dmul_rn(__dmul_rn(y[t], p1), p2), p3);
+    }
 }
 __device__ __forceinline__ double maxabs(double v) { return fabs(v); }
 __device__ __forceinline__ double maxabs(cplx v) { return fmax(fabs(v.x), fabs(v.y)); }
@@ -191,10 +215,130 @@ __device__ __forceinline__ T group_shfl(T v, int src) {
         return __shfl_sync(0xffffffffu, v, src, LPC);
 }
 
-// The row loop of one column group.  GUARD: the guarded loop of Alg. 4 for the groups
-// with `guarded` set (others of the warp run the same substitution without rescales).
-template <typename T, int LPC, int RPL, bool GUARD>
-__device__ __forceinline__ void diag_rows(T (&y)[RPL], const Piv<T> (&pv)[RPL], const double (&oad)[RPL],
+// The substitution of one column group (Alg. 1; the unguarded branch of Alg. 4):
+// x_l = y_l / d_l, y(rows < l) -= x_l U(rows < l, l).  Every lane forms the quotient of its own
+// row of slot t and the owner's quotient is shuffled to the group, so the step-to-step chain is
+// one multiply, one shuffle and one fused update.
+template <typename T, int LPC, int RPL, typename PivF>
+__device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const T *__restrict__ pk,
+                                           int rl, int nrow, int nmax) {
+    typedef S<T> ST;
+#pragma unroll
+    for (int t = RPL - 1; t >= 0; t--) {
+        if (t * LPC >= nmax) continue;                                     // warp-uniform
+        Piv<T> pvt;                                                        // own row of slot t
+        pvt.make(pivot(t * LPC + rl));
+#pragma unroll 1
+        for (int rr = LPC - 1; rr >= 0; rr--) {
+            const int sc = t * LPC + rr;
+            if (sc >= nmax) continue;                                      // warp-uniform
+            const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);          // P:82 / P:297
+            const bool in = sc < nrow;
+            const T xr = in ? xl : ST::zero();
+            const T *col = pk + (sc * (sc - 1)) / 2;
+            if (rl < rr) y[t] = ST::fnms(y[t], xr, col[rl + LPC * t]);
+            else if (rl == rr && in) y[t] = xl;
+#pragma unroll
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, col[rl + LPC * t2]);
+        }
+    }
+}
+
+// Alg. 4's guarded loop with its decisions replayed LAG rows behind the substitution.
+//
+// The guarded loop only ever scales the whole vector by powers of two, so its
+// values are the unscaled substitution's values times 2^-K (K = exponents taken so far) exactly,
+// barring subnormals.  The registers therefore run the plain substitution, in a frame 2^pend
+// above the paper's (pend = exponents decided but not yet applied), and the decisions for row l
+// are taken LAG steps later from |x_l| (kept in shared memory), in the paper's order:
+//   |y_l| >= Omega |d_l|  <=>  |x_l| >= Omega (to rounding)  ->  k1 = minpow2(|x_l|, Omega)
+//   M = 2^-k1 |x_l|,  g = 2^-k1 g + M cnl(l),  g >= Omega  ->  k2 = minpow2(g, Omega)
+// with minpow2 against Omega = 2^970 read off the exponent bits.  The registers are brought to the
+// paper's frame one step after pend passes 12 bits; with the lag they stay within
+// ~2^(12 + growth of LAG+2 rows) of it.  A group whose registers stop being finite (growth beyond
+// 2^54 within that window, e.g. tiny pivots) returns false and is rerun by the synchronous loop.
+template <typename T, int LPC, int RPL, typename PivF>
+__device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__restrict__ pk,
+                                            const double *__restrict__ cn, int rl, int nrow, int nmax,
+                                            bool guarded, double g, int &kt) {
+    typedef S<T> ST;
+    constexpr int LAG = LPC < 4 ? LPC : 4;
+    // K: exponents decided so far; Fl: exponents applied to the registers so far
+    // (registers = unscaled * 2^-Fl, paper = unscaled * 2^-K).  Every LAG steps each lane of the
+    // chunk just solved records |x| of its own row of the slot (ax_cur) and the register frame it
+    // was read in (fl_cur); the previous slot's records move to ax_prev / fl_prev.
+    int K = 0, Fl = 0, pend_prev = 0;
+    double ax_cur = 0.0, ax_prev = 0.0;
+    int fl_cur = 0, fl_prev = 0;
+    bool nonfinite = false;
+    auto replay = [&](int sc2, double axr, int fls) {
+        const bool live = guarded && sc2 < nrow;
+        const double axt = __dmul_rn(axr, pow2i(fls - K));                 // paper frame
+        const bool t1 = live && axt >= kOmega;
+        const int k1 = t1 ? int(__double_as_longlong(axt) >> 52) - 1992 : 0;
+        const double M = t1 ? __dmul_rn(axt, pow2i(-k1)) : axt;
+        double gn = __dadd_rn(t1 ? __dmul_rn(g, pow2i(-k1)) : g, __dmul_rn(M, cn[sc2]));
+        const bool t2 = live && gn >= kOmega;
+        const int k2 = t2 ? int(__double_as_longlong(gn) >> 52) - 1992 : 0;
+        if (t2) gn = __dmul_rn(gn, pow2i(-k2));
+        g = live ? gn : g;
+        K += k1 + k2;
+    };
+#pragma unroll
+    for (int t = RPL - 1; t >= 0; t--) {
+        if (t * LPC >= nmax) continue;                                     // warp-uniform
+        ax_prev = ax_cur;
+        fl_prev = fl_cur;
+        Piv<T> pvt;                                                        // own row of slot t
+        pvt.make(pivot(t * LPC + rl));
+#pragma unroll 1
+        for (int rr = LPC - 1; rr >= 0; rr--) {
+            const int sc = t * LPC + rr;
+            if (sc >= nmax) continue;                                      // warp-uniform
+            const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);
+            const bool in = sc < nrow;
+            const T xr = in ? xl : ST::zero();
+            nonfinite = nonfinite || !(maxabs(xr) <= 1.7976931348623157e308);
+            const T *col = pk + (sc * (sc - 1)) / 2;
+            if (rl < rr) y[t] = ST::fnms(y[t], xr, col[rl + LPC * t]);
+            else if (rl == rr && in) y[t] = xl;
+#pragma unroll
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, col[rl + LPC * t2]);
+            if (sc + LAG < nmax) {                                         // warp-uniform
+                const bool prev = rr + LAG >= LPC;
+                const int src = (rr + LAG) & (LPC - 1);
+                const double axr = __shfl_sync(0xffffffffu, prev ? ax_prev : ax_cur, src, LPC);
+                const int fls = __shfl_sync(0xffffffffu, prev ? fl_prev : fl_cur, src, LPC);
+                replay(sc + LAG, axr, fls);
+            }
+            if (pend_prev >= 12) {                                         // lagged flush
+                scale_all<true>(y, pend_prev);
+                Fl += pend_prev;
+            }
+            pend_prev = K - Fl;
+            if ((rr & (LAG - 1)) == 0 && rl >= rr && rl < rr + LAG) {      // record the chunk
+                ax_cur = modv(y[t]);
+                fl_cur = Fl;
+            }
+        }
+    }
+#pragma unroll
+    for (int sc2 = LAG - 1; sc2 >= 0; sc2--) {
+        if (sc2 < nmax) {
+            const double axr = __shfl_sync(0xffffffffu, ax_cur, sc2, LPC);
+            const int fls = __shfl_sync(0xffffffffu, fl_cur, sc2, LPC);
+            replay(sc2, axr, fls);
+        }
+    }
+    if (K != Fl) scale_all<false>(y, K - Fl);
+    kt = K;
+    return !(guarded && nonfinite);
+}
+
+// The synchronous guarded loop (fallback when phase 1 overflows): Alg. 4 step by step
+// with the rescales applied lazily through pend.
+template <typename T, int LPC, int RPL, bool GUARD, typename PivF>
+__device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot,
                                           const T *__restrict__ pk, const double *__restrict__ cn,
                                           int rl, int nrow, int nmax, bool guarded, double &g, int &kt) {
     typedef S<T> ST;
@@ -202,18 +346,20 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], const Piv<T> (&pv)[RPL], 
 #pragma unroll
     for (int t = RPL - 1; t >= 0; t--) {
         if (t * LPC >= nmax) continue;                                     // warp-uniform
+        Piv<T> pvt;                                                        // own row of slot t
+        const T dt = pivot(t * LPC + rl);
+        pvt.make(dt);
+        const double oadt = __dmul_rn(kOmega, modv(dt));
 #pragma unroll 1
         for (int rr = LPC - 1; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
             if (sc >= nmax) continue;                                      // warp-uniform
             const bool in = sc < nrow;
             const T yl = group_shfl<T, LPC>(y[t], rr);                     // register frame
-            const Piv<T> p = pv[t].template shfl<LPC>(rr);
+            const Piv<T> p = pvt.template shfl<LPC>(rr);
             T xv = p.apply(yl);                                            // P:297 / P:82
             if constexpr (GUARD) {
-                double oadv;                                               // Omega |d_l|
-                if constexpr (ST::cplx_) oadv = __shfl_sync(0xffffffffu, oad[t], rr, LPC);
-                else oadv = __dmul_rn(kOmega, p.absd());
+                const double oadv = __shfl_sync(0xffffffffu, oadt, rr, LPC);   // Omega |d_l|
                 const double cnv = cn[sc];
                 const bool live = in && guarded;
                 // P:279-295 (R8): |y_l| >= Omega |d_l| in the true frame (pend <= 11 here: exact)
@@ -264,12 +410,16 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], const Piv<T> (&pv)[RPL], 
     }
 }
 
-template <typename T, int LPC, int RPL, bool SAFE, int OP>
+// One launch = one diagonal block for all (FB = false: columns [c0, c0 + ncols); FB = true: the
+// columns the main launch handed to the synchronous fallback) active columns.
+template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB>
 __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(DiagArgs<T> a) {
     typedef S<T> ST;
     constexpr int G = 32 / LPC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nfull = int(a.hi - a.lo);
+    const int64_t ncols = FB ? int64_t(*a.fb_count) : a.ncols;
+    if (ncols == 0) return;
     const int64_t npk = int64_t(nfull) * (nfull - 1) / 2 + 128;
     T *pk = reinterpret_cast<T *>(smem_raw);
     T *dg = pk + npk;
@@ -281,8 +431,9 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
         for (int idx = tid; idx < nfull * 128; idx += nth) {       // any blockDim
             const int cq = idx >> 7, rl = idx & 127;
             if (rl < cq) {
-                if (OP == 0) {      // U~(i,c) = U(lo+i, lo+c)
-                    pk[int64_t(cq) * (cq - 1) / 2 + rl] = a.U[(a.lo + rl) + (a.lo + cq) * a.ldu];
+                if (OP == 0) {      // U~(i,c) = U(lo+i, lo+c), asynchronous (waited for below)
+                    cp_async<sizeof(T)>(pk + int64_t(cq) * (cq - 1) / 2 + rl,
+                                        a.U + (a.lo + rl) + (a.lo + cq) * a.ldu, true);
                 } else {            // U~(i,c) = conj(U(hi-1-c, hi-1-i)); U column lo+cq, row lo+rl
                     int ci = nfull - 1 - cq, cc = nfull - 1 - rl;
                     pk[int64_t(cc) * (cc - 1) / 2 + ci] = ST::conj(a.U[(a.lo + rl) + (a.lo + cq) * a.ldu]);
@@ -295,8 +446,13 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
             dg[c] = OP == 0 ? u : ST::conj(u);
             cn[c] = SAFE ? a.cnl[row] : 0.0;
         }
+        cp_async_commit();
     }
-    __syncthreads();
+    __syncthreads();                                               // diagonal and cnl visible
+    // the first column group's loads and precheck overlap the staging of the triangle; every warp
+    // passes this second barrier exactly once (in its first iteration, or after the loop)
+    bool staged = false;
+    auto stage_wait = [&]() { cp_async_wait<0>(); __syncthreads(); staged = true; };
 
     const int lane = tid & 31, grp = lane / LPC, rl = lane % LPC;
     const int64_t wid = (int64_t(blockIdx.x) * nth + tid) >> 5;
@@ -304,10 +460,10 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
     const double delta = SAFE ? *a.delta : 0.0;
     const double Pb = SAFE ? a.P[a.b] : 0.0;
 
-    for (int64_t base = wid * G; base < a.ncols; base += nw * G) {
+    for (int64_t base = wid * G; base < ncols; base += nw * G) {
         const int64_t q = base + grp;
-        const bool valid = q < a.ncols;
-        const int64_t j = a.c0 + (valid ? q : 0);
+        const bool valid = q < ncols;
+        const int64_t j = FB ? (valid ? int64_t(a.fb_list[q]) : a.c0) : a.c0 + (valid ? q : 0);
         const int64_t r = valid ? ((OP == 0 && a.rowend) ? a.rowend[j] : a.m) : 0;
         const bool active = valid && r > a.lo;
         if (SAFE && valid && !active && rl == 0) a.dblk[j] = 0;     // inactive column: no rescale
@@ -320,63 +476,79 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
         if (OP == 1) sh = ST::conj(sh);
         T *x = a.B + j * a.ldb;
         auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
-
-        // ---- load the rows, per-row pivot data (d_l = U(l,l) - s_j; delta for an exact zero,
-        //      P:231-234), Omega |d_l| ----
+        auto pivot = [&](int sc) -> T {                               // d_l = U(l,l) - s_j
+            T dd = sc < nrow ? ST::sub(dg[sc], sh) : ST::real(1.0);
+            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);        // P:231-234
+            return dd;
+        };
+        // ---- load the rows ----
         T y[RPL];
-        Piv<T> pv[RPL];
-        double oad[RPL];
 #pragma unroll
         for (int t = 0; t < RPL; t++) {
             const int sc = rl + LPC * t;
-            const bool in = sc < nrow;
-            y[t] = in ? x[rowof(sc)] : ST::zero();
-            T dd = in ? ST::sub(dg[sc], sh) : ST::real(1.0);
-            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
-            pv[t].make(dd);
-            oad[t] = SAFE && ST::cplx_ ? __dmul_rn(kOmega, modv(dd)) : 0.0;
+            y[t] = sc < nrow ? x[rowof(sc)] : ST::zero();
         }
 
         bool guarded = false;
-        double g = 0.0;
+        double g0 = 0.0;
         if (SAFE) {
-            // ---- precheck, eqs. (4)-(5), in the oracle's order:
-            //      M = max_l g_l/|d_l| (tested as g_l < Omega |d_l|), g_{l-1} = g_l (1 + cnl_l/|d_l|),
-            //      g_top = ||y(I1)||_inf ----
-            double g0 = 0.0;
+            // ---- precheck, eqs. (4)-(5): g_top = ||y(I1)||_inf, g_{l-1} = g_l (1 +
+            //      cnl_l/|d_l|), M = max_l g_l/|d_l| (tested as g_l < Omega |d_l|).  The products
+            //      g_l = g_top prod_{l' > l} tf_l' are formed slot by slot with a suffix scan over
+            //      the LPC lanes (rounding order differs from the sequential product at the ulp
+            //      level, R24) ----
 #pragma unroll
             for (int t = 0; t < RPL; t++)
                 if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
             g0 = group_max<LPC>(g0);
-            double gg = g0;
+            double carry = g0;                                         // g at the top of the slot
             bool okM = true;
 #pragma unroll
             for (int t = RPL - 1; t >= 0; t--) {
                 if (t * LPC >= nmax) continue;
-#pragma unroll 1
-                for (int rr = LPC - 1; rr >= 0; rr--) {
-                    const int sc = t * LPC + rr;
-                    if (sc >= nmax) continue;
-                    double oadv;
-                    if constexpr (ST::cplx_) oadv = __shfl_sync(0xffffffffu, oad[t], rr, LPC);
-                    else oadv = __dmul_rn(kOmega, fabs(__shfl_sync(0xffffffffu, pv[t].d, rr, LPC)));
-                    const double ad = __dmul_rn(oadv, 0x1p-970);
-                    const double tf = __dadd_rn(1.0, __ddiv_rn(cn[sc], ad));
-                    if (sc < nrow) {
-                        okM = okM && gg < oadv;
-                        gg = __dmul_rn(gg, tf);
-                    }
+                const int sc = t * LPC + rl;
+                const bool in = sc < nrow;
+                const double ad = modv(pivot(sc));
+                const double tf = in ? __dadd_rn(1.0, __ddiv_rn(cn[sc], ad)) : 1.0;
+                double suf = tf;                                       // inclusive suffix product
+#pragma unroll
+                for (int o = 1; o < LPC; o <<= 1) {
+                    const double v = __shfl_down_sync(0xffffffffu, suf, o, LPC);
+                    if (rl + o < LPC) suf = __dmul_rn(suf, v);
                 }
+                double exc = __shfl_down_sync(0xffffffffu, suf, 1, LPC);   // rows above, this slot
+                if (rl == LPC - 1) exc = 1.0;
+                const double gl = __dmul_rn(carry, exc);
+                okM = okM && (!in || gl < __dmul_rn(kOmega, ad));
+                carry = __dmul_rn(carry, __shfl_sync(0xffffffffu, suf, 0, LPC));
             }
-            guarded = active && !(okM && gg < kOmega);
-            g = g0;
+#pragma unroll
+            for (int o = 1; o < LPC; o <<= 1) {                       // group AND (every lane shuffles)
+                const bool other = __shfl_xor_sync(0xffffffffu, okM, o, LPC);
+                okM = okM && other;
+            }
+            guarded = active && !(okM && carry < kOmega);
         }
 
+        // ---- the row loop ----
+        if (!staged) stage_wait();
         int kt = 0;
-        if (SAFE && __any_sync(0xffffffffu, guarded))
-            diag_rows<T, LPC, RPL, true>(y, pv, oad, pk, cn, rl, nrow, nmax, guarded, g, kt);
-        else
-            diag_rows<T, LPC, RPL, false>(y, pv, oad, pk, cn, rl, nrow, nmax, false, g, kt);
+        bool handed = false;
+        if constexpr (FB) {
+            double g = g0;
+            diag_rows<T, LPC, RPL, true>(y, pivot, pk, cn, rl, nrow, nmax, guarded, g, kt);
+        } else {
+            if (SAFE && __any_sync(0xffffffffu, guarded)) {
+                const bool ok = diag_lagged<T, LPC, RPL>(y, pivot, pk, cn, rl, nrow, nmax, guarded, g0, kt) &&
+                                !(a.force_fb && guarded);
+                if (!ok) {                                             // hand the column over
+                    handed = true;
+                    if (rl == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = int(j);
+                }
+            } else {
+                diag_subst<T, LPC, RPL>(y, pivot, pk, rl, nrow, nmax);
+            }
+        }
 
         if (SAFE) {
             int ej = 0;
@@ -398,7 +570,7 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
                 ej -= k3;
                 Gj = mulp2n(Gj, k3);
             }
-            if (active && rl == 0) {
+            if (active && rl == 0 && !handed) {
                 a.e[j] = ej;
                 a.G[j] = Gj;
                 a.dblk[j] = -(kt + k3);
@@ -408,9 +580,10 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
 #pragma unroll
         for (int t = 0; t < RPL; t++) {
             int sc = rl + LPC * t;
-            if (sc < nrow) x[rowof(sc)] = y[t];
+            if (sc < nrow && !handed) x[rowof(sc)] = y[t];
         }
     }
+    if (!staged) stage_wait();
 }
 
 }  // namespace mstrsm

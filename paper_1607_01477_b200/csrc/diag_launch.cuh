@@ -1,32 +1,34 @@
 // diag_launch.cuh -- launcher of the diagonal-block kernel (a.3/a.4); included by the
-// diag_{d,z}{N,C}.cu units, each of which instantiates one (scalar, op) pair.
+// diag_{d,z}{N,C}_{plain,safe}.cu units, each of which instantiates one (scalar, op, variant).
 #pragma once
+#include <stdio.h>
+
 #include "runtime.cuh"
 
 namespace mstrsm {
 namespace rt {
-template <typename T, int LPC, int RPL, bool SAFE, int OP>
-int launch_diag_t(const DiagArgs<T> &a) {
-    auto kern = diag_kernel<T, LPC, RPL, SAFE, OP>;
+template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB>
+int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
+    auto kern = diag_kernel<T, LPC, RPL, SAFE, OP, FB>;
     constexpr int kMaxThreads = DiagThreads<T, RPL>::value;
-    int nfull = int(a.hi - a.lo);
-    size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T)));
+    constexpr int G = 32 / LPC;
+    const int nfull = int(a.hi - a.lo);
     static bool attr_set = false;
     if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_set = true;
     }
     // warps per CTA chosen so that the grid covers every SM when there are enough columns
-    const int G = 32 / LPC;
-    int occ1 = occupancy(kern, kMaxThreads, smem);          // CTAs per SM at full size
-    int64_t groups = cdiv(a.ncols, G);
+    const size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T)));
+    int occ1 = occupancy(kern, kMaxThreads, smem);
+    int64_t groups = cdiv(ncols_max, G);
     int64_t wpc = cdiv(groups, int64_t(g_num_sms) * std::max(occ1, 1));
     wpc = std::max<int64_t>(1, std::min<int64_t>(kMaxThreads / 32, wpc));
-    int threads = int(wpc * 32);
+    const int threads = int(wpc * 32);
     int occ = occupancy(kern, threads, smem);
     int grid = int(std::min<int64_t>(cdiv(groups, wpc), int64_t(occ) * g_num_sms));
     if (grid < 1) grid = 1;
-    double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
+    double fl = FB ? 0.0 : double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
     ProfScope ps(PK_DIAG, fl);
     kern<<<grid, threads, smem, g_stream>>>(a);
     CK_LAUNCH("diag_kernel");
@@ -37,14 +39,30 @@ int launch_diag_t(const DiagArgs<T> &a) {
 // 32/LPC columns into a warp (the per-row scalar chain is shared by more columns); when the block
 // has too few active columns to give every SM a full CTA of such warps, RPL = 8 spreads each
 // column over twice the lanes instead (shorter substitution per lane, more warps).
+// Safe variants follow the main launch with the synchronous fallback launch, which exits at once
+// unless the main launch handed columns over (device-side count, no host synchronisation).
+template <typename T, int LPC, int RPL, bool SAFE, int OP>
+int launch_diag_pair(const DiagArgs<T> &a) {
+    if (int rc = launch_diag_k<T, LPC, RPL, SAFE, OP, false>(a, a.ncols)) return rc;
+    if (g_debug_sync) {
+        cudaError_t e = cudaStreamSynchronize(g_stream);
+        int cnt = -1;
+        if (SAFE) cudaMemcpy(&cnt, a.fb_count, 4, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[mstrsm debug] diag<%d,%d> block %lld main done (%s), ncols %lld, handed %d\n", LPC, RPL,
+                (long long)a.b, cudaGetErrorString(e), (long long)a.ncols, cnt);
+    }
+    if (SAFE) return launch_diag_k<T, LPC, RPL, SAFE, OP, true>(a, std::min<int64_t>(a.ncols, int64_t(g_num_sms) * 32));
+    return 0;
+}
+
 template <typename T, bool SAFE, int OP>
 int launch_diag(const DiagArgs<T> &a, int nb) {
     const int64_t full_wave = int64_t(g_num_sms) * (DiagThreads<T, 16>::value / 32);
     auto few = [&](int lpc16) { return cdiv(a.ncols, 32 / lpc16) < full_wave; };
-    if (nb <= 16) return launch_diag_t<T, 1, 16, SAFE, OP>(a);
-    if (nb <= 32) return launch_diag_t<T, 2, 16, SAFE, OP>(a);
-    if (nb <= 64) return few(4) ? launch_diag_t<T, 8, 8, SAFE, OP>(a) : launch_diag_t<T, 4, 16, SAFE, OP>(a);
-    return few(8) ? launch_diag_t<T, 16, 8, SAFE, OP>(a) : launch_diag_t<T, 8, 16, SAFE, OP>(a);
+    if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP>(a);
+    if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP>(a);
+    if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP>(a) : launch_diag_pair<T, 4, 16, SAFE, OP>(a);
+    return few(8) ? launch_diag_pair<T, 16, 8, SAFE, OP>(a) : launch_diag_pair<T, 8, 16, SAFE, OP>(a);
 }
 
 }  // namespace rt

@@ -33,6 +33,7 @@ struct Work {
     void *base = nullptr;
     double *cnl = nullptr, *part = nullptr, *P = nullptr, *delta = nullptr, *G = nullptr;
     int *e = nullptr, *dblk = nullptr, *Etab = nullptr;
+    int *fb_list = nullptr, *fb_count = nullptr;   // diag fallback: column list, count per block
     int64_t *rowend = nullptr;
     void *shifts = nullptr;            // trevc: gathered diag(T)
     cudaStream_t st = nullptr;
@@ -47,6 +48,7 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
     size_t o_cnl = take(m * 8), o_part = take(m * 8), o_P = take(std::max<int64_t>(nblk, 1) * 8),
            o_delta = take(8), o_G = take(n * 8), o_e = take(n * 4), o_d = take(n * 4),
            o_E = take(std::max<int64_t>(nblk, 1) * n * 4), o_r = take(need_rowend ? n * 8 : 0),
+           o_fl = take(n * 4), o_fc = take(std::max<int64_t>(nblk, 1) * 4),
            o_s = take(need_shifts ? n * sizeof(T) : 0);
     w.st = g_stream;
     CK(cudaMallocAsync(&w.base, off, g_stream));
@@ -54,6 +56,7 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
     w.cnl = (double *)(b + o_cnl); w.part = (double *)(b + o_part); w.P = (double *)(b + o_P);
     w.delta = (double *)(b + o_delta); w.G = (double *)(b + o_G); w.e = (int *)(b + o_e);
     w.dblk = (int *)(b + o_d); w.Etab = (int *)(b + o_E);
+    w.fb_list = (int *)(b + o_fl); w.fb_count = (int *)(b + o_fc);
     w.rowend = need_rowend ? (int64_t *)(b + o_r) : nullptr;
     w.shifts = need_shifts ? (void *)(b + o_s) : nullptr;
     return 0;
@@ -105,6 +108,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
                   T *B, int64_t ldb, int64_t n, const int64_t *rowend_dev,
                   const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w) {
     int64_t nblk = cdiv(m, nb);
+    if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));   // diag fallback counts
     for (int64_t b = 0; b < nblk; b++) {
         Blk bl = block_rows(op, m, nb, b);
         int64_t c0 = 0;
@@ -114,15 +118,21 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         }
         int64_t ncols = n - c0;
         if (ncols <= 0) continue;
-        DiagArgs<T> a;
+        DiagArgs<T> a{};
         a.U = U; a.ldu = ldu; a.m = m; a.shifts = shifts; a.sstride = sstride;
         a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
         a.rowend = op == 0 ? rowend_dev : nullptr;
         a.lo = bl.lo; a.hi = bl.hi; a.b = b;
         a.cnl = w.cnl; a.P = w.P; a.delta = w.delta;
         a.G = w.G; a.e = w.e; a.dblk = w.dblk; a.Etab = w.Etab;
+        a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
+        a.force_fb = g_diag_force_fb;
         int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
         if (rc) return rc;
+        if (g_debug_sync) {
+            cudaError_t e = cudaStreamSynchronize(g_stream);
+            fprintf(stderr, "[mstrsm debug] block %lld diag done (%s)\n", (long long)b, cudaGetErrorString(e));
+        }
         int64_t M = op == 0 ? bl.lo : m - bl.hi;
         if (M <= 0) continue;
         GemmArgs<T> g;
@@ -134,6 +144,10 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         g.dblk = SAFE ? w.dblk : nullptr;
         rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g);
         if (rc) return rc;
+        if (g_debug_sync) {
+            cudaError_t e = cudaStreamSynchronize(g_stream);
+            fprintf(stderr, "[mstrsm debug] block %lld gemm done (%s)\n", (long long)b, cudaGetErrorString(e));
+        }
     }
     return 0;
 }

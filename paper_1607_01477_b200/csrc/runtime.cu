@@ -1,5 +1,6 @@
 // runtime.cu -- definitions of the library-wide runtime state (see runtime.cuh).
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <mutex>
 
@@ -13,6 +14,8 @@ std::atomic<int64_t> g_launches{0};
 int *g_flag = nullptr;                 // device: non-finite input seen
 char g_errmsg[512] = "no error";
 int g_num_sms = 0;
+bool g_debug_sync = getenv("MSTRSM_DEBUG_SYNC") != nullptr;   // synchronise + log after each diag launch
+int g_diag_force_fb = getenv("MSTRSM_DIAG_FORCE_FALLBACK") != nullptr;   // testing: synchronous diag path
 static std::mutex g_mu;
 bool g_prof = false;
 std::vector<ProfRec> g_prof_recs;

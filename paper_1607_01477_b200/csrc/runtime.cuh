@@ -20,6 +20,8 @@ extern std::atomic<int64_t> g_launches;
 extern int *g_flag;
 extern char g_errmsg[512];
 extern int g_num_sms;
+extern bool g_debug_sync;
+extern int g_diag_force_fb;
 
 int set_cuda_error(cudaError_t e, const char *where);
 int ensure_init();
