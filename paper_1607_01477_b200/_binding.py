@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmstrsm.so")
+LIB_PATH = os.environ.get("MSTRSM_LIB", os.path.join(_HERE, "libmstrsm.so"))   # override: experiments only
 _lib = None
 
 c_i64, c_int, c_dbl, c_vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p

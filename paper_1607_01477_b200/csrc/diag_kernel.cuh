@@ -255,14 +255,21 @@ __device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const T *__r
 //   M = 2^-k1 |x_l|,  g = 2^-k1 g + M cnl(l),  g >= Omega  ->  k2 = minpow2(g, Omega)
 // with minpow2 against Omega = 2^970 read off the exponent bits.  The registers are brought to the
 // paper's frame one step after pend passes 12 bits; with the lag they stay within
-// ~2^(12 + growth of LAG+2 rows) of it.  A group whose registers stop being finite (growth beyond
+// ~2^(12 + growth of LAG+2 rows) of it (LAG = 2, flush at 12 bits: no c5 column overflows; LAG = 4
+// or a 20-bit flush sent 248 / 307906 c5 columns to the fallback, measured).  A group whose registers stop being finite (growth beyond
 // 2^54 within that window, e.g. tiny pivots) returns false and is rerun by the synchronous loop.
 template <typename T, int LPC, int RPL, typename PivF>
 __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__restrict__ pk,
                                             const double *__restrict__ cn, int rl, int nrow, int nmax,
                                             bool guarded, double g, int &kt) {
     typedef S<T> ST;
-    constexpr int LAG = LPC < 4 ? LPC : 4;
+#ifndef MSTRSM_DIAG_LAG
+#define MSTRSM_DIAG_LAG 2
+#endif
+#ifndef MSTRSM_DIAG_FLUSH
+#define MSTRSM_DIAG_FLUSH 12
+#endif
+    constexpr int LAG = LPC < MSTRSM_DIAG_LAG ? LPC : MSTRSM_DIAG_LAG;
     // K: exponents decided so far; Fl: exponents applied to the registers so far
     // (registers = unscaled * 2^-Fl, paper = unscaled * 2^-K).  Every LAG steps each lane of the
     // chunk just solved records |x| of its own row of the slot (ax_cur) and the register frame it
@@ -298,7 +305,6 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);
             const bool in = sc < nrow;
             const T xr = in ? xl : ST::zero();
-            nonfinite = nonfinite || !(maxabs(xr) <= 1.7976931348623157e308);
             const T *col = pk + (sc * (sc - 1)) / 2;
             if (rl < rr) y[t] = ST::fnms(y[t], xr, col[rl + LPC * t]);
             else if (rl == rr && in) y[t] = xl;
@@ -311,7 +317,7 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
                 const int fls = __shfl_sync(0xffffffffu, prev ? fl_prev : fl_cur, src, LPC);
                 replay(sc + LAG, axr, fls);
             }
-            if (pend_prev >= 12) {                                         // lagged flush
+            if (pend_prev >= MSTRSM_DIAG_FLUSH) {                          // lagged flush
                 scale_all<true>(y, pend_prev);
                 Fl += pend_prev;
             }
@@ -319,6 +325,7 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
             if ((rr & (LAG - 1)) == 0 && rl >= rr && rl < rr + LAG) {      // record the chunk
                 ax_cur = modv(y[t]);
                 fl_cur = Fl;
+                nonfinite |= !(ax_cur <= 1.7976931348623157e308);         // every solved row passes here
             }
         }
     }
@@ -332,6 +339,8 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
     }
     if (K != Fl) scale_all<false>(y, K - Fl);
     kt = K;
+#pragma unroll
+    for (int o = 1; o < LPC; o <<= 1) nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o, LPC);
     return !(guarded && nonfinite);
 }
 
