@@ -87,6 +87,17 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
     const int64_t n0 = int64_t(blockIdx.y) * BN;
     const int nk = (g.K + BK - 1) / BK;
 
+    // per-column epilogue scale 2^{d_j} of this tile (the lazy xSCAL of P:378-380 / P:398), read
+    // from dblk once per CTA while the pipeline fills
+    __shared__ double s_sc[BN];
+    __shared__ int s_d[BN];
+    if (tid < BN) {
+        const int64_t gj = n0 + tid;
+        const int d = (g.dblk && gj < g.N) ? g.dblk[g.col0 + gj] : 0;
+        s_d[tid] = d;
+        s_sc[tid] = d >= -1022 ? __longlong_as_double((long long)(1023 + d) << 52) : 0.0;
+    }
+
     auto stageA = [&](int s) { return smem + s * gemm_stage_elems<T>(); };
     auto stageX = [&](int s) { return smem + s * gemm_stage_elems<T>() + BM * BK; };
 
@@ -227,35 +238,37 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
     cp_async_wait<0>();
     __syncthreads();
 
-    // ---- epilogue: C = 2^d C - acc (C from shared memory) ----
+    // ---- epilogue: C = 2^d C - acc (C from shared memory); one FMA per element (2^0 = 1 is
+    //      exact), bounds checks only on edge tiles, ldexp only for d < -1022 (subnormal scale) ----
     const T *Cs = smem + ((nk + wn) % kGemmStages) * gemm_stage_elems<T>();   // this warp's half
+    const bool full = m0 + BM <= g.M && n0 + BN <= g.N;
 #pragma unroll
     for (int jn = 0; jn < NI; jn++) {
 #pragma unroll
         for (int c = 0; c < 2; c++) {
             const int colh = jn * 8 + tq * 2 + c;
-            int64_t gj = n0 + wn * WN + colh;
-            if (gj >= g.N) continue;
-            int d = g.dblk ? g.dblk[g.col0 + gj] : 0;
-            double sc = d >= -1022 ? ldexp(1.0, d) : 0.0;
+            const int64_t gj = n0 + wn * WN + colh;
+            const double sc = s_sc[wn * WN + colh];
+            const bool tiny = s_d[wn * WN + colh] < -1022;
             T *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
 #pragma unroll
             for (int i = 0; i < MI; i++) {
                 const int row = wm * WM + i * 8 + gq;
-                int64_t gi = m0 + row;
-                if (gi >= g.M) continue;
-                T old = Cs[offC(row, colh)];
+                const int64_t gi = m0 + row;
+                const T old = Cs[offC(row, colh)];
                 T nv;
                 if constexpr (CPX) {
-                    if (d == 0) { nv.x = old.x - accR[i][jn][c]; nv.y = old.y - accI[i][jn][c]; }
-                    else if (d >= -1022) { nv.x = fma(old.x, sc, -accR[i][jn][c]); nv.y = fma(old.y, sc, -accI[i][jn][c]); }
-                    else { nv.x = ldexp(old.x, d) - accR[i][jn][c]; nv.y = ldexp(old.y, d) - accI[i][jn][c]; }
+                    nv.x = fma(old.x, sc, -accR[i][jn][c]);
+                    nv.y = fma(old.y, sc, -accI[i][jn][c]);
                 } else {
-                    if (d == 0) nv = old - accR[i][jn][c];
-                    else if (d >= -1022) nv = fma(old, sc, -accR[i][jn][c]);
+                    nv = fma(old, sc, -accR[i][jn][c]);
+                }
+                if (tiny) {
+                    const int d = s_d[wn * WN + colh];
+                    if constexpr (CPX) { nv.x = ldexp(old.x, d) - accR[i][jn][c]; nv.y = ldexp(old.y, d) - accI[i][jn][c]; }
                     else nv = ldexp(old, d) - accR[i][jn][c];
                 }
-                colp[gi] = nv;
+                if (full || (gi < g.M && gj < g.N)) colp[gi] = nv;
             }
         }
     }
