@@ -104,6 +104,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             if ((local & 1) != q) continue;
             const int64_t m0 = int64_t(tile % tiles_m) * BM, n0 = int64_t(tile / tiles_m) * BN;
             const bool vm0 = m0 + lane < g.M, vm1 = m0 + lane + 32 < g.M;
+            {   // warm L2 with this tile's C (read by the C-half slots after the k-tiles)
+                const int64_t rows = g.M - m0 < BM ? g.M - m0 : int64_t(BM);
+#pragma unroll
+                for (int c2 = 0; c2 < BN / 32; c2++) {
+                    const int64_t gj = n0 + c2 * 32 + lane;
+                    if (gj < g.N && rows > 0) {
+                        // 16-byte aligned start and length (bulk-copy rules)
+                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(g.B + (g.c_r0 + m0) + (g.col0 + gj) * g.ldb);
+                        const uintptr_t al = a0 & ~uintptr_t(15);
+                        const unsigned len = unsigned((a0 - al + rows * ESZ + 15) & ~uintptr_t(15));
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(al), "r"(len) : "memory");
+                    }
+                }
+            }
 #pragma unroll 1
             for (int kt = 0; kt < nk; kt++) {
                 T *As = next_slot(), *Xs = As + BM * BK;
@@ -238,8 +252,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             for (int c = 0; c < 2; c++) {
                 const int colh = jn * 8 + tq * 2 + c;
                 const int64_t gj = n0 + wn * WN + colh;
-                const int d = g.dblk ? s_d[grp][wn * WN + colh] : 0;
-                const double sc = d >= -1022 ? __longlong_as_double((long long)(1023 + d) << 52) : 0.0;
+                // 2^d as f1 * f2 with both factors normal doubles (d < -1022 happens when a column
+                // underflows; the scale is then applied in two exact steps, no ldexp)
+                const int d = max(g.dblk ? s_d[grp][wn * WN + colh] : 0, -2044);
+                const bool lo = d < -1022;
+                const double f1 = lo ? __longlong_as_double((long long)(1023 + d + 1022) << 52) : 1.0;
+                const double f2 = __longlong_as_double((long long)(1023 + (lo ? -1022 : d)) << 52);
                 T *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
 #pragma unroll
                 for (int i = 0; i < MI; i++) {
@@ -248,12 +266,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
                     const T old = Cs[offC(row, colh)];
                     T nv;
                     if constexpr (CPX) {
-                        nv.x = fma(old.x, sc, -accR[i][jn][c]);
-                        nv.y = fma(old.y, sc, -accI[i][jn][c]);
-                        if (d < -1022) { nv.x = ldexp(old.x, d) - accR[i][jn][c]; nv.y = ldexp(old.y, d) - accI[i][jn][c]; }
+                        nv.x = fma(__dmul_rn(old.x, f1), f2, -accR[i][jn][c]);
+                        nv.y = fma(__dmul_rn(old.y, f1), f2, -accI[i][jn][c]);
                     } else {
-                        nv = fma(old, sc, -accR[i][jn][c]);
-                        if (d < -1022) nv = ldexp(old, d) - accR[i][jn][c];
+                        nv = fma(__dmul_rn(old, f1), f2, -accR[i][jn][c]);
                     }
                     if (full || (gi < g.M && gj < g.N)) colp[gi] = nv;
                 }
