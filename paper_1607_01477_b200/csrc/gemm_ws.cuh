@@ -8,11 +8,14 @@
 //   * warpgroups 1 and 2 are two consumer groups that take alternate tiles (2x2 warps of 32x32 per
 //     64x64 tile); one group's epilogue (C read from global, 2^d scale, store) overlaps the other
 //     group's DMMA mainloop;
-//   * warps 0 and 1 of warpgroup 0 are the producers, one per consumer group: each streams the A/X
-//     k-tiles of its group's tiles, in order, into its own kWsRingStages-deep shared-memory ring with
+//   * warpgroup 0 holds the producers, two warps per consumer group: they stream the A/X k-tiles
+//     of the group's tiles, in order, into the group's own kWsRingStages-deep shared-memory ring with
 //     cp.async and signals each stage's "full" mbarrier through cp.async.mbarrier.arrive; the group
 //     releases a stage through its "empty" mbarrier as soon as its four warps have read it, so the
-//     producer runs ahead across tile boundaries (no __syncthreads anywhere in the loop).  One
+//     producer runs ahead across tile boundaries (no __syncthreads anywhere in the loop).  After a
+//     tile's K/8 k-tiles the ring carries the tile's C in four 16-column quarters (with the d_j),
+//     released quarter by quarter by the epilogue, so the next tile's first k-tiles are already
+//     in flight while the epilogue runs.  One
 //     ring per group keeps every barrier's phases consumed in order (a shared ring would let one
 //     group wait on a phase two rounds ahead, which a parity wait cannot tell apart).  This is what the one-tile-per-CTA kernel could not hide: with K = 128 a tile
 //     has only 8 k-tiles, so pipeline fill and epilogue were a third of its time.
@@ -21,8 +24,13 @@
 
 namespace mstrsm {
 
-constexpr int kWsRingStages = 3;                   // per consumer group
+constexpr int kWsRingStages = 6;                   // per consumer group
 constexpr int kWsStages = 2 * kWsRingStages;
+constexpr int kWsBK = 8;                           // k-tile depth (a 64x64 tile has K/8 k-tiles)
+
+// stage = A tile (BM x BK) + X tile (BN x BK); a C quarter (BM x 16 columns) has the same size
+template <typename T>
+__host__ __device__ constexpr int gemm_ws_stage_elems() { return (GemmCfg<T>::BM + GemmCfg<T>::BN) * kWsBK; }
 // 12 warps = 3 warpgroups: producer WG (setmaxnreg 56) + 2 consumer WGs (setmaxnreg 224).  Each SM
 // sub-partition holds one warp of every WG: 56 + 2 * 224 registers x 32 lanes fits its 16K file.
 constexpr int kWsThreads = 384;
@@ -30,7 +38,7 @@ constexpr int kWsProducerRegs = 56, kWsConsumerRegs = 224;
 
 template <typename T>
 __host__ __device__ constexpr int gemm_ws_smem_bytes() {
-    return kWsStages * gemm_stage_elems<T>() * int(sizeof(T));
+    return kWsStages * gemm_ws_stage_elems<T>() * int(sizeof(T));
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t *b, int count) {
@@ -52,33 +60,44 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, int parity) {
     } while (!done);
 }
 
+// swizzled positions (element units) inside a stage
+//  A, op N: (k, m) of a BK x BM tile, m contiguous (16-B slots rotated by k)
+template <typename T> __device__ __forceinline__ int ws_offA_km(int k, int mm) {
+    if constexpr (S<T>::cplx_) return k * 64 + (mm ^ ((k & 3) << 1));
+    else return k * 64 + (mm ^ ((k & 3) << 2));
+}
+//  A, op C and X: (r, k) of a 64 x BK tile, k contiguous (BK = 8)
+template <typename T> __device__ __forceinline__ int ws_offRK(int r, int k) {
+    if constexpr (S<T>::cplx_) return r * kWsBK + (k ^ ((r & 1) << 2));
+    else return r * kWsBK + (k ^ ((r & 3) << 1));
+}
+//  C quarter: (row, column) of a 64 x 16 block, rows contiguous
+template <typename T> __device__ __forceinline__ int ws_offC(int row, int colq) {
+    if constexpr (S<T>::cplx_) return colq * 64 + (row ^ (((colq >> 1) & 3) << 1));
+    else return colq * 64 + (row ^ (((colq >> 1) & 3) << 2));
+}
+
 template <typename T, bool OPC>
 __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, int tiles_m, int ntiles) {
-    constexpr int BM = GemmCfg<T>::BM, BN = GemmCfg<T>::BN, BK = GemmCfg<T>::BK;
+    constexpr int BM = GemmCfg<T>::BM, BN = GemmCfg<T>::BN, BK = kWsBK;
     constexpr int WM = GemmCfg<T>::WM, WN = GemmCfg<T>::WN;
     constexpr int MI = WM / 8, NI = WN / 8;
     constexpr bool CPX = S<T>::cplx_;
     constexpr int ESZ = sizeof(T);
-    constexpr int SE = gemm_stage_elems<T>();
-    static_assert(BM == 64 && BN == 64 && BK == 16 && WN == 32, "addressing below assumes 64x64x16 tiles");
-    static_assert(BM * (BN / 2) <= SE, "a C half must fit in one stage");
+    constexpr int SE = gemm_ws_stage_elems<T>();
+    static_assert(BM == 64 && BN == 64 && WM == 32 && WN == 32, "addressing below assumes 64x64 tiles");
+    static_assert(BM * 16 <= SE, "a C quarter must fit in one stage");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     __shared__ uint64_t full_bar[2][kWsRingStages], empty_bar[2][kWsRingStages];
-    __shared__ int s_d[2][BN];                 // 2^d_j exponents of the group's current tile
-
-    // swizzled [column][row] position of C element (row, colh) inside a C-half stage
-    auto offC = [](int row, int colh) {
-        if constexpr (CPX) return colh * BM + (row ^ (((colh >> 1) & 3) << 1));
-        else return colh * BM + (row ^ (((colh >> 1) & 3) << 2));
-    };
+    __shared__ int s_d[2][BN];                 // d_j of the group's current tile
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nk = (g.K + BK - 1) / BK;
     if (tid == 0) {
         for (int q = 0; q < 2; q++)
             for (int s = 0; s < kWsRingStages; s++) {
-                mbar_init(&full_bar[q][s], 32);     // the producer warp's cp.async arrivals
+                mbar_init(&full_bar[q][s], 64);     // the two producer warps' cp.async arrivals
                 mbar_init(&empty_bar[q][s], 4);     // the 4 warps of the consuming group
             }
     }
@@ -86,11 +105,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
 
     if (warp < 4) {
         // ------------------------------------------------------------------ producers
-        // Per tile of its group: nk k-tile slots, then two C-half slots (C(:, 32h .. 32h+31) and the
-        // matching d_j) so that the epilogue reads C from shared memory.
+        // Two warps per ring: warp 2q+0 loads the A tiles and C columns 0-7 of each quarter,
+        // warp 2q+1 the X tiles and C columns 8-15 (and the d_j).  Interior k-tiles take an
+        // unpredicated path.
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWsProducerRegs));
-        if (warp >= 2) return;
-        const int q = warp;
+        const int q = warp >> 1, half = warp & 1;
         int gk = 0, local = 0;
         auto next_slot = [&]() -> T * {
             const int s = gk % kWsRingStages, r = gk / kWsRingStages;
@@ -98,13 +117,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             return smem + (q * kWsRingStages + s) * SE;
         };
         auto commit_slot = [&]() { mbar_arrive_cpasync(&full_bar[q][gk % kWsRingStages]); gk++; };
-        const int kl = lane & 15, nl = lane >> 4;           // X / A(op C): k = kl, column pair nl
+        const int kl = lane & 7, nl = lane >> 3;            // k-contiguous tiles: k = kl, column nl + 4 it
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, local++) {
             if ((local & 1) != q) continue;
             const int64_t m0 = int64_t(tile % tiles_m) * BM, n0 = int64_t(tile / tiles_m) * BN;
             const bool vm0 = m0 + lane < g.M, vm1 = m0 + lane + 32 < g.M;
-            {   // warm L2 with this tile's C (read by the C-half slots after the k-tiles)
+            const bool mn_in = m0 + BM <= g.M && n0 + BN <= g.N;
+            if (half == 0) {   // warm L2 with this tile's C (read through the ring after the k-tiles)
                 const int64_t rows = g.M - m0 < BM ? g.M - m0 : int64_t(BM);
 #pragma unroll
                 for (int c2 = 0; c2 < BN / 32; c2++) {
@@ -122,51 +142,68 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             for (int kt = 0; kt < nk; kt++) {
                 T *As = next_slot(), *Xs = As + BM * BK;
                 const int k0 = kt * BK;
-                if (!OPC) {                     // A(mm,k) = U(a_r0+m0+mm, a_c0+k0+k): rows contiguous
-                    const T *ua = g.U + (g.a_r0 + m0 + lane) + (g.a_c0 + k0) * g.ldu;
+                const bool interior = mn_in && k0 + BK <= g.K;
+                if (half == 0) {
+                    if (!OPC) {                 // A(mm,k) = U(a_r0+m0+mm, a_c0+k0+k): rows contiguous
+                        const T *ua = g.U + (g.a_r0 + m0 + lane) + (g.a_c0 + k0) * g.ldu;
+                        if (interior) {
+#pragma unroll
+                            for (int k = 0; k < BK; k++) {
+                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane), ua + k * g.ldu, true);
+                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane + 32), ua + k * g.ldu + 32, true);
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < BK; k++) {
+                                const bool vk = k0 + k < g.K;
+                                const T *col = ua + k * g.ldu;
+                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane), vk && vm0 ? col : g.U, vk && vm0);
+                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane + 32), vk && vm1 ? col + 32 : g.U, vk && vm1);
+                            }
+                        }
+                    } else {                    // A(mm,k) = conj(U(a_r0+k0+k, a_c0+m0+mm)): k contiguous
+                        const bool vk = k0 + kl < g.K;
+                        const T *ua = g.U + (g.a_r0 + k0 + kl) + (g.a_c0 + m0 + nl) * g.ldu;
 #pragma unroll 4
-                    for (int k = 0; k < BK; k++) {
-                        const bool vk = k0 + k < g.K;
-                        const T *col = ua + k * g.ldu;
-                        cp_async<ESZ>(As + offA_kmajor<T>(k, lane), vk && vm0 ? col : g.U, vk && vm0);
-                        cp_async<ESZ>(As + offA_kmajor<T>(k, lane + 32), vk && vm1 ? col + 32 : g.U, vk && vm1);
+                        for (int it = 0; it < BM / 4; it++) {
+                            const int mm = 4 * it + nl;
+                            const bool v = vk && m0 + mm < g.M;
+                            cp_async<ESZ>(As + ws_offRK<T>(mm, kl), v ? ua + (4 * it) * g.ldu : g.U, v);
+                        }
                     }
-                } else {                        // A(mm,k) = conj(U(a_r0+k0+k, a_c0+m0+mm)): k contiguous
-                    const bool vk = k0 + kl < g.K;
-                    const T *ua = g.U + (g.a_r0 + k0 + kl) + (g.a_c0 + m0 + nl) * g.ldu;
-#pragma unroll 4
-                    for (int it = 0; it < BM / 2; it++) {
-                        const int mm = 2 * it + nl;
-                        const bool v = vk && m0 + mm < g.M;
-                        cp_async<ESZ>(As + offRK<T>(mm, kl), v ? ua + (2 * it) * g.ldu : g.U, v);
-                    }
-                }
-                {                               // X(k,nn) = B(x_r0+k0+k, col0+n0+nn): k contiguous
-                    const bool vk = k0 + kl < g.K;
+                } else {                        // X(k,nn) = B(x_r0+k0+k, col0+n0+nn): k contiguous
                     const T *xb = g.B + (g.x_r0 + k0 + kl) + (g.col0 + n0 + nl) * g.ldb;
+                    if (interior) {
 #pragma unroll 4
-                    for (int it = 0; it < BN / 2; it++) {
-                        const int nn = 2 * it + nl;
-                        const bool v = vk && n0 + nn < g.N;
-                        cp_async<ESZ>(Xs + offRK<T>(nn, kl), v ? xb + (2 * it) * g.ldb : g.B, v);
+                        for (int it = 0; it < BN / 4; it++)
+                            cp_async<ESZ>(Xs + ws_offRK<T>(4 * it + nl, kl), xb + (4 * it) * g.ldb, true);
+                    } else {
+                        const bool vk = k0 + kl < g.K;
+#pragma unroll 4
+                        for (int it = 0; it < BN / 4; it++) {
+                            const int nn = 4 * it + nl;
+                            const bool v = vk && n0 + nn < g.N;
+                            cp_async<ESZ>(Xs + ws_offRK<T>(nn, kl), v ? xb + (4 * it) * g.ldb : g.B, v);
+                        }
                     }
                 }
                 commit_slot();
             }
 #pragma unroll 1
-            for (int h = 0; h < 2; h++) {       // C half h and its exponents
+            for (int cq = 0; cq < 4; cq++) {    // C quarter cq (columns 16cq .. 16cq+15) and its d_j
                 T *Cs = next_slot();
-                const T *cb = g.B + (g.c_r0 + m0 + lane) + (g.col0 + n0 + 32 * h) * g.ldb;
+                const T *cb = g.B + (g.c_r0 + m0 + lane) + (g.col0 + n0 + 16 * cq + 8 * half) * g.ldb;
 #pragma unroll 4
-                for (int colh = 0; colh < 32; colh++) {
-                    const bool vn = n0 + 32 * h + colh < g.N;
-                    const T *col = cb + colh * g.ldb;
-                    cp_async<ESZ>(Cs + offC(lane, colh), vn && vm0 ? col : g.B, vn && vm0);
-                    cp_async<ESZ>(Cs + offC(lane + 32, colh), vn && vm1 ? col + 32 : g.B, vn && vm1);
+                for (int c8 = 0; c8 < 8; c8++) {
+                    const int colq = 8 * half + c8;
+                    const bool vn = n0 + 16 * cq + colq < g.N;
+                    const T *col = cb + c8 * g.ldb;
+                    cp_async<ESZ>(Cs + ws_offC<T>(lane, colq), vn && vm0 ? col : g.B, vn && vm0);
+                    cp_async<ESZ>(Cs + ws_offC<T>(lane + 32, colq), vn && vm1 ? col + 32 : g.B, vn && vm1);
                 }
-                if (g.dblk) {
-                    const bool vn = n0 + 32 * h + lane < g.N;
-                    cp_async<4>(&s_d[q][32 * h + lane], vn ? g.dblk + g.col0 + n0 + 32 * h + lane : g.dblk, vn);
+                if (half == 1 && g.dblk && lane < 16) {
+                    const bool vn = n0 + 16 * cq + lane < g.N;
+                    cp_async<4>(&s_d[q][16 * cq + lane], vn ? g.dblk + g.col0 + n0 + 16 * cq + lane : g.dblk, vn);
                 }
                 commit_slot();
             }
@@ -204,7 +241,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
 #pragma unroll
                 for (int i = 0; i < MI; i++) {
                     const int mm = wm * WM + i * 8 + gq;
-                    const T v = OPC ? As[offRK<T>(mm, k)] : As[offA_kmajor<T>(k, mm)];
+                    const T v = OPC ? As[ws_offRK<T>(mm, k)] : As[ws_offA_km<T>(k, mm)];
                     if constexpr (CPX) { ar[i] = v.x; ai[i] = OPC ? -v.y : v.y; }
                     else { ar[i] = v; ai[i] = 0.0; }
                     nai[i] = -ai[i];
@@ -212,7 +249,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
 #pragma unroll
                 for (int jn = 0; jn < NI; jn++) {
                     const int nn = wn * WN + jn * 8 + gq;
-                    const T v = Xs[offRK<T>(nn, k)];
+                    const T v = Xs[ws_offRK<T>(nn, k)];
                     if constexpr (CPX) { br[jn] = v.x; bi[jn] = v.y; }
                     else { br[jn] = v; bi[jn] = 0.0; }
                 }
@@ -239,45 +276,56 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             if (lane == 0) mbar_arrive(&empty_bar[grp][s]);
         }
 
-        // ---- epilogue: C = 2^d C - acc with C and d from the two C-half slots (every warp waits
-        //      for both and releases both, keeping the 4-arrival count of the ring) ----
-        const int s0 = gk % kWsRingStages, s1 = (gk + 1) % kWsRingStages;
-        mbar_wait(&full_bar[grp][s0], (gk / kWsRingStages) & 1);
-        mbar_wait(&full_bar[grp][s1], ((gk + 1) / kWsRingStages) & 1);
-        const T *Cs = smem + (grp * kWsRingStages + (wn ? s1 : s0)) * SE;     // this warp's half
-        const bool full = m0 + BM <= g.M && n0 + BN <= g.N;
+        // ---- epilogue: C = 2^d C - acc, C and d from the four C-quarter slots.  Every warp waits
+        //      for all four (the ring's 4-arrival count), releases the two it does not read at once
+        //      and each of its own two as soon as it is done with it. ----
+        int sq[4];
 #pragma unroll
-        for (int jn = 0; jn < NI; jn++) {
-#pragma unroll
-            for (int c = 0; c < 2; c++) {
-                const int colh = jn * 8 + tq * 2 + c;
-                const int64_t gj = n0 + wn * WN + colh;
-                // 2^d as f1 * f2 with both factors normal doubles (d < -1022 happens when a column
-                // underflows; the scale is then applied in two exact steps, no ldexp)
-                const int d = max(g.dblk ? s_d[grp][wn * WN + colh] : 0, -2044);
-                const bool lo = d < -1022;
-                const double f1 = lo ? __longlong_as_double((long long)(1023 + d + 1022) << 52) : 1.0;
-                const double f2 = __longlong_as_double((long long)(1023 + (lo ? -1022 : d)) << 52);
-                T *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
-#pragma unroll
-                for (int i = 0; i < MI; i++) {
-                    const int row = wm * WM + i * 8 + gq;
-                    const int64_t gi = m0 + row;
-                    const T old = Cs[offC(row, colh)];
-                    T nv;
-                    if constexpr (CPX) {
-                        nv.x = fma(__dmul_rn(old.x, f1), f2, -accR[i][jn][c]);
-                        nv.y = fma(__dmul_rn(old.y, f1), f2, -accI[i][jn][c]);
-                    } else {
-                        nv = fma(__dmul_rn(old, f1), f2, -accR[i][jn][c]);
-                    }
-                    if (full || (gi < g.M && gj < g.N)) colp[gi] = nv;
-                }
-            }
+        for (int cq = 0; cq < 4; cq++) {
+            sq[cq] = (gk + cq) % kWsRingStages;
+            mbar_wait(&full_bar[grp][sq[cq]], ((gk + cq) / kWsRingStages) & 1);
         }
         __syncwarp();
-        if (lane == 0) { mbar_arrive(&empty_bar[grp][s0]); mbar_arrive(&empty_bar[grp][s1]); }
-        gk += 2;
+        if (lane == 0) { mbar_arrive(&empty_bar[grp][sq[2 - 2 * wn]]); mbar_arrive(&empty_bar[grp][sq[3 - 2 * wn]]); }
+        const bool full = m0 + BM <= g.M && n0 + BN <= g.N;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {           // own quarters 2 wn + h: columns jn = 2h, 2h+1
+            const T *Cs = smem + (grp * kWsRingStages + sq[2 * wn + h]) * SE;
+#pragma unroll
+            for (int jj = 0; jj < 2; jj++) {
+                const int jn = 2 * h + jj;
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    const int colq = jj * 8 + tq * 2 + c;            // column inside the quarter
+                    const int colh = jn * 8 + tq * 2 + c;            // column inside the warp tile
+                    const int64_t gj = n0 + wn * WN + colh;
+                    // 2^d as f1 * f2 with both factors normal doubles (d < -1022 happens when a
+                    // column underflows; the scale is then applied in two exact steps, no ldexp)
+                    const int d = max(g.dblk ? s_d[grp][wn * WN + colh] : 0, -2044);
+                    const bool lo = d < -1022;
+                    const double f1 = lo ? __longlong_as_double((long long)(1023 + d + 1022) << 52) : 1.0;
+                    const double f2 = __longlong_as_double((long long)(1023 + (lo ? -1022 : d)) << 52);
+                    T *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
+#pragma unroll
+                    for (int i = 0; i < MI; i++) {
+                        const int row = wm * WM + i * 8 + gq;
+                        const int64_t gi = m0 + row;
+                        const T old = Cs[ws_offC<T>(row, colq)];
+                        T nv;
+                        if constexpr (CPX) {
+                            nv.x = fma(__dmul_rn(old.x, f1), f2, -accR[i][jn][c]);
+                            nv.y = fma(__dmul_rn(old.y, f1), f2, -accI[i][jn][c]);
+                        } else {
+                            nv = fma(__dmul_rn(old, f1), f2, -accR[i][jn][c]);
+                        }
+                        if (full || (gi < g.M && gj < g.N)) colp[gi] = nv;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[grp][sq[2 * wn + h]]);
+        }
+        gk += 4;
     }
 }
 
