@@ -35,6 +35,9 @@ __host__ __device__ constexpr int gemm_ws_stage_elems() { return (GemmCfg<T>::BM
 // sub-partition holds one warp of every WG: 56 + 2 * 224 registers x 32 lanes fits its 16K file.
 constexpr int kWsThreads = 384;
 constexpr int kWsProducerRegs = 56, kWsConsumerRegs = 224;
+// The CTA starts with 168 registers per thread (65536 / 384, rounded down); the consumers' increase
+// is served only from what the producer warpgroup releases: (168 - 56) * 128 >= (224 - 168) * 256.
+static_assert((168 - kWsProducerRegs) * 128 >= (kWsConsumerRegs - 168) * 256, "setmaxnreg pool");
 
 template <typename T>
 __host__ __device__ constexpr int gemm_ws_smem_bytes() {
@@ -279,18 +282,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
         // ---- epilogue: C = 2^d C - acc, C and d from the four C-quarter slots.  Every warp waits
         //      for all four (the ring's 4-arrival count), releases the two it does not read at once
         //      and each of its own two as soon as it is done with it. ----
-        int sq[4];
+        auto sq = [&](int cq) { return (gk + cq) % kWsRingStages; };
 #pragma unroll
-        for (int cq = 0; cq < 4; cq++) {
-            sq[cq] = (gk + cq) % kWsRingStages;
-            mbar_wait(&full_bar[grp][sq[cq]], ((gk + cq) / kWsRingStages) & 1);
-        }
+        for (int cq = 0; cq < 4; cq++) mbar_wait(&full_bar[grp][sq(cq)], ((gk + cq) / kWsRingStages) & 1);
         __syncwarp();
-        if (lane == 0) { mbar_arrive(&empty_bar[grp][sq[2 - 2 * wn]]); mbar_arrive(&empty_bar[grp][sq[3 - 2 * wn]]); }
+        if (lane == 0) { mbar_arrive(&empty_bar[grp][sq(2 - 2 * wn)]); mbar_arrive(&empty_bar[grp][sq(3 - 2 * wn)]); }
         const bool full = m0 + BM <= g.M && n0 + BN <= g.N;
 #pragma unroll
         for (int h = 0; h < 2; h++) {           // own quarters 2 wn + h: columns jn = 2h, 2h+1
-            const T *Cs = smem + (grp * kWsRingStages + sq[2 * wn + h]) * SE;
+            const T *Cs = smem + (grp * kWsRingStages + sq(2 * wn + h)) * SE;
 #pragma unroll
             for (int jj = 0; jj < 2; jj++) {
                 const int jn = 2 * h + jj;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[grp][sq[2 * wn + h]]);
+            if (lane == 0) mbar_arrive(&empty_bar[grp][sq(2 * wn + h)]);
         }
         gk += 4;
     }
