@@ -131,7 +131,7 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic(kernel: str = "gemm_update_kernel"):
+def ncu_traffic(kernel: str = "gemm_ws_kernel"):
     """dram bytes per launch of the GEMM from the committed ncu --set full capture, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     try:
@@ -304,7 +304,7 @@ def run_cuda(args, cfgname):
     traffic, _ = ncu_traffic()
     roofline = {"bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": (gemm_tf / peak_tf) if gemm_tf else None, "traffic": traffic,
-                "kernel": "gemm_update_kernel<double2,false> (mma.sync m8n8k4 f64 -> DMMA)",
+                "kernel": "gemm_ws_kernel<double2,false> (persistent warp-specialised, mma.sync m8n8k4 f64 -> DMMA)",
                 "peak_source": "measured: register-resident DMMA loop on all SMs (mstrsm_fp64_peak), "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "dfma_peak": dfma_tf,
@@ -358,7 +358,9 @@ def e2e_host(ms, T_host, m, nb, args):
         times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     fl = algorithmic_flops_cols(np.arange(m), True)
-    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(m) * m * 16,
+    # trevc_z_host copies the upper triangle of T by 128-column panels (rows 0 .. panel end)
+    h2d = sum(min(m, c0 + 128) * (min(m, c0 + 128) - c0) for c0 in range(0, m, 128)) * 16
+    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(m) * m * 16 + m * 12, "ms_per_step": dt * 1e3,
             "eigvecs_per_s": m / dt, "steps": steps, "api": "trevc_z_host (C ABI, host buffers, pinned)"}
 

@@ -410,9 +410,12 @@ int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_d
     CK(cudaMallocAsync(&dZ, bytes, g_stream));
     CK(cudaMallocAsync(&ds, m * 8, g_stream));
     CK(cudaMallocAsync(&de, m * 4, g_stream));
-    if (ldt == m) CK(cudaMemcpyAsync(dT, T_host, bytes, cudaMemcpyHostToDevice, g_stream));
-    else CK(cudaMemcpy2DAsync(dT, m * sizeof(cplx), T_host, ldt * sizeof(cplx), m * sizeof(cplx), m,
-                              cudaMemcpyHostToDevice, g_stream));
+    // only the upper triangle of T is ever read: copy it by 128-column panels (rows 0 .. panel end)
+    for (int64_t c0 = 0; c0 < m; c0 += 128) {
+        const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+        CK(cudaMemcpy2DAsync(dT + c0 * m, m * sizeof(cplx), T_host + c0 * ldt, ldt * sizeof(cplx),
+                             size_t(c1) * sizeof(cplx), size_t(c1 - c0), cudaMemcpyHostToDevice, g_stream));
+    }
     int rc = trevc_impl<cplx>(dT, m, m, nullptr, m, dZ, m, ds, de, nb);
     if (rc == 0) {
         if (ldz == m) CK(cudaMemcpyAsync(Z_host, dZ, bytes, cudaMemcpyDeviceToHost, g_stream));

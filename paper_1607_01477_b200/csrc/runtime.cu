@@ -32,6 +32,12 @@ int ensure_init() {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    // keep stream-ordered allocations cached between calls (workspace, host-entry staging)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     CK(cudaMalloc(&g_flag, sizeof(int)));
     CK(cudaMemset(g_flag, 0, sizeof(int)));
     return 0;
