@@ -158,6 +158,11 @@ int64_t     mstrsm_launch_count(int reset);
  * 1 = diagonal-block kernel, 2 = other), the summed device time, the launch count and the
  * algorithmic flops of those launches (GEMM: 2 M N K real / 8 M N K complex).            */
 int         mstrsm_profile(int enable);
+/* Real DMMA products per complex multiply-add in the update GEMM: 3 (default: P1 = Ar Xr,
+ * P2 = Ai Xi, P3 = (Ar + Ai)(Xr + Xi), Re = P1 - P2, Im = P3 - P1 - P2) or 4 (Re = Ar Xr - Ai Xi,
+ * Im = Ar Xi + Ai Xr; environment MSTRSM_GEMM=4m or classic).  The profile's flops stay the
+ * algorithmic complex count (8 M N K); executed real flops = that x (products / 4).            */
+int         mstrsm_gemm_real_products(void);
 int         mstrsm_profile_read(int kind, double *total_ms, int64_t *launches, double *flops);
 
 /* FP64 roofline probe: a register-resident DMMA (mma.sync.m8n8k4.f64) loop and a DFMA loop

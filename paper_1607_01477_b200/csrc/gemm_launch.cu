@@ -1,19 +1,26 @@
 // gemm_launch.cu -- launcher + instantiations of the DMMA update GEMM (a.5).
-//   default: the persistent warp-specialised kernel (gemm_ws.cuh);
-//   MSTRSM_GEMM=classic selects the one-tile-per-CTA kernel (gemm_kernel.cuh) for comparison.
+//   default: the persistent warp-specialised kernel -- complex operands with three real products
+//   (gemm_ws3m.cuh), real operands gemm_ws.cuh;
+//   MSTRSM_GEMM=4m: complex with four real products (gemm_ws.cuh);
+//   MSTRSM_GEMM=classic: the one-tile-per-CTA kernel (gemm_kernel.cuh).  (Comparison only.)
 #include <stdlib.h>
 #include <string.h>
 
-#include "gemm_ws.cuh"
+#include "gemm_ws3m.cuh"
 #include "runtime.cuh"
 
 namespace mstrsm {
 namespace rt {
-static bool use_classic() {
+// 0 = ws (complex: 3M), 1 = classic, 2 = ws with four products for complex
+int gemm_variant() {
     static int v = -1;
-    if (v < 0) { const char *e = getenv("MSTRSM_GEMM"); v = (e && !strcmp(e, "classic")) ? 1 : 0; }
-    return v == 1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_GEMM");
+        v = (e && !strcmp(e, "classic")) ? 1 : (e && !strcmp(e, "4m")) ? 2 : 0;
+    }
+    return v;
 }
+static bool use_classic() { return gemm_variant() == 1; }
 
 template <typename T, bool OPC>
 int launch_gemm(const GemmArgs<T> &g) {
@@ -32,6 +39,22 @@ int launch_gemm(const GemmArgs<T> &g) {
         kern<<<grid, kGemmThreads, smem, g_stream>>>(g);
         CK_LAUNCH("gemm_update_kernel");
         return 0;
+    }
+    if constexpr (S<T>::cplx_) {
+        if (gemm_variant() == 0) {
+            auto kern = gemm_ws3m_kernel<OPC>;
+            static bool attr3 = false;
+            if (!attr3) {
+                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3mSmemBytes));
+                attr3 = true;
+            }
+            const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
+            const int grid = int(std::min<int64_t>(nt, g_num_sms));
+            ProfScope ps(PK_GEMM, flops);
+            kern<<<grid, kWsThreads, k3mSmemBytes, g_stream>>>(g, int(tm), int(nt));
+            CK_LAUNCH("gemm_ws3m_kernel");
+            return 0;
+        }
     }
     auto kern = gemm_ws_kernel<T, OPC>;
     static bool attr_set = false;

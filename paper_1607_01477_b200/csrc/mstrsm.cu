@@ -467,6 +467,8 @@ int64_t mstrsm_launch_count(int reset) {
     return reset ? g_launches.exchange(0) : g_launches.load();
 }
 
+int mstrsm_gemm_real_products(void) { return mstrsm::rt::gemm_variant() == 0 ? 3 : 4; }
+
 int mstrsm_profile(int enable) {
     for (auto &r : g_prof_recs) { g_ev_pool.push_back(r.e0); g_ev_pool.push_back(r.e1); }
     g_prof_recs.clear();
