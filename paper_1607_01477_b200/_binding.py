@@ -25,7 +25,7 @@ __all__ = [
     "mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
-    "mstrsm_profile", "mstrsm_profile_read",
+    "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
     "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count",
 ]
 
@@ -63,6 +63,7 @@ def load():
         "mstrsm_error_string": [c_int],
         "mstrsm_profile": [c_int],
         "mstrsm_profile_read": [c_int, P, P, P],
+        "mstrsm_gemm_real_products": [],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -218,6 +219,11 @@ def mstrsm_profile_read(kind: int):
     return t.value, c.value, f.value
 
 
+def mstrsm_gemm_real_products() -> int:
+    """Real DMMA products per complex multiply-add in the update GEMM (3: 3M, 4: four products)."""
+    return int(load().mstrsm_gemm_real_products())
+
+
 def mstrsm_error_string(code: int) -> str:
     return load().mstrsm_error_string(code).decode()
 
@@ -226,6 +232,7 @@ def mstrsm_error_string(code: int) -> str:
 status = mstrsm_status
 launch_count = mstrsm_launch_count
 fp64_peak = mstrsm_fp64_peak
+gemm_real_products = mstrsm_gemm_real_products
 
 
 def colmajor(t):

@@ -53,10 +53,13 @@ __host__ __device__ inline int64_t diag_smem_bytes(int nfull, int esize) {
     return pk * esize + int64_t(nfull) * esize + int64_t(nfull) * 8;
 }
 
-// Threads per CTA of an instantiation (its __launch_bounds__): 10 warps when each lane holds 16
-// rows (up to 204 registers), 14 warps when it holds 8 (up to 146).
+// Threads per CTA of an instantiation (its __launch_bounds__): 12 warps when each lane holds 16
+// rows (up to 168 registers), 14 warps when it holds 8 (up to 146).
 template <typename T, int RPL> struct DiagThreads {
-    static constexpr int value = RPL >= 16 ? 320 : 448;
+#ifndef MSTRSM_DIAG_T16
+#define MSTRSM_DIAG_T16 384
+#endif
+    static constexpr int value = RPL >= 16 ? MSTRSM_DIAG_T16 : 448;
 };
 
 // 2^k as a double for -1022 <= k <= 1023 (exact, built from the exponent bits).

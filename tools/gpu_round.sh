@@ -13,9 +13,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_bench_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/ncu_list_$TAG.log 2>&1
 echo "ncu list exit $?" >> gpurun_out/ncu_list_$TAG.log
-timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:gemm_update -s 60 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:gemm_ws -s 60 -c 1 \
     -o gpurun_out/prof_gemm_c5_$TAG python tools/profile_run.py --config c5 > gpurun_out/ncu_gemm_$TAG.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:diag_kernel -s 60 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:diag_kernel -s 120 -c 1 \
     -o gpurun_out/prof_diag_c5_$TAG python tools/profile_run.py --config c5 > gpurun_out/ncu_diag_$TAG.log 2>&1
 fi
 ls -la gpurun_out
