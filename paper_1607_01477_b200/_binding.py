@@ -26,7 +26,7 @@ __all__ = [
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
-    "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count",
+    "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count", "gemm_real_products",
 ]
 
 
