@@ -65,6 +65,14 @@ def _load():
             f = getattr(lib, f"oracle_trevc_{sfx}")
             f.restype = c_int
             f.argtypes = [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int]
+            f = getattr(lib, f"oracle_mstrsm_gen_{sfx}")
+            f.restype = c_int
+            f.argtypes = [c_int, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64,
+                          c_vp, c_vp, c_int, c_int]
+            f = getattr(lib, f"oracle_tgevc_{sfx}")
+            f.restype = c_int
+            f.argtypes = [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp,
+                          c_int, c_int]
         lib.oracle_pseudospectra_z.restype = c_int
         lib.oracle_pseudospectra_z.argtypes = [c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_vp, c_vp,
                                                c_vp, c_int, c_int]
@@ -175,6 +183,61 @@ def trevc(T, *, nb: int = 64, cols=None, nthreads: int = 0):
     if rc != 0:
         raise ValueError(f"oracle_trevc returned {rc}")
     return Z, e
+
+
+def mstrsm_gen(U, V, shifts, B, *, safe: bool = True, nb: int = 64, row_end=None,
+               nthreads: int = 0):
+    """Generalized multi-shift solve (U - s_j V) x_j = c_j b_j: Alg. 7 (safe=False) or Alg. 8
+    (safe=True) of the paper's appendix, one column at a time.  Returns (X, e), c_j = 2**e_j."""
+    lib = _load()
+    cplx = any(np.iscomplexobj(a) for a in (U, V, shifts, B))
+    dtype = np.complex128 if cplx else np.float64
+    sfx = _sfx(dtype)
+    U = _fortran(np.asarray(U), dtype)
+    V = _fortran(np.asarray(V), dtype)
+    X = np.array(B, dtype=dtype, order="F", copy=True)
+    if X.ndim == 1:
+        X = X.reshape(-1, 1, order="F")
+    m, n = X.shape
+    assert U.shape == (m, m) and V.shape == (m, m)
+    s = np.ascontiguousarray(np.asarray(shifts, dtype=dtype).reshape(-1))
+    assert s.shape[0] == n
+    re = None
+    if row_end is not None:
+        re = np.ascontiguousarray(np.asarray(row_end, dtype=np.int64).reshape(-1))
+    e = np.zeros(n, dtype=np.int32)
+    rc = getattr(lib, f"oracle_mstrsm_gen_{sfx}")(1 if safe else 0, _ptr(U), max(1, m), _ptr(V),
+                                                  max(1, m), m, _ptr(s), 1, _ptr(X), max(1, m), n,
+                                                  _ptr(re), _ptr(e), nb, nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle_mstrsm_gen_{sfx} returned {rc}")
+    return X, e
+
+
+def tgevc(T, S, *, nb: int = 64, cols=None, nthreads: int = 0):
+    """GeneralizedTriangEig (Alg. 9): eigenvectors of the upper-triangular pencil (T, S),
+    lambda_k = T(k,k)/S(k,k), Z(k,k) = c_k = 2**e_k.  Returns (Z, lambda, e)."""
+    lib = _load()
+    cplx = np.iscomplexobj(T) or np.iscomplexobj(S)
+    dtype = np.complex128 if cplx else np.float64
+    T = _fortran(np.asarray(T), dtype)
+    S = _fortran(np.asarray(S), dtype)
+    m = T.shape[0]
+    c = None
+    if cols is not None:
+        c = np.ascontiguousarray(np.asarray(cols, dtype=np.int64).reshape(-1))
+        ncols = c.shape[0]
+    else:
+        ncols = m
+    Z = np.zeros((m, ncols), dtype=dtype, order="F")
+    lam = np.zeros(ncols, dtype=dtype)
+    e = np.zeros(ncols, dtype=np.int32)
+    rc = getattr(lib, f"oracle_tgevc_{_sfx(dtype)}")(_ptr(T), max(1, m), _ptr(S), max(1, m), m, _ptr(c),
+                                                     ncols, _ptr(Z), max(1, m), _ptr(lam), _ptr(e), nb,
+                                                     nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle_tgevc returned {rc}")
+    return Z, lam, e
 
 
 def pseudospectra(U, z, *, iters: int = 15, v0=None, nb: int = 64, nthreads: int = 0):

@@ -71,6 +71,7 @@ static void run_threads(void *(*fn)(void *), void *arg, int nthreads)
 #define P_ d_
 #define FN(name) name##_d
 #include "oracle_algo.inc"
+#include "oracle_gen.inc"
 #undef S
 #undef P_
 #undef FN
@@ -80,6 +81,7 @@ static void run_threads(void *(*fn)(void *), void *arg, int nthreads)
 #define P_ z_
 #define FN(name) name##_z
 #include "oracle_algo.inc"
+#include "oracle_gen.inc"
 #undef S
 #undef P_
 #undef FN

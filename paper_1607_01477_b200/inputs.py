@@ -157,3 +157,38 @@ def e1_hermitian_triangle(m: int, seed: int = 0):
     lam = rng.uniform(1.0, 2.0, m)
     H = (Q * lam) @ Q.conj().T
     return np.asfortranarray(np.triu(H))
+
+
+def g1_pencil(m: int = 4096, complex_: bool = True, seed: int = 0):
+    """Generalized stand-in, not a BASELINE config: an upper-triangular pencil
+    (T, S) for GeneralizedTriangEig (Alg. 9).  T is Grcar-like as in config 5 (diag 1 + complex
+    N(0,1e-3), superdiagonals 1..3 = 1, further entries complex N(0,1)/sqrt(m)), so the safe solve
+    rescales heavily; S has diagonal 1 + N(0,1e-3) (real, finite eigenvalues lambda_k =
+    T(k,k)/S(k,k) clustered like config 5's) and strictly upper entries N(0, 1/m) (complex circular
+    when complex_)."""
+    rng = np.random.default_rng([SEED, 103, seed])
+    if complex_:
+        dz = rng.standard_normal(2 * m) * np.sqrt(0.5e-3)
+        T = np.zeros((m, m), dtype=np.complex128, order="F")
+        T[np.arange(m), np.arange(m)] = 1.0 + dz[0::2] + 1j * dz[1::2]
+    else:
+        T = np.zeros((m, m), dtype=np.float64, order="F")
+        T[np.arange(m), np.arange(m)] = 1.0 + rng.standard_normal(m) * np.sqrt(1e-3)
+
+    def band(k, col):
+        col[max(0, k - 3):k] = 1.0
+        return col
+
+    if complex_:
+        _fill_strict_upper_complex(T, rng, np.sqrt(0.5 / m), col_fn=band)
+        S = np.zeros((m, m), dtype=np.complex128, order="F")
+        S[np.arange(m), np.arange(m)] = 1.0 + rng.standard_normal(m) * np.sqrt(1e-3)
+        _fill_strict_upper_complex(S, rng, np.sqrt(0.5 / m))
+    else:
+        _fill_strict_upper_real(T, rng, np.sqrt(1.0 / m))
+        for k in range(m):
+            T[max(0, k - 3):k, k] = 1.0
+        S = np.zeros((m, m), dtype=np.float64, order="F")
+        S[np.arange(m), np.arange(m)] = 1.0 + rng.standard_normal(m) * np.sqrt(1e-3)
+        _fill_strict_upper_real(S, rng, np.sqrt(1.0 / m))
+    return T, S

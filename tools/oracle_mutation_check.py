@@ -15,6 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ALGO = "oracle/oracle_algo.inc"
 MAIN = "oracle/mstrsm_oracle.c"
 SCAL = "oracle/oracle_scalar.h"
+GEN = "oracle/oracle_gen.inc"
+PINS, GPINS = "tests/test_oracle_pins.py", "tests/test_oracle_gen.py"
 
 MUTANTS = [
     ("growth bound uses cnl*|d| (eq. 5)", ALGO, "g = g * (1.0 + cnl[l] / ad);", "g = g * (1.0 + cnl[l] * ad);"),
@@ -47,13 +49,33 @@ MUTANTS = [
      "Z[q * ldz + i] = i < k ? T[k * ldt + i] : ZERO();"),
     ("zmod prescale wrong direction", SCAL, "if (big > 0x1p+500) s = -600;", "if (big > 0x1p+500) s = 600;"),
     ("op C diag not conjugated", ALGO, "x[l] = DIV(x[l], CONJ(SUB(UA(l, l), s)));", "x[l] = DIV(x[l], SUB(UA(l, l), s));"),
+    # generalized solve (Alg. 7/8) and GeneralizedTriangEig (Alg. 9), run against tests/test_oracle_gen.py
+    ("gen: V update sign (P:896 += V C)", GEN, "x[i] = SUB(x[i], MUL(VA(i, l), NEG(c[l - lo])));",
+     "x[i] = SUB(x[i], MUL(VA(i, l), c[l - lo]));", GPINS),
+    ("gen: V update dropped", GEN, "x[i] = SUB(x[i], MUL(VA(i, l), NEG(c[l - lo])));", "(void)0;", GPINS),
+    ("gen: U' without lambda (P:873)", GEN, "#define UP(i, l) SUB(UA(i, l), MUL(lam, VA(i, l)))",
+     "#define UP(i, l) SUB(UA(i, l), VA(i, l))", GPINS),
+    ("gen: panel term drops |lambda| ||V|| (P:952)", GEN, "G = G + (PU[b] + alam * PV[b]) * xm;",
+     "G = G + PU[b] * xm;", GPINS),
+    ("gen: C formed before the G(j) rescale (as printed in Alg. 8, R32)", GEN,
+     [("for (int64_t l = lo; l < h; l++) c[l - lo] = MUL(lam, x[l]);\n", ""),
+      ("G = G + (PU[b] + alam * PV[b]) * xm;",
+       "for (int64_t l = lo; l < h; l++) c[l - lo] = MUL(lam, x[l]);\n            G = G + (PU[b] + alam * PV[b]) * xm;")],
+     None, GPINS),
+    ("gen: lambda = S/T (P:985)", GEN, "lam[q] = DIV(T[k * ldt + k], Sm[k * lds + k]);",
+     "lam[q] = DIV(Sm[k * lds + k], T[k * ldt + k]);", GPINS),
+    ("gen: Z RHS ignores S diag(lambda) (P:987)", GEN,
+     "Z[q * ldz + i] = i < k ? SUB(MUL(Sm[k * lds + i], lam[q]), T[k * ldt + i]) : ZERO();",
+     "Z[q * ldz + i] = i < k ? NEG(T[k * ldt + i]) : ZERO();", GPINS),
 ]
 
 
 def main():
     lines = []
     survived = 0
-    for name, rel, old, new in MUTANTS:
+    for mut in MUTANTS:
+        name, rel, old, new = mut[:4]
+        tests = mut[4] if len(mut) > 4 else PINS
         tmp = tempfile.mkdtemp(prefix="omut_")
         try:
             for d in ("oracle", "tests", "paper_1607_01477_b200"):
@@ -61,11 +83,13 @@ def main():
                                 ignore=shutil.ignore_patterns("*.so", "__pycache__", "*.o"))
             p = os.path.join(tmp, rel)
             src = open(p).read()
-            if old not in src:
-                raise SystemExit(f"mutation site not found: {name}")
-            open(p, "w").write(src.replace(old, new, 1))
+            for o, n in (old if isinstance(old, list) else [(old, new)]):
+                if o not in src:
+                    raise SystemExit(f"mutation site not found: {name}")
+                src = src.replace(o, n, 1)
+            open(p, "w").write(src)
             r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
-                                "tests/test_oracle_pins.py"], cwd=tmp, capture_output=True, text=True,
+                                tests], cwd=tmp, capture_output=True, text=True,
                                timeout=600)
             killed = r.returncode != 0
             first = next((ln for ln in r.stdout.splitlines() if ln.startswith("FAILED")), "")
