@@ -5,7 +5,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr
 PKG := paper_1607_01477_b200
 CSRC := $(PKG)/csrc
-UNITS := mstrsm runtime gemm_launch $(foreach t,d z,$(foreach o,N C,$(foreach v,plain safe,diag_$(t)$(o)_$(v))))
+UNITS := mstrsm runtime gemm_launch $(foreach t,d z,$(foreach o,N C G,$(foreach v,plain safe,diag_$(t)$(o)_$(v))))
 OBJS := $(addprefix build/,$(addsuffix .o,$(UNITS)))
 HDRS := $(wildcard $(CSRC)/*.cuh) include/mstrsm.h
 

@@ -142,6 +142,35 @@ int pseudospectra_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstr
                     int32_t *flags, int nb);
 
 /* ------------------------------------------------------------------------------------
+ * Generalized multi-shift triangular solve, appendix Alg. 7 (safe = 0) and Alg. 8
+ * (safe = 1): for j = 0..n-1 find x_j and c_j = 2^{e_j} in [0,1] with
+ *     (U - shifts[j] V) x_j = c_j b_j          (op N only; B(:,j) = b_j on entry, x_j on exit)
+ * U, V: m x m upper triangular, device, read-only (strictly lower triangles never read).
+ * The diagonal blocks U' = U(I1,I1) - lambda V(I1,I1) are formed on the fly; the update
+ * is B(I0) -= U(I0,I1) X(I1) and B(I0) += V(I0,I1) C, C = lambda X(I1).  Bounds: R30;
+ * zero pivots of U' are replaced by delta_j = 2^-52 (||U|| + |lambda_j| ||V||) (R31); C is formed
+ * after the column rescale (R32).  1 <= nb <= 64 (nb = 0: 64).  Other arguments as mstrsm_*_ex
+ * (row_end_host a HOST pointer, nullable).  Errors: -i for argument i, 1 CUDA error.        */
+int mstrsm_d_gen(int safe, const double *U, int64_t ldu, const double *V, int64_t ldv, int64_t m,
+                 const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
+                 const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb);
+int mstrsm_z_gen(int safe, const mstrsm_dcomplex *U, int64_t ldu, const mstrsm_dcomplex *V, int64_t ldv,
+                 int64_t m, const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
+                 int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
+                 int nb);
+
+/* GeneralizedTriangEig, appendix Alg. 9 first function: lambda_k = T(k,k)/S(k,k)
+ * (finite eigenvalues: S(k,k) != 0 required), Z(:,k) := -T(:,k) + lambda_k S(:,k) on rows < k,
+ * safe generalized solve with the P:503-508 shortcut, Z(k,k) := c_k = 2^{e_k}; rows > k are 0.
+ * T Z = S Z diag(lambda) backward-stably.  T, S (device, read-only), Z (device, m x m output),
+ * lambda (device, nullable, m), scales / scale_exp (device, nullable, m).  1 <= nb <= 64.   */
+int tgevc_d(const double *T, int64_t ldt, const double *S, int64_t lds, int64_t m, double *Z, int64_t ldz,
+            double *lambda, double *scales, int32_t *scale_exp, int nb);
+int tgevc_z(const mstrsm_dcomplex *T, int64_t ldt, const mstrsm_dcomplex *S, int64_t lds, int64_t m,
+            mstrsm_dcomplex *Z, int64_t ldz, mstrsm_dcomplex *lambda, double *scales, int32_t *scale_exp,
+            int nb);
+
+/* ------------------------------------------------------------------------------------
  * Runtime helpers */
 int         mstrsm_set_stream(void *cuda_stream);  /* cudaStream_t; NULL = legacy stream */
 void       *mstrsm_get_stream(void);

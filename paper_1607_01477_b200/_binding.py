@@ -24,6 +24,7 @@ __all__ = [
     "load", "LIB_PATH", "MstrsmError",
     "mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
+    "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
     "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count", "gemm_real_products",
@@ -56,6 +57,10 @@ def load():
         "trevc_z_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
+        "mstrsm_d_gen": [c_int, P, c_i64, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
+        "mstrsm_z_gen": [c_int, P, c_i64, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
+        "tgevc_d": [P, c_i64, P, c_i64, c_i64, P, c_i64, P, P, P, c_int],
+        "tgevc_z": [P, c_i64, P, c_i64, c_i64, P, c_i64, P, P, P, c_int],
         "mstrsm_set_stream": [P],
         "mstrsm_status": [],
         "mstrsm_launch_count": [c_int],
@@ -179,6 +184,26 @@ def trevc_z_host(T_host: np.ndarray, m: int, Z_host: np.ndarray, scales_host=Non
                             ptr(scales_host), ptr(exp_host), nb), "trevc_z_host")
 
 
+def mstrsm_d_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
+    arr, p = _host_i64(row_end_host)
+    _call("mstrsm_d_gen", safe, _ptr(U), ldu, _ptr(V), ldv, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
+          _ptr(scales), _ptr(scale_exp), nb)
+
+
+def mstrsm_z_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
+    arr, p = _host_i64(row_end_host)
+    _call("mstrsm_z_gen", safe, _ptr(U), ldu, _ptr(V), ldv, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
+          _ptr(scales), _ptr(scale_exp), nb)
+
+
+def tgevc_d(T, ldt, S, lds, m, Z, ldz, lam, scales, scale_exp, nb):
+    _call("tgevc_d", _ptr(T), ldt, _ptr(S), lds, m, _ptr(Z), ldz, _ptr(lam), _ptr(scales), _ptr(scale_exp), nb)
+
+
+def tgevc_z(T, ldt, S, lds, m, Z, ldz, lam, scales, scale_exp, nb):
+    _call("tgevc_z", _ptr(T), ldt, _ptr(S), lds, m, _ptr(Z), ldz, _ptr(lam), _ptr(scales), _ptr(scale_exp), nb)
+
+
 def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
     _call("pseudospectra_z", _ptr(U), ldu, m, _ptr(z), npts, iters, _ptr(v0), _ptr(sigma_min),
           _ptr(flags), nb)
@@ -268,6 +293,33 @@ def trevc(T, *, nb: int = 64, cols=None):
     else:
         (trevc_z_cols if cplx else trevc_d_cols)(T, _ld(T), m, cols, ncols, Z, _ld(Z), scales, exps, nb)
     return Z, scales, exps
+
+
+def solve_gen(U, V, shifts, B, *, safe: bool = True, nb: int = 64, row_end=None, shift_stride: int = 1):
+    """In-place generalized multi-shift solve (U - s_j V) x_j = c_j b_j on column-major CUDA
+    tensors (Alg. 7/8); returns (B, scales, scale_exp)."""
+    torch = _torch()
+    m, n = B.shape
+    cplx = B.dtype == torch.complex128
+    scales = torch.empty(n, dtype=torch.float64, device=B.device)
+    exps = torch.empty(n, dtype=torch.int32, device=B.device)
+    f = mstrsm_z_gen if cplx else mstrsm_d_gen
+    f(1 if safe else 0, U, _ld(U), V, _ld(V), m, shifts, shift_stride, B, _ld(B), n, row_end, scales, exps, nb)
+    return B, scales, exps
+
+
+def tgevc(T, S, *, nb: int = 64):
+    """Eigenvectors of the upper-triangular pencil (T, S) (Alg. 9); returns (Z, lambda, scales,
+    scale_exp) as CUDA tensors (Z column-major)."""
+    torch = _torch()
+    m = T.shape[0]
+    Z = torch.empty((m, m), dtype=T.dtype, device=T.device).t()
+    lam = torch.empty(m, dtype=T.dtype, device=T.device)
+    scales = torch.empty(m, dtype=torch.float64, device=T.device)
+    exps = torch.empty(m, dtype=torch.int32, device=T.device)
+    f = tgevc_z if T.dtype == torch.complex128 else tgevc_d
+    f(T, _ld(T), S, _ld(S), m, Z, _ld(Z), lam, scales, exps, nb)
+    return Z, lam, scales, exps
 
 
 def pseudospectra(U, z, v0, *, iters: int = 15, nb: int = 64):

@@ -130,7 +130,8 @@ __global__ void colsum_c_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
     rs[i] = s;
 }
 
-// delta = 2^-52 max(rs) (or DBL_MIN when U == 0), one block.
+// delta[0] = 2^-52 max(rs) (or DBL_MIN when U == 0); delta[1] = 2^-52 max(rs) (the raw value the
+// generalized solve combines per shift, R31).  One block.
 __global__ void delta_kernel(int64_t m, const double *__restrict__ rs, double *__restrict__ delta) {
     __shared__ double red[32];
     double v = 0.0;
@@ -141,7 +142,10 @@ __global__ void delta_kernel(int64_t m, const double *__restrict__ rs, double *_
     if (threadIdx.x < 32) {
         v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
         v = warp_max(v);
-        if (threadIdx.x == 0) *delta = v > 0.0 ? ldexp(v, -52) : 2.2250738585072014e-308;
+        if (threadIdx.x == 0) {
+            delta[0] = v > 0.0 ? ldexp(v, -52) : 2.2250738585072014e-308;
+            delta[1] = ldexp(v, -52);
+        }
     }
 }
 
@@ -209,6 +213,43 @@ __global__ void init_trevc_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t
             G[q] = g;
             e[q] = 0;
             if (!(S<T>::mod(d) <= 1.7976931348623157e308)) atomicExch(nonfinite, 1);
+        }
+    }
+}
+
+// a.1 init for GeneralizedTriangEig (Alg. 9).  Column q holds eigenvector k = q:
+//   lambda_q = T(k,k) / S(k,k);  Z(l,q) = S(l,k) lambda_q - T(l,k) for l < k, 0 for l >= k;
+//   G_q = max_{l<k} |Z(l,q)|;  row_end_q = k.
+template <typename T>
+__global__ void init_tgevc_kernel(const T *__restrict__ Tm, int64_t ldt, const T *__restrict__ Sm,
+                                  int64_t lds, int64_t m, T *__restrict__ Z, int64_t ldz,
+                                  T *__restrict__ lam, int64_t *__restrict__ rowend,
+                                  double *__restrict__ G, int *__restrict__ e,
+                                  int *__restrict__ nonfinite) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w; k < m; k += nw) {
+        const T *tc = Tm + k * ldt, *sc = Sm + k * lds;
+        const T l = S<T>::div(tc[k], sc[k]);
+        T *z = Z + k * ldz;
+        double g = 0.0;
+        for (int64_t i = lane; i < m; i += 32) {
+            if (i < k) {
+                const T v = S<T>::sub(S<T>::mul(sc[i], l), tc[i]);   // P:987 Z := -T + S diag(lambda)
+                g = fmax(g, S<T>::mod(v));
+                z[i] = v;
+            } else {
+                z[i] = S<T>::zero();
+            }
+        }
+        g = warp_max(g);
+        if (lane == 0) {
+            lam[k] = l;
+            rowend[k] = k;
+            G[k] = g;
+            e[k] = 0;
+            if (!(S<T>::mod(l) <= 1.7976931348623157e308)) atomicExch(nonfinite, 1);
         }
     }
 }

@@ -24,6 +24,7 @@ template <> struct S<double> {
     __device__ __forceinline__ static double zero() { return 0.0; }
     __device__ __forceinline__ static double sub(double a, double b) { return __dsub_rn(a, b); }
     __device__ __forceinline__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+    __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
     __device__ __forceinline__ static double mod(double a) { return fabs(a); }
     __device__ __forceinline__ static double conj(double a) { return a; }
     __device__ __forceinline__ static double neg(double a) { return -a; }
@@ -40,6 +41,9 @@ template <> struct S<cplx> {
     __device__ __forceinline__ static cplx mk(double r, double i) { return make_double2(r, i); }
     __device__ __forceinline__ static cplx zero() { return mk(0.0, 0.0); }
     __device__ __forceinline__ static cplx sub(cplx a, cplx b) { return mk(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+    __device__ __forceinline__ static cplx mul(cplx a, cplx b) {
+        return mk(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+    }
     // Smith (1962), without FMA contraction.
     __device__ __forceinline__ static cplx div(cplx a, cplx b) {
         if (fabs(b.y) <= fabs(b.x)) {

@@ -45,12 +45,18 @@ struct DiagArgs {
     double *G; int *e; int *dblk; int *Etab;
     int *fb_list; int *fb_count;   // columns handed to the synchronous fallback (safe variants)
     int force_fb;                  // testing: hand every guarded column to the fallback
+    // generalized solve (Alg. 7/8, op N): V with its norms, and the output C = -lambda_j X(I1,j)
+    // (n_b x n, column j at Cbuf + j * ldc) that the V product of the update reads
+    const T *V; int64_t ldv;
+    const double *cnlV, *PV, *deltaV;
+    T *Cbuf; int64_t ldc;
 };
 
-// Shared memory: the packed strictly upper triangle, the diagonal and cnl.
-__host__ __device__ inline int64_t diag_smem_bytes(int nfull, int esize) {
+// Shared memory: the packed strictly upper triangle, the diagonal and cnl (generalized: the same
+// three for V as well).
+__host__ __device__ inline int64_t diag_smem_bytes(int nfull, int esize, bool gen = false) {
     int64_t pk = int64_t(nfull) * (nfull - 1) / 2 + 128;
-    return pk * esize + int64_t(nfull) * esize + int64_t(nfull) * 8;
+    return (gen ? 2 : 1) * (pk * esize + int64_t(nfull) * esize + int64_t(nfull) * 8);
 }
 
 // Threads per CTA of an instantiation (its __launch_bounds__): 12 warps when each lane holds 16
@@ -218,12 +224,32 @@ __device__ __forceinline__ T group_shfl(T v, int src) {
         return __shfl_sync(0xffffffffu, v, src, LPC);
 }
 
+// Element and bound accessor of the matrix a row loop solves with.  Standard solve: U'(i,l) =
+// U(i,l) from the packed triangle, cnl(l) of U.  Generalized solve (Alg. 7/8): U'(i,l) =
+// U(i,l) - lambda_j V(i,l) formed on the fly (P:873 / P:924, one fused complex multiply-subtract),
+// bound cnlU(l) + |lambda_j| cnlV(l) (R30).
+template <typename T, bool GEN>
+struct UAcc {
+    const T *pk, *pkV;
+    const double *cn, *cnV;
+    T lam;
+    double alam;
+    __device__ __forceinline__ T operator()(int idx) const {
+        if constexpr (GEN) return S<T>::fnms(pk[idx], lam, pkV[idx]);
+        else return pk[idx];
+    }
+    __device__ __forceinline__ double cnl(int sc) const {
+        if constexpr (GEN) return fma(alam, cnV[sc], cn[sc]);
+        else return cn[sc];
+    }
+};
+
 // The substitution of one column group (Alg. 1; the unguarded branch of Alg. 4):
 // x_l = y_l / d_l, y(rows < l) -= x_l U(rows < l, l).  Every lane forms the quotient of its own
 // row of slot t and the owner's quotient is shuffled to the group, so the step-to-step chain is
 // one multiply, one shuffle and one fused update.
-template <typename T, int LPC, int RPL, typename PivF>
-__device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const T *__restrict__ pk,
+template <typename T, int LPC, int RPL, typename PivF, typename Acc>
+__device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const Acc &ua,
                                            int rl, int nrow, int nmax) {
     typedef S<T> ST;
 #pragma unroll
@@ -238,11 +264,11 @@ __device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const T *__r
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);          // P:82 / P:297
             const bool in = sc < nrow;
             const T xr = in ? xl : ST::zero();
-            const T *col = pk + (sc * (sc - 1)) / 2;
-            if (rl < rr) y[t] = ST::fnms(y[t], xr, col[rl + LPC * t]);
+            const int col = (sc * (sc - 1)) / 2;
+            if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + rl + LPC * t));
             else if (rl == rr && in) y[t] = xl;
 #pragma unroll
-            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, col[rl + LPC * t2]);
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
         }
     }
 }
@@ -261,9 +287,8 @@ __device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const T *__r
 // ~2^(12 + growth of LAG+2 rows) of it (LAG = 2, flush at 12 bits: no c5 column overflows; LAG = 4
 // or a 20-bit flush sent 248 / 307906 c5 columns to the fallback, measured).  A group whose registers stop being finite (growth beyond
 // 2^54 within that window, e.g. tiny pivots) returns false and is rerun by the synchronous loop.
-template <typename T, int LPC, int RPL, typename PivF>
-__device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__restrict__ pk,
-                                            const double *__restrict__ cn, int rl, int nrow, int nmax,
+template <typename T, int LPC, int RPL, typename PivF, typename Acc>
+__device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &ua, int rl, int nrow, int nmax,
                                             bool guarded, double g, int &kt) {
     typedef S<T> ST;
 #ifndef MSTRSM_DIAG_LAG
@@ -287,7 +312,7 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
         const bool t1 = live && axt >= kOmega;
         const int k1 = t1 ? int(__double_as_longlong(axt) >> 52) - 1992 : 0;
         const double M = t1 ? __dmul_rn(axt, pow2i(-k1)) : axt;
-        double gn = __dadd_rn(t1 ? __dmul_rn(g, pow2i(-k1)) : g, __dmul_rn(M, cn[sc2]));
+        double gn = __dadd_rn(t1 ? __dmul_rn(g, pow2i(-k1)) : g, __dmul_rn(M, ua.cnl(sc2)));
         const bool t2 = live && gn >= kOmega;
         const int k2 = t2 ? int(__double_as_longlong(gn) >> 52) - 1992 : 0;
         if (t2) gn = __dmul_rn(gn, pow2i(-k2));
@@ -308,11 +333,11 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);
             const bool in = sc < nrow;
             const T xr = in ? xl : ST::zero();
-            const T *col = pk + (sc * (sc - 1)) / 2;
-            if (rl < rr) y[t] = ST::fnms(y[t], xr, col[rl + LPC * t]);
+            const int col = (sc * (sc - 1)) / 2;
+            if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + rl + LPC * t));
             else if (rl == rr && in) y[t] = xl;
 #pragma unroll
-            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, col[rl + LPC * t2]);
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
             if (sc + LAG < nmax) {                                         // warp-uniform
                 const bool prev = rr + LAG >= LPC;
                 const int src = (rr + LAG) & (LPC - 1);
@@ -349,9 +374,8 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const T *__
 
 // The synchronous guarded loop (fallback when phase 1 overflows): Alg. 4 step by step
 // with the rescales applied lazily through pend.
-template <typename T, int LPC, int RPL, bool GUARD, typename PivF>
-__device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot,
-                                          const T *__restrict__ pk, const double *__restrict__ cn,
+template <typename T, int LPC, int RPL, bool GUARD, typename PivF, typename Acc>
+__device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot, const Acc &ua,
                                           int rl, int nrow, int nmax, bool guarded, double &g, int &kt) {
     typedef S<T> ST;
     int pend = 0;
@@ -372,7 +396,7 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot,
             T xv = p.apply(yl);                                            // P:297 / P:82
             if constexpr (GUARD) {
                 const double oadv = __shfl_sync(0xffffffffu, oadt, rr, LPC);   // Omega |d_l|
-                const double cnv = cn[sc];
+                const double cnv = ua.cnl(sc);
                 const bool live = in && guarded;
                 // P:279-295 (R8): |y_l| >= Omega |d_l| in the true frame (pend <= 11 here: exact)
                 const double ay = __dmul_rn(modv(yl), pow2i(-pend));
@@ -401,14 +425,14 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot,
             }
             const T xr = in ? xv : ST::zero();
             // owner stores x_l; substitution within the block (P:315 / P:84): rows sc' < sc
-            const T *col = pk + (sc * (sc - 1)) / 2;
+            const int col = (sc * (sc - 1)) / 2;
             {
                 const int i = rl + LPC * t;
-                if (rl < rr) y[t] = ST::fnms(y[t], xr, col[i]);
+                if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + i));
                 else if (rl == rr && in) y[t] = xv;
             }
 #pragma unroll
-            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, col[rl + LPC * t2]);
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
             if constexpr (GUARD) {
                 if (pend >= 12) {                                          // back to the true frame
                     scale_all<true>(y, pend);
@@ -424,18 +448,22 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot,
 
 // One launch = one diagonal block for all (FB = false: columns [c0, c0 + ncols); FB = true: the
 // columns the main launch handed to the synchronous fallback) active columns.
-template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB>
+template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB, bool GEN = false>
 __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(DiagArgs<T> a) {
     typedef S<T> ST;
     constexpr int G = 32 / LPC;
+    static_assert(!GEN || OP == 0, "the generalized solve is op N only");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nfull = int(a.hi - a.lo);
     const int64_t ncols = FB ? int64_t(*a.fb_count) : a.ncols;
     if (ncols == 0) return;
     const int64_t npk = int64_t(nfull) * (nfull - 1) / 2 + 128;
     T *pk = reinterpret_cast<T *>(smem_raw);
-    T *dg = pk + npk;
-    double *cn = reinterpret_cast<double *>(dg + nfull);
+    T *pkV = pk + (GEN ? npk : 0);
+    T *dg = pkV + npk;
+    T *dgV = dg + (GEN ? nfull : 0);
+    double *cn = reinterpret_cast<double *>(dgV + nfull);
+    double *cnV = cn + (GEN ? nfull : 0);
 
     // ---- stage U(I1,I1) (packed, solve coordinates), its diagonal and cnl ----
     const int tid = threadIdx.x, nth = blockDim.x;
@@ -458,6 +486,19 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
             dg[c] = OP == 0 ? u : ST::conj(u);
             cn[c] = SAFE ? a.cnl[row] : 0.0;
         }
+        if constexpr (GEN) {                                        // V(I1,I1), its diagonal, cnlV
+            for (int idx = tid; idx < nfull * 128; idx += nth) {
+                const int cq = idx >> 7, rl = idx & 127;
+                if (rl < cq)
+                    cp_async<sizeof(T)>(pkV + int64_t(cq) * (cq - 1) / 2 + rl,
+                                        a.V + (a.lo + rl) + (a.lo + cq) * a.ldv, true);
+            }
+            for (int c = tid; c < nfull; c += nth) {
+                const int64_t row = a.lo + c;
+                dgV[c] = a.V[row + row * a.ldv];
+                cnV[c] = SAFE ? a.cnlV[row] : 0.0;
+            }
+        }
         cp_async_commit();
     }
     __syncthreads();                                               // diagonal and cnl visible
@@ -469,8 +510,10 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
     const int lane = tid & 31, grp = lane / LPC, rl = lane % LPC;
     const int64_t wid = (int64_t(blockIdx.x) * nth + tid) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * nth) >> 5;
-    const double delta = SAFE ? *a.delta : 0.0;
+    const double delta = SAFE ? a.delta[0] : 0.0;
     const double Pb = SAFE ? a.P[a.b] : 0.0;
+    const double PbV = SAFE && GEN ? a.PV[a.b] : 0.0;
+    const double rawU = SAFE && GEN ? a.delta[1] : 0.0, rawV = SAFE && GEN ? a.deltaV[1] : 0.0;
 
     for (int64_t base = wid * G; base < ncols; base += nw * G) {
         const int64_t q = base + grp;
@@ -488,11 +531,18 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
         if (OP == 1) sh = ST::conj(sh);
         T *x = a.B + j * a.ldb;
         auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
-        auto pivot = [&](int sc) -> T {                               // d_l = U(l,l) - s_j
-            T dd = sc < nrow ? ST::sub(dg[sc], sh) : ST::real(1.0);
-            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
+        const double alam = GEN ? modv(sh) : 0.0;
+        double delta_j = delta;
+        if (GEN) {                                                    // R31
+            delta_j = fma(alam, rawV, rawU);
+            if (!(delta_j > 0.0)) delta_j = 2.2250738585072014e-308;
+        }
+        auto pivot = [&](int sc) -> T {                               // d_l = U(l,l) - s_j (V(l,l))
+            T dd = sc < nrow ? (GEN ? ST::fnms(dg[sc], sh, dgV[sc]) : ST::sub(dg[sc], sh)) : ST::real(1.0);
+            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta_j);
             return dd;
         };
+        const UAcc<T, GEN> ua{pk, pkV, cn, cnV, sh, alam};
         // ---- load the rows ----
         T y[RPL];
 #pragma unroll
@@ -521,7 +571,7 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
                 const int sc = t * LPC + rl;
                 const bool in = sc < nrow;
                 const double ad = modv(pivot(sc));
-                const double tf = in ? __dadd_rn(1.0, __ddiv_rn(cn[sc], ad)) : 1.0;
+                const double tf = in ? __dadd_rn(1.0, __ddiv_rn(ua.cnl(sc < nfull ? sc : 0), ad)) : 1.0;
                 double suf = tf;                                       // inclusive suffix product
 #pragma unroll
                 for (int o = 1; o < LPC; o <<= 1) {
@@ -548,17 +598,17 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
         bool handed = false;
         if constexpr (FB) {
             double g = g0;
-            diag_rows<T, LPC, RPL, true>(y, pivot, pk, cn, rl, nrow, nmax, guarded, g, kt);
+            diag_rows<T, LPC, RPL, true>(y, pivot, ua, rl, nrow, nmax, guarded, g, kt);
         } else {
             if (SAFE && __any_sync(0xffffffffu, guarded)) {
-                const bool ok = diag_lagged<T, LPC, RPL>(y, pivot, pk, cn, rl, nrow, nmax, guarded, g0, kt) &&
+                const bool ok = diag_lagged<T, LPC, RPL>(y, pivot, ua, rl, nrow, nmax, guarded, g0, kt) &&
                                 !(a.force_fb && guarded);
                 if (!ok) {                                             // hand the column over
                     handed = true;
                     if (rl == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = int(j);
                 }
             } else {
-                diag_subst<T, LPC, RPL>(y, pivot, pk, rl, nrow, nmax);
+                diag_subst<T, LPC, RPL>(y, pivot, ua, rl, nrow, nmax);
             }
         }
 
@@ -574,7 +624,7 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
 #pragma unroll
             for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
             xm = group_max<LPC>(xm);
-            Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
+            Gj = __dadd_rn(Gj, __dmul_rn(GEN ? fma(alam, PbV, Pb) : Pb, xm));   // P:392 / P:952 (R30)
             int k3 = 0;
             if (Gj >= kOmega) {
                 k3 = minpow2_bits(Gj, kOmega);
@@ -593,6 +643,17 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
         for (int t = 0; t < RPL; t++) {
             int sc = rl + LPC * t;
             if (sc < nrow && !handed) x[rowof(sc)] = y[t];
+        }
+        if constexpr (GEN) {       // C(:,j) = -lambda_j X(I1,j), after the rescales (R32)
+            if (valid && !handed) {
+                const T nl = ST::neg(sh);
+                T *cj = a.Cbuf + j * a.ldc;
+#pragma unroll
+                for (int t = 0; t < RPL; t++) {
+                    const int sc = rl + LPC * t;
+                    if (sc < nfull) cj[sc] = ST::fnms(ST::zero(), nl, ST::neg(y[t]));   // = -lambda y
+                }
+            }
         }
     }
     if (!staged) stage_wait();

@@ -7,9 +7,9 @@
 
 namespace mstrsm {
 namespace rt {
-template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB>
+template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB, bool GEN>
 int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
-    auto kern = diag_kernel<T, LPC, RPL, SAFE, OP, FB>;
+    auto kern = diag_kernel<T, LPC, RPL, SAFE, OP, FB, GEN>;
     constexpr int kMaxThreads = DiagThreads<T, RPL>::value;
     constexpr int G = 32 / LPC;
     const int nfull = int(a.hi - a.lo);
@@ -19,7 +19,7 @@ int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
         attr_set = true;
     }
     // warps per CTA chosen so that the grid covers every SM when there are enough columns
-    const size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T)));
+    const size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T), GEN));
     int occ1 = occupancy(kern, kMaxThreads, smem);
     int64_t groups = cdiv(ncols_max, G);
     int64_t wpc = cdiv(groups, int64_t(g_num_sms) * std::max(occ1, 1));
@@ -41,9 +41,9 @@ int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
 // column over twice the lanes instead (shorter substitution per lane, more warps).
 // Safe variants follow the main launch with the synchronous fallback launch, which exits at once
 // unless the main launch handed columns over (device-side count, no host synchronisation).
-template <typename T, int LPC, int RPL, bool SAFE, int OP>
+template <typename T, int LPC, int RPL, bool SAFE, int OP, bool GEN>
 int launch_diag_pair(const DiagArgs<T> &a) {
-    if (int rc = launch_diag_k<T, LPC, RPL, SAFE, OP, false>(a, a.ncols)) return rc;
+    if (int rc = launch_diag_k<T, LPC, RPL, SAFE, OP, false, GEN>(a, a.ncols)) return rc;
     if (g_debug_sync) {
         cudaError_t e = cudaStreamSynchronize(g_stream);
         int cnt = -1;
@@ -51,7 +51,7 @@ int launch_diag_pair(const DiagArgs<T> &a) {
         fprintf(stderr, "[mstrsm debug] diag<%d,%d> block %lld main done (%s), ncols %lld, handed %d\n", LPC, RPL,
                 (long long)a.b, cudaGetErrorString(e), (long long)a.ncols, cnt);
     }
-    if (SAFE) return launch_diag_k<T, LPC, RPL, SAFE, OP, true>(a, std::min<int64_t>(a.ncols, int64_t(g_num_sms) * 32));
+    if (SAFE) return launch_diag_k<T, LPC, RPL, SAFE, OP, true, GEN>(a, std::min<int64_t>(a.ncols, int64_t(g_num_sms) * 32));
     return 0;
 }
 
@@ -59,10 +59,21 @@ template <typename T, bool SAFE, int OP>
 int launch_diag(const DiagArgs<T> &a, int nb) {
     const int64_t full_wave = int64_t(g_num_sms) * (DiagThreads<T, 16>::value / 32);
     auto few = [&](int lpc16) { return cdiv(a.ncols, 32 / lpc16) < full_wave; };
-    if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP>(a);
-    if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP>(a);
-    if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP>(a) : launch_diag_pair<T, 4, 16, SAFE, OP>(a);
-    return few(8) ? launch_diag_pair<T, 16, 8, SAFE, OP>(a) : launch_diag_pair<T, 8, 16, SAFE, OP>(a);
+    if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP, false>(a);
+    if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP, false>(a);
+    if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 4, 16, SAFE, OP, false>(a);
+    return few(8) ? launch_diag_pair<T, 16, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 8, 16, SAFE, OP, false>(a);
+}
+
+// Generalized solve (Alg. 7/8, op N): U' = U - lambda V on the fly; n_b <= 64 (two packed
+// triangles in shared memory).
+template <typename T, bool SAFE>
+int launch_diag_gen(const DiagArgs<T> &a, int nb) {
+    const int64_t full_wave = int64_t(g_num_sms) * (DiagThreads<T, 16>::value / 32);
+    if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, 0, true>(a);
+    if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, 0, true>(a);
+    return cdiv(a.ncols, 8) < full_wave ? launch_diag_pair<T, 8, 8, SAFE, 0, true>(a)
+                                        : launch_diag_pair<T, 4, 16, SAFE, 0, true>(a);
 }
 
 }  // namespace rt

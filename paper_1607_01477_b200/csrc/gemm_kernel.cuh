@@ -33,6 +33,8 @@ struct GemmArgs {
     int64_t M, N; int K;
     int64_t a_r0, a_c0;    // op N: A(i,k) = U(a_r0+i, a_c0+k); op C: A(i,k) = conj(U(a_r0+k, a_c0+i))
     int64_t c_r0, x_r0;    // C rows start, X rows start
+    const T *X; int64_t ldx;   // X(k,j) = X[(x_r0 + k) + (col0 + j) * ldx] (X = B for the U product;
+                               // the generalized solve's V product reads C = -lambda X from a buffer)
     int64_t col0;          // first column
     const int *dblk;       // per-column exponent delta (nullable)
 };
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
             int64_t gj = n0 + nn;
             int gk = k0 + k;
             bool v = gj < g.N && gk < g.K;
-            const T *src = g.B + (v ? (g.x_r0 + gk) + (g.col0 + gj) * g.ldb : 0);
+            const T *src = g.X + (v ? (g.x_r0 + gk) + (g.col0 + gj) * g.ldx : 0);
             cp_async<ESZ>(Xs + offRK<T>(nn, k), src, v);
         }
     };

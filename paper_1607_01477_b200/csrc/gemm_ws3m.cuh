@@ -110,19 +110,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3m_kernel(GemmArgs<cplx>
                             cp_async<16>(As + m3_offRK(mm, kl), v ? ua + (4 * it) * g.ldu : g.U, v);
                         }
                     }
-                } else {                        // X(k,nn) = B(x_r0+k0+k, col0+n0+nn): k contiguous
-                    const cplx *xb = g.B + (g.x_r0 + k0 + kl) + (g.col0 + n0 + nl) * g.ldb;
+                } else {                        // X(k,nn) = X(x_r0+k0+k, col0+n0+nn): k contiguous
+                    const cplx *xb = g.X + (g.x_r0 + k0 + kl) + (g.col0 + n0 + nl) * g.ldx;
                     if (interior) {
 #pragma unroll 4
                         for (int it = 0; it < BN / 4; it++)
-                            cp_async<16>(Xs + m3_offRK(4 * it + nl, kl), xb + (4 * it) * g.ldb, true);
+                            cp_async<16>(Xs + m3_offRK(4 * it + nl, kl), xb + (4 * it) * g.ldx, true);
                     } else {
                         const bool vk = k0 + kl < g.K;
 #pragma unroll 4
                         for (int it = 0; it < BN / 4; it++) {
                             const int nn = 4 * it + nl;
                             const bool v = vk && n0 + nn < g.N;
-                            cp_async<16>(Xs + m3_offRK(nn, kl), v ? xb + (4 * it) * g.ldb : g.B, v);
+                            cp_async<16>(Xs + m3_offRK(nn, kl), v ? xb + (4 * it) * g.ldx : g.X, v);
                         }
                     }
                 }

@@ -46,7 +46,7 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     size_t o_cnl = take(m * 8), o_part = take(m * 8), o_P = take(std::max<int64_t>(nblk, 1) * 8),
-           o_delta = take(8), o_G = take(n * 8), o_e = take(n * 4), o_d = take(n * 4),
+           o_delta = take(16), o_G = take(n * 8), o_e = take(n * 4), o_d = take(n * 4),
            o_E = take(std::max<int64_t>(nblk, 1) * n * 4), o_r = take(need_rowend ? n * 8 : 0),
            o_fl = take(n * 4), o_fc = take(std::max<int64_t>(nblk, 1) * 4),
            o_s = take(need_shifts ? n * sizeof(T) : 0);
@@ -141,6 +141,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         if (op == 0) { g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0; }
         else { g.a_r0 = bl.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
         g.x_r0 = bl.lo; g.col0 = c0;
+        g.X = B; g.ldx = ldb;
         g.dblk = SAFE ? w.dblk : nullptr;
         rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g);
         if (rc) return rc;
@@ -259,6 +260,152 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
     int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w);
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
     if (cols_dev) cudaFreeAsync(cols_dev, g_stream);
+    return rc;
+}
+
+// ---------------------------------------------------------------- generalized solve (Alg. 7/8)
+// Per block: the generalized diagonal kernel (U' = U - lambda_j V on the fly, C = -lambda_j X(I1)),
+// then the update B(I0,act) = 2^d B(I0,act) - U(I0,I1) X(I1,act) - V(I0,I1) C (P:893-896 /
+// P:970-974) as two launches of the DMMA update GEMM (the second with d = 0, X = C).
+template <typename T, bool SAFE>
+int blocked_solve_gen(const T *U, int64_t ldu, const T *V, int64_t ldv, int64_t m, const T *shifts,
+                      int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *rowend_dev,
+                      const std::vector<int64_t> *rowend_sorted_host, bool zero_c, int nb, Work &w,
+                      Work &wv, T *Cbuf) {
+    int64_t nblk = cdiv(m, nb);
+    if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));
+    for (int64_t b = 0; b < nblk; b++) {
+        Blk bl = block_rows(0, m, nb, b);
+        int64_t c0 = 0;
+        if (rowend_sorted_host) {
+            const auto &re = *rowend_sorted_host;
+            c0 = std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();
+        }
+        int64_t ncols = n - c0;
+        if (ncols <= 0) continue;
+        if (zero_c) CK(cudaMemsetAsync(Cbuf + c0 * nb, 0, size_t(ncols) * nb * sizeof(T), g_stream));
+        DiagArgs<T> a{};
+        a.U = U; a.ldu = ldu; a.m = m; a.shifts = shifts; a.sstride = sstride;
+        a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
+        a.rowend = rowend_dev;
+        a.lo = bl.lo; a.hi = bl.hi; a.b = b;
+        a.cnl = w.cnl; a.P = w.P; a.delta = w.delta;
+        a.G = w.G; a.e = w.e; a.dblk = w.dblk; a.Etab = w.Etab;
+        a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
+        a.force_fb = g_diag_force_fb;
+        a.V = V; a.ldv = ldv; a.cnlV = wv.cnl; a.PV = wv.P; a.deltaV = wv.delta;
+        a.Cbuf = Cbuf; a.ldc = nb;
+        if (int rc = launch_diag_gen<T, SAFE>(a, nb)) return rc;
+        const int64_t M = bl.lo;
+        if (M <= 0) continue;
+        GemmArgs<T> g;
+        g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
+        g.M = M; g.N = ncols; g.K = int(bl.hi - bl.lo);
+        g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0;
+        g.x_r0 = bl.lo; g.col0 = c0;
+        g.X = B; g.ldx = ldb;
+        g.dblk = SAFE ? w.dblk : nullptr;
+        if (int rc = launch_gemm<T, false>(g)) return rc;               // - U(I0,I1) X(I1)
+        GemmArgs<T> g2 = g;
+        g2.U = V; g2.ldu = ldv; g2.X = Cbuf; g2.ldx = nb; g2.x_r0 = 0; g2.dblk = nullptr;
+        if (int rc = launch_gemm<T, false>(g2)) return rc;              // - V(I0,I1) C, C = -lambda X
+    }
+    return 0;
+}
+
+template <typename T>
+int mstrsm_gen_impl(int safe, const T *U, int64_t ldu, const T *V, int64_t ldv, int64_t m, const T *shifts,
+                    int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                    double *scales, int32_t *scale_exp, int nb) {
+    if (safe != 0 && safe != 1) return -1;
+    if (m < 0) return -6;
+    if (ldu < std::max<int64_t>(1, m)) return -3;
+    if (ldv < std::max<int64_t>(1, m)) return -5;
+    if (sstride < 0) return -8;
+    if (ldb < std::max<int64_t>(1, m)) return -10;
+    if (n < 0) return -11;
+    if (nb == 0) nb = 64;
+    if (nb < 1 || nb > 64) return -15;
+    if (m == 0 || n == 0) return 0;
+    if (!U) return -2;
+    if (!V) return -4;
+    if (!shifts) return -7;
+    if (!B) return -9;
+    if (safe && !scales) return -13;
+    if (int rc = ensure_init()) return rc;
+    Work w, wv;
+    if (int rc = alloc_work<T>(w, m, n, nb, row_end_host != nullptr, false)) return rc;
+    if (int rc = alloc_work<T>(wv, m, 1, nb, false, false)) return rc;
+    std::vector<int64_t> re_host;
+    bool sorted = false;
+    if (row_end_host) {
+        re_host.assign(row_end_host, row_end_host + n);
+        for (auto &v : re_host) v = v < 0 ? 0 : (v > m ? m : v);
+        sorted = is_sorted_nondecreasing(re_host.data(), n);
+        CK(cudaMemcpyAsync(w.rowend, re_host.data(), n * 8, cudaMemcpyHostToDevice, g_stream));
+    }
+    T *Cbuf = nullptr;
+    CK(cudaMallocAsync(&Cbuf, size_t(nb) * n * sizeof(T), g_stream));
+    int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
+    int rc = 0;
+    if (safe) {
+        if ((rc = norm_pass<T>(0, U, ldu, m, nb, w)) == 0) rc = norm_pass<T>(0, V, ldv, m, nb, wv);
+        if (!rc) {
+            init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, shifts, sstride, w.G, w.e, g_flag);
+            CK_LAUNCH("init_rhs_kernel");
+            rc = blocked_solve_gen<T, true>(U, ldu, V, ldv, m, shifts, sstride, B, ldb, n, w.rowend,
+                                            sorted ? &re_host : nullptr, row_end_host && !sorted, nb, w, wv, Cbuf);
+        }
+    } else {
+        if (w.rowend) {
+            init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, nullptr, 0, nullptr, nullptr, nullptr);
+            CK_LAUNCH("init_rhs_kernel");
+        }
+        rc = blocked_solve_gen<T, false>(U, ldu, V, ldv, m, shifts, sstride, B, ldb, n, w.rowend,
+                                         sorted ? &re_host : nullptr, row_end_host && !sorted, nb, w, wv, Cbuf);
+    }
+    if (!rc && (scales || scale_exp || safe))
+        rc = finalize<T>(0, safe, B, ldb, m, n, nb, w.rowend, scales, scale_exp, nullptr, w);
+    cudaFreeAsync(Cbuf, g_stream);
+    return rc;
+}
+
+// GeneralizedTriangEig, Alg. 9 first function with the P:503-508 shortcut.
+template <typename T>
+int tgevc_impl(const T *Tm, int64_t ldt, const T *Sm, int64_t lds, int64_t m, T *Z, int64_t ldz,
+               T *lambda, double *scales, int32_t *scale_exp, int nb) {
+    if (m < 0) return -5;
+    if (ldt < std::max<int64_t>(1, m)) return -2;
+    if (lds < std::max<int64_t>(1, m)) return -4;
+    if (ldz < std::max<int64_t>(1, m)) return -7;
+    if (nb == 0) nb = 64;
+    if (nb < 1 || nb > 64) return -11;
+    if (m == 0) return 0;
+    if (!Tm) return -1;
+    if (!Sm) return -3;
+    if (!Z) return -6;
+    if (int rc = ensure_init()) return rc;
+    Work w, wv;
+    if (int rc = alloc_work<T>(w, m, m, nb, true, true)) return rc;
+    if (int rc = alloc_work<T>(wv, m, 1, nb, false, false)) return rc;
+    T *lam = static_cast<T *>(w.shifts);
+    T *Cbuf = nullptr;
+    CK(cudaMallocAsync(&Cbuf, size_t(nb) * m * sizeof(T), g_stream));
+    int rc = norm_pass<T>(0, Tm, ldt, m, nb, w);
+    if (!rc) rc = norm_pass<T>(0, Sm, lds, m, nb, wv);
+    if (!rc) {
+        int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
+        init_tgevc_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, Sm, lds, m, Z, ldz, lam, w.rowend, w.G,
+                                                            w.e, g_flag);
+        CK_LAUNCH("init_tgevc_kernel");
+        std::vector<int64_t> cols(m);
+        for (int64_t k = 0; k < m; k++) cols[k] = k;
+        rc = blocked_solve_gen<T, true>(Tm, ldt, Sm, lds, m, lam, 1, Z, ldz, m, w.rowend, &cols, false, nb,
+                                        w, wv, Cbuf);
+    }
+    if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, m, nb, w.rowend, scales, scale_exp, w.rowend, w);
+    if (!rc && lambda) CK(cudaMemcpyAsync(lambda, lam, m * sizeof(T), cudaMemcpyDeviceToDevice, g_stream));
+    cudaFreeAsync(Cbuf, g_stream);
     return rc;
 }
 
@@ -430,6 +577,30 @@ int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_d
     cudaFreeAsync(de, g_stream);
     CK(cudaStreamSynchronize(g_stream));
     return rc;
+}
+
+int mstrsm_d_gen(int safe, const double *U, int64_t ldu, const double *V, int64_t ldv, int64_t m,
+                 const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
+                 const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb) {
+    return mstrsm_gen_impl<double>(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host,
+                                   scales, scale_exp, nb);
+}
+int mstrsm_z_gen(int safe, const mstrsm_dcomplex *U, int64_t ldu, const mstrsm_dcomplex *V, int64_t ldv,
+                 int64_t m, const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
+                 int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
+                 int nb) {
+    return mstrsm_gen_impl<cplx>(safe, (const cplx *)U, ldu, (const cplx *)V, ldv, m, (const cplx *)shifts,
+                                 shift_stride, (cplx *)B, ldb, n, row_end_host, scales, scale_exp, nb);
+}
+int tgevc_d(const double *T, int64_t ldt, const double *S, int64_t lds, int64_t m, double *Z, int64_t ldz,
+            double *lambda, double *scales, int32_t *scale_exp, int nb) {
+    return tgevc_impl<double>(T, ldt, S, lds, m, Z, ldz, lambda, scales, scale_exp, nb);
+}
+int tgevc_z(const mstrsm_dcomplex *T, int64_t ldt, const mstrsm_dcomplex *S, int64_t lds, int64_t m,
+            mstrsm_dcomplex *Z, int64_t ldz, mstrsm_dcomplex *lambda, double *scales, int32_t *scale_exp,
+            int nb) {
+    return tgevc_impl<cplx>((const cplx *)T, ldt, (const cplx *)S, lds, m, (cplx *)Z, ldz, (cplx *)lambda,
+                            scales, scale_exp, nb);
 }
 
 int pseudospectra_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z, int64_t npts, int iters,

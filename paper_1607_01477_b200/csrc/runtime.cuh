@@ -71,6 +71,7 @@ int occupancy(K kern, int threads, size_t smem) {
 
 // launchers compiled in their own translation units (diag_*.cu, gemm_launch.cu)
 template <typename T, bool SAFE, int OP> int launch_diag(const DiagArgs<T> &a, int nb);
+template <typename T, bool SAFE> int launch_diag_gen(const DiagArgs<T> &a, int nb);
 template <typename T, bool OPC> int launch_gemm(const GemmArgs<T> &g);
 int gemm_variant();   // 0 = warp-specialised (complex: 3 real products), 1 = classic, 2 = ws 4 products
 
