@@ -1,0 +1,90 @@
+"""Measurement of every §8 workload besides the headline (bench.py times config 5): one JSON line
+per workload with device-timed throughput (CUDA events on the library stream, warm-up first),
+algorithmic GFLOP/s (R18), units/s, and the per-kind kernel time from the live profile.
+
+    python tools/bench_rows.py [--steps 3] [--warmup 2] [--only c3,c4,...]
+
+Workloads: c1 (dense safe solve, real), c2 (TriangEig real), c3 (TriangEig complex), c4 (inverse
+Lanczos pseudospectra, 2 x 15 solves over 16384 points), g1 (GeneralizedTriangEig, complex m=4096,
+SURVEY §8f row f1).  Inputs are seeded synthetic stand-ins."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def eig_flops(m, cplx, products=1):
+    k = np.arange(m, dtype=np.float64)
+    return float(np.sum(k * k)) * (4.0 if cplx else 1.0) * products
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--only", default="c1,c2,c3,c4,g1")
+    a = ap.parse_args()
+    import torch
+    import paper_1607_01477_b200 as ms
+    from paper_1607_01477_b200 import inputs
+    ms.load()
+    dev = lambda x: torch.from_numpy(np.asfortranarray(x)).cuda()
+    work = {}
+    if "c1" in a.only:
+        U, s, B = inputs.c1_plain_real()
+        Ud, sd, B0 = dev(U), dev(s), dev(B)
+        Bd = B0.clone()
+        work["c1"] = (lambda: (Bd.copy_(B0), ms.solve(Ud, sd, Bd, safe=True, nb=32)),
+                      256.0 ** 2 * 64, 64, "shifts/s", "c1: safe multi-shift solve, real, m=256, n=64, n_b=32")
+    if "c2" in a.only:
+        T = dev(inputs.c2_trevc_real())
+        work["c2"] = (lambda: ms.trevc(T, nb=64), eig_flops(2048, False), 2048, "eigvecs/s",
+                      "c2: TriangEig real, m=2048, n_b=64")
+    if "c3" in a.only:
+        T3 = dev(inputs.c3_trevc_complex())
+        work["c3"] = (lambda: ms.trevc(T3, nb=128), eig_flops(8192, True), 8192, "eigvecs/s",
+                      "c3: TriangEig complex, m=8192, n_b=128")
+    if "c4" in a.only:
+        U4, z, v0 = inputs.c4_pseudospectra()
+        U4d, zd, vd = dev(U4), dev(z), dev(v0)
+        work["c4"] = (lambda: ms.pseudospectra(U4d, zd, vd, iters=15, nb=64),
+                      15 * 2 * 4.0 * 1024 ** 2 * z.shape[0], z.shape[0], "points/s",
+                      "c4: inverse-Lanczos pseudospectra, complex m=1024, 128x128 grid, 15 steps (30 solves)")
+    if "g1" in a.only:
+        Tg, Sg = inputs.g1_pencil(m=4096)
+        Tgd, Sgd = dev(Tg), dev(Sg)
+        work["g1"] = (lambda: ms.tgevc(Tgd, Sgd, nb=64), eig_flops(4096, True, products=2), 4096,
+                      "eigvecs/s", "g1: GeneralizedTriangEig complex pencil, m=4096, n_b=64 (SURVEY §8f f1)")
+    for name, (fn, flops, units, uname, desc) in work.items():
+        for _ in range(a.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_step = e0.elapsed_time(e1) / a.steps
+        ms.mstrsm_profile(1)                     # one more step for the per-kind breakdown
+        fn()
+        torch.cuda.synchronize()
+        gm, gn, _ = ms.mstrsm_profile_read(0)
+        dm, dn, _ = ms.mstrsm_profile_read(1)
+        ms.mstrsm_profile(0)
+        print(json.dumps({"workload": desc, "config": name, "ms_per_step": ms_step,
+                          "gflops_algorithmic": flops / (ms_step * 1e-3) / 1e9,
+                          uname: units / (ms_step * 1e-3), "steps": a.steps, "warmup": a.warmup,
+                          "gemm_ms_profiled_step": gm, "diag_ms_profiled_step": dm,
+                          "timing": "CUDA events around the timed steps (no per-launch events); the "
+                                    "per-kind split comes from one extra step with per-launch events"}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
