@@ -228,7 +228,7 @@ __device__ __forceinline__ T group_shfl(T v, int src) {
 // U(i,l) from the packed triangle, cnl(l) of U.  Generalized solve (Alg. 7/8): U'(i,l) =
 // U(i,l) - lambda_j V(i,l) formed on the fly (P:873 / P:924, one fused complex multiply-subtract),
 // bound cnlU(l) + |lambda_j| cnlV(l) (R30).
-template <typename T, bool GEN>
+template <typename T, bool GEN, bool CONJ = false>
 struct UAcc {
     const T *pk, *pkV;
     const double *cn, *cnV;
@@ -236,6 +236,7 @@ struct UAcc {
     double alam;
     __device__ __forceinline__ T operator()(int idx) const {
         if constexpr (GEN) return S<T>::fnms(pk[idx], lam, pkV[idx]);
+        else if constexpr (CONJ) return S<T>::conj(pk[idx]);      // op C: L = U^H staged unconjugated
         else return pk[idx];
     }
     __device__ __forceinline__ double cnl(int sc) const {
@@ -474,9 +475,10 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
                 if (OP == 0) {      // U~(i,c) = U(lo+i, lo+c), asynchronous (waited for below)
                     cp_async<sizeof(T)>(pk + int64_t(cq) * (cq - 1) / 2 + rl,
                                         a.U + (a.lo + rl) + (a.lo + cq) * a.ldu, true);
-                } else {            // U~(i,c) = conj(U(hi-1-c, hi-1-i)); U column lo+cq, row lo+rl
+                } else {            // U~(i,c) = conj(U(hi-1-c, hi-1-i)) (conjugated at use, UAcc)
                     int ci = nfull - 1 - cq, cc = nfull - 1 - rl;
-                    pk[int64_t(cc) * (cc - 1) / 2 + ci] = ST::conj(a.U[(a.lo + rl) + (a.lo + cq) * a.ldu]);
+                    cp_async<sizeof(T)>(pk + int64_t(cc) * (cc - 1) / 2 + ci,
+                                        a.U + (a.lo + rl) + (a.lo + cq) * a.ldu, true);
                 }
             }
         }
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
             if (SAFE && ST::is_zero(dd)) dd = ST::real(delta_j);
             return dd;
         };
-        const UAcc<T, GEN> ua{pk, pkV, cn, cnV, sh, alam};
+        const UAcc<T, GEN, OP == 1> ua{pk, pkV, cn, cnV, sh, alam};
         // ---- load the rows ----
         T y[RPL];
 #pragma unroll
@@ -559,30 +561,36 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
             //      g_l = g_top prod_{l' > l} tf_l' are formed slot by slot with a suffix scan over
             //      the LPC lanes (rounding order differs from the sequential product at the ulp
             //      level, R24) ----
+            //      The test only chooses between the unguarded loop and the guarded one, which
+            //      produces the same result whenever no rescale triggers, so it uses upper bounds of
+            //      |y| (sqrt 2 max(|re|,|im|)) and lower bounds of |d| (max(|re|,|im|)): a column
+            //      the exact test would pass may take the guarded loop, never the reverse ----
+            double gub = 0.0;
 #pragma unroll
             for (int t = 0; t < RPL; t++)
-                if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
-            g0 = group_max<LPC>(g0);
-            double carry = g0;                                         // g at the top of the slot
+                if (rl + LPC * t < nrow) gub = fmax(gub, maxabs(y[t]));
+            gub = group_max<LPC>(gub);
+            if constexpr (ST::cplx_) gub = __dmul_ru(gub, 1.4142135623730951);
+            double carry = gub;                                        // g at the top of the slot
             bool okM = true;
-#pragma unroll
+#pragma unroll 1
             for (int t = RPL - 1; t >= 0; t--) {
                 if (t * LPC >= nmax) continue;
                 const int sc = t * LPC + rl;
                 const bool in = sc < nrow;
-                const double ad = modv(pivot(sc));
-                const double tf = in ? __dadd_rn(1.0, __ddiv_rn(ua.cnl(sc < nfull ? sc : 0), ad)) : 1.0;
+                const double ad = maxabs(pivot(sc));                   // <= |d_l|
+                const double tf = in ? __dadd_ru(1.0, __ddiv_ru(ua.cnl(sc < nfull ? sc : 0), ad)) : 1.0;
                 double suf = tf;                                       // inclusive suffix product
 #pragma unroll
                 for (int o = 1; o < LPC; o <<= 1) {
                     const double v = __shfl_down_sync(0xffffffffu, suf, o, LPC);
-                    if (rl + o < LPC) suf = __dmul_rn(suf, v);
+                    if (rl + o < LPC) suf = __dmul_ru(suf, v);
                 }
                 double exc = __shfl_down_sync(0xffffffffu, suf, 1, LPC);   // rows above, this slot
                 if (rl == LPC - 1) exc = 1.0;
-                const double gl = __dmul_rn(carry, exc);
+                const double gl = __dmul_ru(carry, exc);
                 okM = okM && (!in || gl < __dmul_rn(kOmega, ad));
-                carry = __dmul_rn(carry, __shfl_sync(0xffffffffu, suf, 0, LPC));
+                carry = __dmul_ru(carry, __shfl_sync(0xffffffffu, suf, 0, LPC));
             }
 #pragma unroll
             for (int o = 1; o < LPC; o <<= 1) {                       // group AND (every lane shuffles)
@@ -590,6 +598,12 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
                 okM = okM && other;
             }
             guarded = active && !(okM && carry < kOmega);
+            if (__any_sync(0xffffffffu, guarded)) {                    // g := ||y(I1)||_inf
+#pragma unroll
+                for (int t = 0; t < RPL; t++)
+                    if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
+                g0 = group_max<LPC>(g0);
+            }
         }
 
         // ---- the row loop ----
