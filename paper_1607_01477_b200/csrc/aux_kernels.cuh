@@ -254,6 +254,20 @@ __global__ void init_tgevc_kernel(const T *__restrict__ Tm, int64_t ldt, const T
     }
 }
 
+// Operand sums for the complex 3M update GEMM: P(i,k) = Re U(i,k) + sign Im U(i,k)
+// on the strictly upper triangle (op N: sign = +1; op C, whose A operand is conj(U)^T: sign = -1).
+__global__ void presum_kernel(const cplx *__restrict__ U, int64_t ldu, int64_t m, double *__restrict__ P,
+                              int64_t ldp, double sign) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w; k < m; k += nw) {
+        const cplx *uc = U + k * ldu;
+        double *pc = P + k * ldp;
+        for (int64_t i = lane; i < k; i += 32) pc[i] = fma(sign, uc[i].y, uc[i].x);
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // a.6 finalize.  Block b finalised rows I1(b) of column j in the frame E[b][j]; the final frame
 // is e_j, so X(I1(b), j) *= 2^{e_j - E[b][j]} (exact powers of two; the lazy form of the

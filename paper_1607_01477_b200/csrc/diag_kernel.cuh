@@ -50,6 +50,8 @@ struct DiagArgs {
     const T *V; int64_t ldv;
     const double *cnlV, *PV, *deltaV;
     T *Cbuf; int64_t ldc;
+    // complex 3M update (nullable): Re + Im of the finished rows I1, Xsum[(row - lo) + j * ldxs]
+    double *Xsum; int64_t ldxs;
 };
 
 // Shared memory: the packed strictly upper triangle, the diagonal and cnl (generalized: the same
@@ -657,6 +659,16 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
         for (int t = 0; t < RPL; t++) {
             int sc = rl + LPC * t;
             if (sc < nrow && !handed) x[rowof(sc)] = y[t];
+        }
+        if constexpr (ST::cplx_) {  // operand sums for the 3M update GEMM
+            if (a.Xsum && valid && !handed) {
+                double *xs = a.Xsum + j * a.ldxs;
+#pragma unroll
+                for (int t = 0; t < RPL; t++) {
+                    const int sc = rl + LPC * t;
+                    if (sc < nfull) xs[rowof(sc) - a.lo] = __dadd_rn(y[t].x, y[t].y);
+                }
+            }
         }
         if constexpr (GEN) {       // C(:,j) = -lambda_j X(I1,j), after the rescales (R32)
             if (valid && !handed) {

@@ -35,6 +35,11 @@ struct GemmArgs {
     int64_t c_r0, x_r0;    // C rows start, X rows start
     const T *X; int64_t ldx;   // X(k,j) = X[(x_r0 + k) + (col0 + j) * ldx] (X = B for the U product;
                                // the generalized solve's V product reads C = -lambda X from a buffer)
+    // complex 3M only (nullable): the sums Re + Im of the operands, precomputed:
+    //   As indexed like A (op N: As[(a_r0+i) + (a_c0+k) ldas]; op C: As[(a_r0+k) + (a_c0+i) ldas],
+    //   there holding Re - Im = Re(conj)), Xs(k,j) = Xs[k + (col0 + j) ldxs]
+    const double *As; int64_t ldas;
+    const double *Xsum; int64_t ldxs;
     int64_t col0;          // first column
     const int *dblk;       // per-column exponent delta (nullable)
 };

@@ -6,7 +6,9 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "gemm_ws3m.cuh"
+#include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
+
+#include "gemm_ws3p.cuh"
 #include "runtime.cuh"
 
 namespace mstrsm {
@@ -20,6 +22,39 @@ int gemm_variant() {
     }
     return v;
 }
+// MSTRSM_3M_PRESUM=0: keep the in-register operand sums (comparison only)
+bool gemm_presum_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_3M_PRESUM");
+        v = (e && !strcmp(e, "0")) ? 0 : 1;
+    }
+    return v == 1;
+}
+// cuTensorMapEncodeTiled through the runtime's driver entry point
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+// 2-D map over a column-major (rows x cols) f64 array with leading dimension ld (elements)
+static bool encode_2d(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols, uint64_t ld,
+                      uint32_t box_rows, uint32_t box_cols, CUtensorMapSwizzle sw) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {rows, cols}, strides[1] = {ld * 8};
+    cuuint32_t box[2] = {box_rows, box_cols}, es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool use_classic() { return gemm_variant() == 1; }
 
 template <typename T, bool OPC>
@@ -41,6 +76,27 @@ int launch_gemm(const GemmArgs<T> &g) {
         return 0;
     }
     if constexpr (S<T>::cplx_) {
+        if (gemm_variant() == 0 && !OPC && g.As && g.Xsum && g.a_r0 % 2 == 0 && g.ldas % 2 == 0 &&
+            g.ldxs % 2 == 0) {                   // sums precomputed: bulk-copy producer, LDS + DMMA
+            // X: rows x_r0.. (as 2K doubles) x columns col0.., X+: K x N doubles
+            CUtensorMap tmX, tmXs;
+            if (!encode_2d(&tmX, g.X + g.x_r0 + g.col0 * g.ldx, uint64_t(2 * g.K), uint64_t(g.N), uint64_t(2 * g.ldx),
+                           2 * k3mBK, k3mBN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+                !encode_2d(&tmXs, g.Xsum + g.col0 * g.ldxs, uint64_t(g.K), uint64_t(g.N), uint64_t(g.ldxs), k3mBK,
+                           k3mBN, CU_TENSOR_MAP_SWIZZLE_64B))
+                return set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (3M update operands)");
+            static bool attrp = false;
+            if (!attrp) {
+                CK(cudaFuncSetAttribute(gemm_ws3p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k3pSmemBytes));
+                attrp = true;
+            }
+            const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
+            const int grid = int(std::min<int64_t>(nt, g_num_sms));
+            ProfScope ps(PK_GEMM, flops);
+            gemm_ws3p_kernel<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs);
+            CK_LAUNCH("gemm_ws3p_kernel");
+            return 0;
+        }
         if (gemm_variant() == 0) {
             auto kern = gemm_ws3m_kernel<OPC>;
             static bool attr3 = false;

@@ -106,7 +106,8 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w) {
 template <typename T, bool SAFE>
 int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride,
                   T *B, int64_t ldb, int64_t n, const int64_t *rowend_dev,
-                  const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w) {
+                  const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w,
+                  const double *Usum = nullptr, double *Xsum = nullptr, int64_t ldus = 0, int ldxs = 0) {
     int64_t nblk = cdiv(m, nb);
     if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));   // diag fallback counts
     for (int64_t b = 0; b < nblk; b++) {
@@ -127,6 +128,9 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         a.G = w.G; a.e = w.e; a.dblk = w.dblk; a.Etab = w.Etab;
         a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
         a.force_fb = g_diag_force_fb;
+        a.Xsum = Xsum; a.ldxs = ldxs;
+        if (Xsum && rowend_dev && !rowend_sorted_host)        // inactive columns in range: zero rows
+            CK(cudaMemsetAsync(Xsum + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
         int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
         if (rc) return rc;
         if (g_debug_sync) {
@@ -135,13 +139,14 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         }
         int64_t M = op == 0 ? bl.lo : m - bl.hi;
         if (M <= 0) continue;
-        GemmArgs<T> g;
+        GemmArgs<T> g{};
         g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
         g.M = M; g.N = ncols; g.K = int(bl.hi - bl.lo);
         if (op == 0) { g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0; }
         else { g.a_r0 = bl.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
         g.x_r0 = bl.lo; g.col0 = c0;
         g.X = B; g.ldx = ldb;
+        if (Usum && Xsum) { g.As = Usum; g.ldas = ldus; g.Xsum = Xsum; g.ldxs = ldxs; }
         g.dblk = SAFE ? w.dblk : nullptr;
         rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g);
         if (rc) return rc;
@@ -151,6 +156,35 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         }
     }
     return 0;
+}
+
+// Sum planes for the complex 3M update (nullptr when the 3-product kernel is not in use or T is
+// real): Usum (m x m doubles, strictly upper part) for operator op, Xsum (nb x n doubles).
+struct SumPlanes {
+    double *U = nullptr, *X = nullptr;
+    int64_t ldu = 0;
+    int ldx = 0;
+    cudaStream_t st = nullptr;
+    ~SumPlanes() { if (U) cudaFreeAsync(U, st); if (X) cudaFreeAsync(X, st); }
+};
+template <typename T>
+int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, int64_t n, int nb) {
+    if constexpr (!S<T>::cplx_) return 0;
+    else {
+        // op C keeps the in-register sums (its A operand is k-contiguous)
+        if (gemm_variant() != 0 || m == 0 || op != 0 || !gemm_presum_enabled()) return 0;
+        sp.st = g_stream;
+        // even leading dimensions (16-byte aligned bulk copies), ldu > m so that a copy rounded
+        // up to 16 bytes past the last row of a column stays inside that column
+        sp.ldu = (m + 2) & ~int64_t(1);
+        sp.ldx = (nb + 1) & ~1;
+        CK(cudaMallocAsync(&sp.U, size_t(sp.ldu) * m * 8, g_stream));
+        CK(cudaMallocAsync(&sp.X, size_t(sp.ldx) * std::max<int64_t>(n, 1) * 8, g_stream));
+        int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
+        presum_kernel<<<blocks, 256, 0, g_stream>>>(U, ldu, m, sp.U, sp.ldu, op == 0 ? 1.0 : -1.0);
+        CK_LAUNCH("presum_kernel");
+        return 0;
+    }
 }
 
 template <typename T>
@@ -208,16 +242,20 @@ int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T
         if (int rc = norm_pass<T>(op, U, ldu, m, nb, w)) return rc;
         init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, shifts, sstride, w.G, w.e, g_flag);
         CK_LAUNCH("init_rhs_kernel");
+        SumPlanes sp;
+        if (int rc = make_sum_planes<T>(sp, op, U, ldu, m, n, nb)) return rc;
         int rc = blocked_solve<T, true>(op, U, ldu, m, shifts, sstride, B, ldb, n, w.rowend,
-                                        sorted ? &re_host : nullptr, nb, w);
+                                        sorted ? &re_host : nullptr, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
         if (rc) return rc;
     } else {
         if (w.rowend) {
             init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, nullptr, 0, nullptr, nullptr, nullptr);
             CK_LAUNCH("init_rhs_kernel");
         }
+        SumPlanes sp;
+        if (int rc = make_sum_planes<T>(sp, op, U, ldu, m, n, nb)) return rc;
         int rc = blocked_solve<T, false>(op, U, ldu, m, shifts, sstride, B, ldb, n, w.rowend,
-                                         sorted ? &re_host : nullptr, nb, w);
+                                         sorted ? &re_host : nullptr, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
         if (rc) return rc;
     }
     if (scales || scale_exp || safe)
@@ -257,7 +295,9 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
                                                         w.rowend, w.G, w.e, g_flag);
     CK_LAUNCH("init_trevc_kernel");
     // row_end_q = cols[q] (the P:503-508 shortcut), sorted ascending
-    int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w);
+    SumPlanes sp;
+    if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb)) return rc;
+    int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
     if (cols_dev) cudaFreeAsync(cols_dev, g_stream);
     return rc;
@@ -298,7 +338,7 @@ int blocked_solve_gen(const T *U, int64_t ldu, const T *V, int64_t ldv, int64_t 
         if (int rc = launch_diag_gen<T, SAFE>(a, nb)) return rc;
         const int64_t M = bl.lo;
         if (M <= 0) continue;
-        GemmArgs<T> g;
+        GemmArgs<T> g{};
         g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
         g.M = M; g.N = ncols; g.K = int(bl.hi - bl.lo);
         g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0;
@@ -429,6 +469,9 @@ int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int
     if (int rc = alloc_work<cplx>(wC, m, npts, nb, false, false)) return rc;
     if (int rc = norm_pass<cplx>(0, U, ldu, m, nb, wN)) return rc;
     if (int rc = norm_pass<cplx>(1, U, ldu, m, nb, wC)) return rc;
+    SumPlanes spN, spC;
+    if (int rc = make_sum_planes<cplx>(spN, 0, U, ldu, m, npts, nb)) return rc;
+    if (int rc = make_sum_planes<cplx>(spC, 1, U, ldu, m, npts, nb)) return rc;
     size_t vec = size_t(m) * npts * sizeof(cplx);
     size_t small = size_t(npts) * 8;
     size_t total = 4 * vec + 2 * size_t(iters) * small + 8 * small + 1024;
@@ -454,14 +497,14 @@ int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int
         CK_LAUNCH("copy_cols_kernel");
         init_rhs_kernel<cplx><<<blocks, 256, 0, g_stream>>>(st.Y, m, m, npts, nullptr, z, 1, wN.G, wN.e, g_flag);
         CK_LAUNCH("init_rhs_kernel");
-        rc = blocked_solve<cplx, true>(0, U, ldu, m, z, 1, st.Y, m, npts, nullptr, nullptr, nb, wN);
+        rc = blocked_solve<cplx, true>(0, U, ldu, m, z, 1, st.Y, m, npts, nullptr, nullptr, nb, wN, spN.U, spN.X, spN.ldu, spN.ldx);
         if (!rc) rc = finalize<cplx>(0, 1, st.Y, m, m, npts, nb, nullptr, nullptr, e1, nullptr, wN);
         if (rc) break;
         copy_cols_kernel<<<blocks, 256, 0, g_stream>>>(st.Y, st.W, m, npts);
         CK_LAUNCH("copy_cols_kernel");
         init_rhs_kernel<cplx><<<blocks, 256, 0, g_stream>>>(st.W, m, m, npts, nullptr, nullptr, 0, wC.G, wC.e, nullptr);
         CK_LAUNCH("init_rhs_kernel");
-        rc = blocked_solve<cplx, true>(1, U, ldu, m, z, 1, st.W, m, npts, nullptr, nullptr, nb, wC);
+        rc = blocked_solve<cplx, true>(1, U, ldu, m, z, 1, st.W, m, npts, nullptr, nullptr, nb, wC, spC.U, spC.X, spC.ldu, spC.ldx);
         if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, npts, nb, nullptr, nullptr, e2, nullptr, wC);
         if (rc) break;
         lanczos_step_kernel<<<blocks, 256, 0, g_stream>>>(st, m, npts, it, iters);

@@ -73,6 +73,7 @@ int occupancy(K kern, int threads, size_t smem) {
 template <typename T, bool SAFE, int OP> int launch_diag(const DiagArgs<T> &a, int nb);
 template <typename T, bool SAFE> int launch_diag_gen(const DiagArgs<T> &a, int nb);
 template <typename T, bool OPC> int launch_gemm(const GemmArgs<T> &g);
+bool gemm_presum_enabled();   // complex 3M with precomputed operand sums (gemm_ws3p.cuh)
 int gemm_variant();   // 0 = warp-specialised (complex: 3 real products), 1 = classic, 2 = ws 4 products
 
 }  // namespace rt
