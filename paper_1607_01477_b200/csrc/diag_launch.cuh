@@ -57,8 +57,13 @@ int launch_diag_pair(const DiagArgs<T> &a) {
 
 template <typename T, bool SAFE, int OP>
 int launch_diag(const DiagArgs<T> &a, int nb) {
-    const int64_t full_wave = int64_t(g_num_sms) * (DiagThreads<T, 16>::value / 32);
-    auto few = [&](int lpc16) { return cdiv(a.ncols, 32 / lpc16) < full_wave; };
+    // Whole passes of the grid over the columns: a pass of the RPL = 16 layout takes about 1.2x
+    // one of the RPL = 8 layout (c5 launch list, profiles/r01), so pick the cheaper pass count.
+    auto passes = [&](int lpc, int rpl) {
+        const int64_t per_pass = int64_t(g_num_sms) * (rpl >= 16 ? DiagThreads<T, 16>::value : DiagThreads<T, 8>::value) / 32 * (32 / lpc);
+        return cdiv(a.ncols, per_pass);
+    };
+    auto few = [&](int lpc16) { return 10 * passes(2 * lpc16, 8) < 12 * passes(lpc16, 16); };
     if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP, false>(a);
     if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP, false>(a);
     if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 4, 16, SAFE, OP, false>(a);
