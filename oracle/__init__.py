@@ -185,6 +185,21 @@ def trevc(T, *, nb: int = 64, cols=None, nthreads: int = 0):
     return Z, e
 
 
+def eig_backtransform(Q, Z):
+    """X := Q Z, the back-transformation step of Eig (`X := Q Z  (xGEMM)`).
+
+    The step is a plain matrix product, taken as the library primitive (numpy matmul in fp64);
+    column q of X keeps the scale c_q of Z(:, q)."""
+    return np.asfortranarray(np.asarray(Q) @ np.asarray(Z))
+
+
+def trevc_qz(T, Q, *, nb: int = 64, nthreads: int = 0):
+    """Eig's last two steps: Z = TriangEig(T) (Alg. 6, ``trevc``), X = Q Z.
+    Returns (X, e): eigenvectors of A = Q T Q^H, column k scaled by c_k = 2**e_k."""
+    Z, e = trevc(T, nb=nb, nthreads=nthreads)
+    return eig_backtransform(Q, Z), e
+
+
 def mstrsm_gen(U, V, shifts, B, *, safe: bool = True, nb: int = 64, row_end=None,
                nthreads: int = 0):
     """Generalized multi-shift solve (U - s_j V) x_j = c_j b_j: Alg. 7 (safe=False) or Alg. 8

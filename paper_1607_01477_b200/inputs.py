@@ -192,3 +192,25 @@ def g1_pencil(m: int = 4096, complex_: bool = True, seed: int = 0):
         S[np.arange(m), np.arange(m)] = 1.0 + rng.standard_normal(m) * np.sqrt(1e-3)
         _fill_strict_upper_real(S, rng, np.sqrt(1.0 / m))
     return T, S
+
+
+def schur_pair(m: int, complex_: bool = True, seed: int = 0):
+    """Back-transformation stand-in, not a BASELINE config: a Schur pair
+    (T, Q) of A = Q T Q^H.  T is the config-3 (complex) or config-2 (real) generator at size m;
+    Q is the orthonormal factor of the QR of a Gaussian matrix (complex circular / real)."""
+    T = c3_trevc_complex(m) if complex_ else c2_trevc_real(m)
+    rng = np.random.default_rng([SEED, 104, seed, m])
+    G = rng.standard_normal((m, 2 * m if complex_ else m))
+    Q, _ = np.linalg.qr(G[:, 0::2] + 1j * G[:, 1::2] if complex_ else G)
+    return T, np.asfortranarray(Q)
+
+
+def dense_q(m: int, complex_: bool = True, seed: int = 0):
+    """A dense m x m stand-in for Q at bench sizes (a QR at m = 8192 would dominate the setup):
+    entries N(0, 1/m) (complex circular), so ||Q(:,k)||_2 ~ 1.  Throughput of X = Q Z does not
+    depend on Q being unitary."""
+    rng = np.random.default_rng([SEED, 105, seed, m])
+    if complex_:
+        v = rng.standard_normal((m, 2 * m)) * np.sqrt(0.5 / m)
+        return np.asfortranarray(v[:, 0::2] + 1j * v[:, 1::2])
+    return np.asfortranarray(rng.standard_normal((m, m)) / np.sqrt(m))
