@@ -171,6 +171,30 @@ int tgevc_z(const mstrsm_dcomplex *T, int64_t ldt, const mstrsm_dcomplex *S, int
             int nb);
 
 /* ------------------------------------------------------------------------------------
+ * Back-transformation of Eig: X := Q Z, the xGEMM step after
+ * TriangEig, here a TRMM-shaped DMMA contraction exploiting that column q of Z is zero below
+ * row cols[q] (Z from trevc_*: upper triangular).  Column scales are unchanged: X(:,q) is the
+ * eigenvector of A = Q T Q^H times the same c_q as Z(:,q).
+ *   Q      m x m (ldq >= max(1,m)), device, read-only (any matrix; unitary for Eig)
+ *   Z      m x n (ldz >= max(1,m)), device, read-only
+ *   cols_host  HOST pointer, nullable: n strictly increasing row bounds, Z(r,q) = 0 for
+ *          r > cols_host[q] (trevc_*_cols order); NULL = cols[q] = q (n <= m)
+ *   X      m x n output (ldx >= max(1,m)), device; must not overlap Q or Z
+ * Errors: -i for argument i, 1 CUDA error.  Asynchronous on the library stream.            */
+int eig_backtransform_d(const double *Q, int64_t ldq, int64_t m, const double *Z, int64_t ldz, int64_t n,
+                        const int64_t *cols_host, double *X, int64_t ldx);
+int eig_backtransform_z(const mstrsm_dcomplex *Q, int64_t ldq, int64_t m, const mstrsm_dcomplex *Z,
+                        int64_t ldz, int64_t n, const int64_t *cols_host, mstrsm_dcomplex *X, int64_t ldx);
+
+/* Eig's last two steps fused: Z := TriangEig(T) in a library-owned workspace
+ * (trevc_*, same nb rules), then X := Q Z.  X (m x m, device) holds the eigenvectors of
+ * A = Q T Q^H, column k scaled by c_k = scales[k] = 2^{scale_exp[k]} (nullable outputs).   */
+int trevc_qz_d(const double *T, int64_t ldt, int64_t m, const double *Q, int64_t ldq, double *X,
+               int64_t ldx, double *scales, int32_t *scale_exp, int nb);
+int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dcomplex *Q, int64_t ldq,
+               mstrsm_dcomplex *X, int64_t ldx, double *scales, int32_t *scale_exp, int nb);
+
+/* ------------------------------------------------------------------------------------
  * Runtime helpers */
 int         mstrsm_set_stream(void *cuda_stream);  /* cudaStream_t; NULL = legacy stream */
 void       *mstrsm_get_stream(void);

@@ -25,6 +25,7 @@ __all__ = [
     "mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
+    "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
     "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count", "gemm_real_products",
@@ -61,6 +62,10 @@ def load():
         "mstrsm_z_gen": [c_int, P, c_i64, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
         "tgevc_d": [P, c_i64, P, c_i64, c_i64, P, c_i64, P, P, P, c_int],
         "tgevc_z": [P, c_i64, P, c_i64, c_i64, P, c_i64, P, P, P, c_int],
+        "eig_backtransform_d": [P, c_i64, c_i64, P, c_i64, c_i64, P, P, c_i64],
+        "eig_backtransform_z": [P, c_i64, c_i64, P, c_i64, c_i64, P, P, c_i64],
+        "trevc_qz_d": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
+        "trevc_qz_z": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "mstrsm_set_stream": [P],
         "mstrsm_status": [],
         "mstrsm_launch_count": [c_int],
@@ -320,6 +325,48 @@ def tgevc(T, S, *, nb: int = 64):
     f = tgevc_z if T.dtype == torch.complex128 else tgevc_d
     f(T, _ld(T), S, _ld(S), m, Z, _ld(Z), lam, scales, exps, nb)
     return Z, lam, scales, exps
+
+
+def eig_backtransform_d(Q, ldq, m, Z, ldz, n, cols_host, X, ldx):
+    arr, p = _host_i64(cols_host)
+    _call("eig_backtransform_d", _ptr(Q), ldq, m, _ptr(Z), ldz, n, p, _ptr(X), ldx)
+
+
+def eig_backtransform_z(Q, ldq, m, Z, ldz, n, cols_host, X, ldx):
+    arr, p = _host_i64(cols_host)
+    _call("eig_backtransform_z", _ptr(Q), ldq, m, _ptr(Z), ldz, n, p, _ptr(X), ldx)
+
+
+def trevc_qz_d(T, ldt, m, Q, ldq, X, ldx, scales, scale_exp, nb):
+    _call("trevc_qz_d", _ptr(T), ldt, m, _ptr(Q), ldq, _ptr(X), ldx, _ptr(scales), _ptr(scale_exp), nb)
+
+
+def trevc_qz_z(T, ldt, m, Q, ldq, X, ldx, scales, scale_exp, nb):
+    _call("trevc_qz_z", _ptr(T), ldt, m, _ptr(Q), ldq, _ptr(X), ldx, _ptr(scales), _ptr(scale_exp), nb)
+
+
+def eig_backtransform(Q, Z, *, cols=None):
+    """X = Q Z on column-major CUDA tensors, Z zero below row cols[q] in column q
+    (default q: upper triangular); returns X (column-major)."""
+    torch = _torch()
+    m, n = Z.shape
+    X = torch.empty((n, m), dtype=Z.dtype, device=Z.device).t()
+    f = eig_backtransform_z if Z.dtype == torch.complex128 else eig_backtransform_d
+    f(Q, _ld(Q), m, Z, _ld(Z), n, cols, X, _ld(X))
+    return X
+
+
+def trevc_qz(T, Q, *, nb: int = 64):
+    """Eigenvectors of A = Q T Q^H from its Schur pair (TriangEig, then X = Q Z, P:536-546);
+    returns (X, scales, scale_exp) as CUDA tensors (X column-major)."""
+    torch = _torch()
+    m = T.shape[0]
+    X = torch.empty((m, m), dtype=T.dtype, device=T.device).t()
+    scales = torch.empty(m, dtype=torch.float64, device=T.device)
+    exps = torch.empty(m, dtype=torch.int32, device=T.device)
+    f = trevc_qz_z if T.dtype == torch.complex128 else trevc_qz_d
+    f(T, _ld(T), m, Q, _ld(Q), X, _ld(X), scales, exps, nb)
+    return X, scales, exps
 
 
 def pseudospectra(U, z, v0, *, iters: int = 15, nb: int = 64):

@@ -254,17 +254,29 @@ __global__ void init_tgevc_kernel(const T *__restrict__ Tm, int64_t ldt, const T
     }
 }
 
+// X := -X on an m x n column-major array (the back-transformation's sign, mstrsm.cu)
+template <typename T>
+__global__ void negate_kernel(T *__restrict__ X, int64_t ldx, int64_t m, int64_t n) {
+    const int64_t total = m * n, stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t c = i / m, r = i - c * m;
+        X[r + c * ldx] = S<T>::neg(X[r + c * ldx]);
+    }
+}
+
 // Operand sums for the complex 3M update GEMM: P(i,k) = Re U(i,k) + sign Im U(i,k)
 // on the strictly upper triangle (op N: sign = +1; op C, whose A operand is conj(U)^T: sign = -1).
+// rows = 0: strictly upper part of an m x m triangle; rows > 0: all `rows` rows of ncols columns.
 __global__ void presum_kernel(const cplx *__restrict__ U, int64_t ldu, int64_t m, double *__restrict__ P,
-                              int64_t ldp, double sign) {
+                              int64_t ldp, double sign, int64_t rows = 0) {
     int lane = threadIdx.x & 31;
     int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t k = w; k < m; k += nw) {
         const cplx *uc = U + k * ldu;
         double *pc = P + k * ldp;
-        for (int64_t i = lane; i < k; i += 32) pc[i] = fma(sign, uc[i].y, uc[i].x);
+        const int64_t r = rows > 0 ? rows : k;
+        for (int64_t i = lane; i < r; i += 32) pc[i] = fma(sign, uc[i].y, uc[i].x);
     }
 }
 

@@ -303,6 +303,86 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
     return rc;
 }
 
+// ---------------------------------------------------------------- back-transformation (f2)
+// X := Q Z.  The update GEMM computes C <- C - A X, so X is zeroed, receives -Q Z
+// panel by panel and is negated once.  Panel p (columns [p0, p1)) only needs rows 0..cols[p1-1]
+// of Z (zero below, TRMM shape): K = cols[p1-1] + 1, about m/(2 W) extra flops over the exact
+// triangle for W = 1024-column panels.
+template <typename T>
+int backtransform_impl(const T *Q, int64_t ldq, int64_t m, const T *Z, int64_t ldz, int64_t n,
+                       const int64_t *cols_host, T *X, int64_t ldx) {
+    if (m < 0) return -3;
+    if (ldq < std::max<int64_t>(1, m)) return -2;
+    if (ldz < std::max<int64_t>(1, m)) return -5;
+    if (n < 0 || (!cols_host && n > m)) return -6;
+    if (ldx < std::max<int64_t>(1, m)) return -9;
+    if (m == 0 || n == 0) return 0;
+    if (!Q) return -1;
+    if (!Z) return -4;
+    if (!X) return -8;
+    if (cols_host)
+        for (int64_t q = 0; q < n; q++)
+            if (cols_host[q] < 0 || cols_host[q] >= m || (q > 0 && cols_host[q] <= cols_host[q - 1])) return -7;
+    if (int rc = ensure_init()) return rc;
+    CK(cudaMemset2DAsync(X, size_t(ldx) * sizeof(T), 0, size_t(m) * sizeof(T), size_t(n), g_stream));
+    SumPlanes sp;                       // complex: operand sums of Q and Z for the 3M kernel
+    if constexpr (S<T>::cplx_) {
+        if (gemm_variant() == 0 && gemm_presum_enabled()) {
+            sp.st = g_stream;
+            sp.ldu = (m + 2) & ~int64_t(1);
+            sp.ldx = int((m + 2) & ~int64_t(1));
+            CK(cudaMallocAsync(&sp.U, size_t(sp.ldu) * m * 8, g_stream));
+            CK(cudaMallocAsync(&sp.X, size_t(sp.ldx) * n * 8, g_stream));
+            presum_kernel<<<int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16)), 256, 0, g_stream>>>(
+                Q, ldq, m, sp.U, sp.ldu, 1.0, m);
+            CK_LAUNCH("presum_kernel");
+            presum_kernel<<<int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16)), 256, 0, g_stream>>>(
+                Z, ldz, n, sp.X, sp.ldx, 1.0, m);
+            CK_LAUNCH("presum_kernel");
+        }
+    }
+    constexpr int64_t W = 1024;
+    for (int64_t p0 = 0; p0 < n; p0 += W) {
+        const int64_t p1 = std::min(n, p0 + W);
+        const int64_t K = (cols_host ? cols_host[p1 - 1] : p1 - 1) + 1;
+        GemmArgs<T> g{};
+        g.U = Q; g.ldu = ldq; g.B = X; g.ldb = ldx;
+        g.M = m; g.N = p1 - p0; g.K = int(K);
+        g.a_r0 = 0; g.a_c0 = 0; g.c_r0 = 0; g.x_r0 = 0; g.col0 = p0;
+        g.X = Z; g.ldx = ldz;
+        g.dblk = nullptr;
+        if (sp.U) { g.As = sp.U; g.ldas = sp.ldu; g.Xsum = sp.X; g.ldxs = sp.ldx; }
+        if (int rc = launch_gemm<T, false>(g)) return rc;
+    }
+    const int blocks = int(std::min<int64_t>(cdiv(m * n, 256), int64_t(g_num_sms) * 16));
+    negate_kernel<T><<<blocks, 256, 0, g_stream>>>(X, ldx, m, n);
+    CK_LAUNCH("negate_kernel");
+    return 0;
+}
+
+template <typename T>
+int trevc_qz_impl(const T *Tm, int64_t ldt, int64_t m, const T *Q, int64_t ldq, T *X, int64_t ldx,
+                  double *scales, int32_t *scale_exp, int nb) {
+    if (m < 0) return -3;
+    if (ldt < std::max<int64_t>(1, m)) return -2;
+    if (ldq < std::max<int64_t>(1, m)) return -5;
+    if (ldx < std::max<int64_t>(1, m)) return -7;
+    if (nb != 0 && (nb < 1 || nb > 128)) return -10;
+    if (m == 0) return 0;
+    if (!Tm) return -1;
+    if (!Q) return -4;
+    if (!X) return -6;
+    if (int rc = ensure_init()) return rc;
+    T *Z = nullptr;
+    CK(cudaMallocAsync(&Z, size_t(m) * m * sizeof(T), g_stream));
+    int rc = trevc_impl<T>(Tm, ldt, m, nullptr, m, Z, m, scales, scale_exp, nb);
+    if (rc < 0) rc = 1;                       // arguments were validated above
+    if (!rc) rc = backtransform_impl<T>(Q, ldq, m, Z, m, m, nullptr, X, ldx);
+    if (rc < 0) rc = 1;
+    cudaFreeAsync(Z, g_stream);
+    return rc;
+}
+
 // ---------------------------------------------------------------- generalized solve (Alg. 7/8)
 // Per block: the generalized diagonal kernel (U' = U - lambda_j V on the fly, C = -lambda_j X(I1)),
 // then the update B(I0,act) = 2^d B(I0,act) - U(I0,I1) X(I1,act) - V(I0,I1) C (P:893-896 /
@@ -581,6 +661,23 @@ int trevc_d_cols(const double *T, int64_t ldt, int64_t m, const int64_t *cols_ho
 int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
                  mstrsm_dcomplex *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
     return trevc_impl<cplx>((const cplx *)T, ldt, m, cols_host, ncols, (cplx *)Z, ldz, scales, scale_exp, nb);
+}
+
+int eig_backtransform_d(const double *Q, int64_t ldq, int64_t m, const double *Z, int64_t ldz, int64_t n,
+                        const int64_t *cols_host, double *X, int64_t ldx) {
+    return backtransform_impl<double>(Q, ldq, m, Z, ldz, n, cols_host, X, ldx);
+}
+int eig_backtransform_z(const mstrsm_dcomplex *Q, int64_t ldq, int64_t m, const mstrsm_dcomplex *Z, int64_t ldz,
+                        int64_t n, const int64_t *cols_host, mstrsm_dcomplex *X, int64_t ldx) {
+    return backtransform_impl<cplx>((const cplx *)Q, ldq, m, (const cplx *)Z, ldz, n, cols_host, (cplx *)X, ldx);
+}
+int trevc_qz_d(const double *T, int64_t ldt, int64_t m, const double *Q, int64_t ldq, double *X, int64_t ldx,
+               double *scales, int32_t *scale_exp, int nb) {
+    return trevc_qz_impl<double>(T, ldt, m, Q, ldq, X, ldx, scales, scale_exp, nb);
+}
+int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dcomplex *Q, int64_t ldq,
+               mstrsm_dcomplex *X, int64_t ldx, double *scales, int32_t *scale_exp, int nb) {
+    return trevc_qz_impl<cplx>((const cplx *)T, ldt, m, (const cplx *)Q, ldq, (cplx *)X, ldx, scales, scale_exp, nb);
 }
 
 int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *Z_host, int64_t ldz,

@@ -26,7 +26,8 @@ def test_header_declares_the_survey_boundary():
     for required in ["mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
                      "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
                      "mstrsm_set_stream", "mstrsm_get_stream", "mstrsm_error_string", "mstrsm_status",
-                     "mstrsm_launch_count", "mstrsm_fp64_peak"]:
+                     "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d",
+                     "tgevc_z", "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z"]:
         assert required in names
 
 
@@ -70,6 +71,15 @@ def test_invalid_arguments_are_rejected_without_cuda():
     assert lib.trevc_z(P, 3, 3, P, 3, P, P, 200) == -8
     # pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma, flags, nb)
     assert lib.pseudospectra_z(P, 4, 4, P, 1, 0, P, P, P, 0) == -6
+    # eig_backtransform_z(Q, ldq, m, Z, ldz, n, cols, X, ldx)
+    assert lib.eig_backtransform_z(P, 3, 4, P, 4, 4, P, P, 4) == -2
+    assert lib.eig_backtransform_z(P, 4, 4, P, 4, 5, P, P, 4) == -6      # n > m without row bounds
+    assert lib.eig_backtransform_d(P, 4, 4, P, 4, 4, P, P, 3) == -9
+    bad = (ctypes.c_int64 * 2)(2, 2)
+    assert lib.eig_backtransform_d(ctypes.c_void_p(8), 4, 4, ctypes.c_void_p(8), 4, 2, bad, ctypes.c_void_p(8), 4) == -7
+    # trevc_qz_z(T, ldt, m, Q, ldq, X, ldx, scales, exp, nb)
+    assert lib.trevc_qz_z(P, 4, 4, P, 3, P, 4, P, P, 0) == -5
+    assert lib.trevc_qz_d(P, 4, 4, P, 4, P, 4, P, P, 129) == -10
 
 
 def test_empty_problems_return_zero_without_cuda():
@@ -79,6 +89,8 @@ def test_empty_problems_return_zero_without_cuda():
     assert lib.mstrsm_d_safe(P, 4, 4, P, P, 4, 0, P, 0) == 0
     assert lib.trevc_d(P, 1, 0, P, 1, P, P, 0) == 0
     assert lib.pseudospectra_z(P, 1, 0, P, 0, 15, P, P, P, 0) == 0
+    assert lib.eig_backtransform_z(P, 1, 0, P, 1, 0, P, P, 1) == 0
+    assert lib.trevc_qz_d(P, 1, 0, P, 1, P, 1, P, P, 0) == 0
 
 
 def test_error_strings():

@@ -6,7 +6,8 @@ algorithmic GFLOP/s (R18), units/s, and the per-kind kernel time from the live p
 
 Workloads: c1 (dense safe solve, real), c2 (TriangEig real), c3 (TriangEig complex), c4 (inverse
 Lanczos pseudospectra, 2 x 15 solves over 16384 points), g1 (GeneralizedTriangEig, complex m=4096,
-SURVEY §8f row f1).  Inputs are seeded synthetic stand-ins."""
+SURVEY §8f row f1), f2 / f2_bt (TriangEig + X = Q Z and the back-transformation alone, complex
+m=8192, row f2).  Inputs are seeded synthetic stand-ins."""
 import argparse
 import json
 import os
@@ -27,7 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--only", default="c1,c2,c3,c4,g1")
+    ap.add_argument("--only", default="c1,c2,c3,c4,g1,f2")
     a = ap.parse_args()
     import torch
     import paper_1607_01477_b200 as ms
@@ -60,6 +61,16 @@ def main():
         Tgd, Sgd = dev(Tg), dev(Sg)
         work["g1"] = (lambda: ms.tgevc(Tgd, Sgd, nb=64), eig_flops(4096, True, products=2), 4096,
                       "eigvecs/s", "g1: GeneralizedTriangEig complex pencil, m=4096, n_b=64 (SURVEY §8f f1)")
+    if "f2" in a.only:
+        mq = 8192
+        Tq = dev(inputs.c3_trevc_complex(mq))
+        Qq = dev(inputs.dense_q(mq, True))
+        Zq, _, _ = ms.trevc(Tq, nb=128)
+        bt_flops = 8.0 * mq * mq * (mq + 1) / 2.0          # X = Q Z, Z upper triangular (complex x4)
+        work["f2_bt"] = (lambda: ms.eig_backtransform(Qq, Zq), bt_flops, mq, "eigvecs/s",
+                         "f2: back-transformation X = Q Z alone, complex m=8192 (SURVEY §8f f2)")
+        work["f2"] = (lambda: ms.trevc_qz(Tq, Qq, nb=128), eig_flops(mq, True) + bt_flops, mq, "eigvecs/s",
+                      "f2: TriangEig + back-transformation (Eig's last two steps), complex m=8192, n_b=128")
     for name, (fn, flops, units, uname, desc) in work.items():
         for _ in range(a.warmup):
             fn()
