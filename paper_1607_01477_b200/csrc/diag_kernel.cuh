@@ -260,16 +260,16 @@ __device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const Acc &u
         if (t * LPC >= nmax) continue;                                     // warp-uniform
         Piv<T> pvt;                                                        // own row of slot t
         pvt.make(pivot(t * LPC + rl));
+        const int rr_hi = min(LPC - 1, nmax - 1 - t * LPC);               // rows >= nmax skipped
 #pragma unroll 1
-        for (int rr = LPC - 1; rr >= 0; rr--) {
+        for (int rr = rr_hi; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
-            if (sc >= nmax) continue;                                      // warp-uniform
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);          // P:82 / P:297
             const bool in = sc < nrow;
             const T xr = in ? xl : ST::zero();
             const int col = (sc * (sc - 1)) / 2;
-            if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + rl + LPC * t));
-            else if (rl == rr && in) y[t] = xl;
+            const T upd = ST::fnms(y[t], xr, ua(col + rl + LPC * t));
+            y[t] = rl < rr ? upd : ((rl == rr && in) ? xl : y[t]);
 #pragma unroll
             for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
         }
@@ -309,13 +309,13 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
     double ax_cur = 0.0, ax_prev = 0.0;
     int fl_cur = 0, fl_prev = 0;
     bool nonfinite = false;
-    auto replay = [&](int sc2, double axr, int fls) {
-        const bool live = guarded && sc2 < nrow;
+    auto replay = [&](int sc2, double axr, int fls, bool rep) {
+        const bool live = rep && guarded && sc2 < nrow;
         const double axt = __dmul_rn(axr, pow2i(fls - K));                 // paper frame
         const bool t1 = live && axt >= kOmega;
         const int k1 = t1 ? int(__double_as_longlong(axt) >> 52) - 1992 : 0;
         const double M = t1 ? __dmul_rn(axt, pow2i(-k1)) : axt;
-        double gn = __dadd_rn(t1 ? __dmul_rn(g, pow2i(-k1)) : g, __dmul_rn(M, ua.cnl(sc2)));
+        double gn = __dadd_rn(t1 ? __dmul_rn(g, pow2i(-k1)) : g, __dmul_rn(M, ua.cnl(sc2 < nmax ? sc2 : 0)));
         const bool t2 = live && gn >= kOmega;
         const int k2 = t2 ? int(__double_as_longlong(gn) >> 52) - 1992 : 0;
         if (t2) gn = __dmul_rn(gn, pow2i(-k2));
@@ -329,34 +329,36 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
         fl_prev = fl_cur;
         Piv<T> pvt;                                                        // own row of slot t
         pvt.make(pivot(t * LPC + rl));
+        const int rr_hi = min(LPC - 1, nmax - 1 - t * LPC);               // rows >= nmax skipped
 #pragma unroll 1
-        for (int rr = LPC - 1; rr >= 0; rr--) {
+        for (int rr = rr_hi; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
-            if (sc >= nmax) continue;                                      // warp-uniform
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);
             const bool in = sc < nrow;
             const T xr = in ? xl : ST::zero();
             const int col = (sc * (sc - 1)) / 2;
-            if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + rl + LPC * t));
-            else if (rl == rr && in) y[t] = xl;
+            const T upd = ST::fnms(y[t], xr, ua(col + rl + LPC * t));      // (index in the padded triangle)
+            y[t] = rl < rr ? upd : ((rl == rr && in) ? xl : y[t]);
 #pragma unroll
             for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
-            if (sc + LAG < nmax) {                                         // warp-uniform
+            {                                                              // replay row sc + LAG
                 const bool prev = rr + LAG >= LPC;
                 const int src = (rr + LAG) & (LPC - 1);
                 const double axr = __shfl_sync(0xffffffffu, prev ? ax_prev : ax_cur, src, LPC);
                 const int fls = __shfl_sync(0xffffffffu, prev ? fl_prev : fl_cur, src, LPC);
-                replay(sc + LAG, axr, fls);
+                replay(sc + LAG, axr, fls, sc + LAG < nmax);
             }
-            if (pend_prev >= MSTRSM_DIAG_FLUSH) {                          // lagged flush
+            if (pend_prev >= MSTRSM_DIAG_FLUSH) {                          // lagged flush (rare)
                 scale_all<true>(y, pend_prev);
                 Fl += pend_prev;
             }
             pend_prev = K - Fl;
-            if ((rr & (LAG - 1)) == 0 && rl >= rr && rl < rr + LAG) {      // record the chunk
-                ax_cur = modv(y[t]);
-                fl_cur = Fl;
-                nonfinite |= !(ax_cur <= 1.7976931348623157e308);         // every solved row passes here
+            if ((rr & (LAG - 1)) == 0) {                                   // warp-uniform: record the chunk
+                const bool rec = rl >= rr && rl < rr + LAG;
+                const double axn = modv(y[t]);
+                ax_cur = rec ? axn : ax_cur;
+                fl_cur = rec ? Fl : fl_cur;
+                nonfinite |= rec && !(axn <= 1.7976931348623157e308);     // every solved row passes here
             }
         }
     }
@@ -365,7 +367,7 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
         if (sc2 < nmax) {
             const double axr = __shfl_sync(0xffffffffu, ax_cur, sc2, LPC);
             const int fls = __shfl_sync(0xffffffffu, fl_cur, sc2, LPC);
-            replay(sc2, axr, fls);
+            replay(sc2, axr, fls, true);
         }
     }
     if (K != Fl) scale_all<false>(y, K - Fl);
