@@ -247,6 +247,11 @@ struct UAcc {
     }
 };
 
+#ifndef MSTRSM_DIAG_RR_UNROLL
+#define MSTRSM_DIAG_RR_UNROLL 1
+#endif
+constexpr int kDiagRrUnroll = MSTRSM_DIAG_RR_UNROLL;     // unroll of the runtime row loop
+
 // The substitution of one column group (Alg. 1; the unguarded branch of Alg. 4):
 // x_l = y_l / d_l, y(rows < l) -= x_l U(rows < l, l).  Every lane forms the quotient of its own
 // row of slot t and the owner's quotient is shuffled to the group, so the step-to-step chain is
@@ -261,7 +266,7 @@ __device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const Acc &u
         Piv<T> pvt;                                                        // own row of slot t
         pvt.make(pivot(t * LPC + rl));
         const int rr_hi = min(LPC - 1, nmax - 1 - t * LPC);               // rows >= nmax skipped
-#pragma unroll 1
+#pragma unroll kDiagRrUnroll
         for (int rr = rr_hi; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);          // P:82 / P:297
@@ -330,7 +335,7 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
         Piv<T> pvt;                                                        // own row of slot t
         pvt.make(pivot(t * LPC + rl));
         const int rr_hi = min(LPC - 1, nmax - 1 - t * LPC);               // rows >= nmax skipped
-#pragma unroll 1
+#pragma unroll kDiagRrUnroll
         for (int rr = rr_hi; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);
