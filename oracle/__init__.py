@@ -76,6 +76,9 @@ def _load():
         lib.oracle_pseudospectra_z.restype = c_int
         lib.oracle_pseudospectra_z.argtypes = [c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_vp, c_vp,
                                                c_vp, c_int, c_int]
+        lib.oracle_spectral_cloud_z.restype = c_int
+        lib.oracle_spectral_cloud_z.argtypes = [c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_dbl, c_vp, c_vp,
+                                                c_vp, c_vp, c_int, c_int]
         lib.oracle_tridiag_lmax.restype = c_dbl
         lib.oracle_tridiag_lmax.argtypes = [c_vp, c_vp, c_int]
         lib.oracle_zmod.restype = c_dbl
@@ -271,6 +274,64 @@ def pseudospectra(U, z, *, iters: int = 15, v0=None, nb: int = 64, nthreads: int
     if rc != 0:
         raise ValueError(f"oracle_pseudospectra_z returned {rc}")
     return sig, flags
+
+
+def spectral_cloud(U, z, *, maxit: int = 15, tol: float = 1e-10, v0=None, nb: int = 64,
+                   nthreads: int = 0):
+    """SpectralCloud: resolvent-norm estimates 1/sigma_min(U - z I) are returned
+    as sigma_min per point.  Alg. VL's Lanczos with per-point deflation (R33): a point stops after
+    the first step k >= 2 whose Ritz value theta_k = lambda_max(T_k) satisfies
+    |theta_k - theta_{k-1}| <= tol theta_k.  Returns (sigma, flags, its): flags bit0 = rescaled
+    solve (R25), bit1 = not settled within maxit steps; its = Lanczos steps taken."""
+    lib = _load()
+    U = _fortran(U, np.complex128)
+    m = U.shape[0]
+    z = np.ascontiguousarray(np.asarray(z, dtype=np.complex128).reshape(-1))
+    if v0 is None:
+        v0 = np.ones(m, dtype=np.complex128) / np.sqrt(m)
+    v0 = np.ascontiguousarray(np.asarray(v0, dtype=np.complex128))
+    sig = np.zeros(z.shape[0])
+    flags = np.zeros(z.shape[0], dtype=np.int32)
+    its = np.zeros(z.shape[0], dtype=np.int32)
+    rc = lib.oracle_spectral_cloud_z(_ptr(U), max(1, m), m, _ptr(z), z.shape[0], maxit, float(tol),
+                                     _ptr(v0), _ptr(sig), _ptr(flags), _ptr(its), nb, nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle_spectral_cloud_z returned {rc}")
+    return sig, flags, its
+
+
+def window_grid(x0: float, x1: float, nx: int, y0: float, y1: float, ny: int):
+    """SpectralWindow's grid: endpoint-inclusive linspace on both axes, point index
+    ix + nx * iy (R15)."""
+    gx = np.linspace(x0, x1, nx)
+    gy = np.linspace(y0, y1, ny)
+    return (gx[None, :] + 1j * gy[:, None]).reshape(-1)
+
+
+def spectral_window(U, x0, x1, nx, y0, y1, ny, **kw):
+    """SpectralWindow: SpectralCloud over the grid of window_grid."""
+    return spectral_cloud(U, window_grid(x0, x1, nx, y0, y1, ny), **kw)
+
+
+def portrait_window(U):
+    """SpectralPortrait's automatic window (R34, after S:411): the bounding box of
+    diag(U) padded on each side by 0.25 max(box width, box height, 1e-2 ||U||_inf), ||U||_inf the
+    max row sum of |U(i, k)| over k >= i.  Returns (x0, x1, y0, y1)."""
+    U = np.asarray(U)
+    d = np.diag(U)
+    x0, x1 = float(np.min(d.real)), float(np.max(d.real))
+    y0, y1 = float(np.min(d.imag)), float(np.max(d.imag))
+    unorm = float(np.max(np.sum(np.abs(np.triu(U)), axis=1)))
+    pad = 0.25 * max(x1 - x0, y1 - y0, 1e-2 * unorm)
+    return x0 - pad, x1 + pad, y0 - pad, y1 + pad
+
+
+def spectral_portrait(U, nx, ny, **kw):
+    """SpectralPortrait: SpectralWindow over portrait_window(U).  Returns
+    (sigma, flags, its, window)."""
+    x0, x1, y0, y1 = portrait_window(U)
+    sig, flags, its = spectral_window(U, x0, x1, nx, y0, y1, ny, **kw)
+    return sig, flags, its, (x0, x1, y0, y1)
 
 
 def tridiag_lmax(a, b) -> float:

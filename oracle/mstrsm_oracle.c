@@ -139,6 +139,7 @@ typedef struct {
     const ozc *U; int64_t ldu, m;
     const ozc *z; int64_t npts; int iters;
     const ozc *v0; double *sigma; int32_t *flags; int nb;
+    double tol; int32_t *its;       /* SpectralCloud deflation (R33); tol = 0: fixed iters */
     const double *cnlN, *PN, *cnlC, *PC; double deltaN, deltaC;
     int64_t next; pthread_mutex_t mu;
 } ps_job_t;
@@ -176,8 +177,8 @@ static void *ps_worker(void *arg)
         if (p >= J->npts) break;
         ozc z = J->z[p];
         for (int64_t i = 0; i < m; i++) { v[i] = J->v0[i]; vp[i] = z_zero(); }
-        double beta_prev = 0.0, amax = 0.0, sigma = 0.0;
-        int k = 0, flag = 0;
+        double beta_prev = 0.0, amax = 0.0, sigma = 0.0, theta_prev = 0.0;
+        int k = 0, flag = 0, conv = 0;
         for (int it = 0; it < J->iters; it++) {
             for (int64_t i = 0; i < m; i++) y[i] = v[i];
             int e1 = col_N_z(J->U, J->ldu, m, z, y, m, 1, J->nb, J->cnlN, J->PN, J->deltaN);
@@ -204,6 +205,11 @@ static void *ps_worker(void *arg)
             al[k] = a; be[k] = b; k++;
             if (a > amax) amax = a;
             if (b <= (double)m * 0x1p-52 * amax) break;     /* Krylov space exhausted */
+            if (J->tol > 0.0) {       /* R33: the point leaves the batch when its estimate settles */
+                double theta = oracle_tridiag_lmax(al, be, k);
+                if (k >= 2 && fabs(theta - theta_prev) <= J->tol * theta) { conv = 1; break; }
+                theta_prev = theta;
+            }
             for (int64_t i = 0; i < m; i++) {
                 vp[i] = v[i];
                 v[i].re = w[i].re / b;
@@ -216,15 +222,21 @@ static void *ps_worker(void *arg)
             sigma = lmax > 0.0 ? 1.0 / sqrt(lmax) : INFINITY;
         }
         J->sigma[p] = sigma;
+        /* bit1: tol > 0 and neither converged nor exhausted within iters steps */
+        if (J->tol > 0.0 && !flag && !conv && k == J->iters) flag |= 2;
         if (J->flags) J->flags[p] = flag;
+        if (J->its) J->its[p] = k;
     }
     free(v); free(vp); free(y); free(w); free(al); free(be);
     return NULL;
 }
 
-int oracle_pseudospectra_z(const ozc *U, int64_t ldu, int64_t m, const ozc *z,
-                           int64_t npts, int iters, const ozc *v0, double *sigma,
-                           int32_t *flags, int nb, int nthreads)
+/* SpectralCloud: as oracle_pseudospectra_z, but with tol > 0 a point stops after
+ * the first step k >= 2 with |theta_k - theta_{k-1}| <= tol theta_k, theta_k = lambda_max of the
+ * k-step tridiagonal (R33); its[p] = Lanczos steps taken; flags bit1 = not settled in `iters`. */
+int oracle_spectral_cloud_z(const ozc *U, int64_t ldu, int64_t m, const ozc *z,
+                            int64_t npts, int iters, double tol, const ozc *v0, double *sigma,
+                            int32_t *flags, int32_t *its, int nb, int nthreads)
 {
     if (m < 1 || npts < 0 || iters < 1 || nb < 1) return -1;
     if (npts == 0) return 0;
@@ -239,6 +251,7 @@ int oracle_pseudospectra_z(const ozc *U, int64_t ldu, int64_t m, const ozc *z,
     ps_job_t J;
     J.U = U; J.ldu = ldu; J.m = m; J.z = z; J.npts = npts; J.iters = iters;
     J.v0 = v0; J.sigma = sigma; J.flags = flags; J.nb = nb;
+    J.tol = tol > 0.0 ? tol : 0.0; J.its = its;
     J.cnlN = cnlN; J.PN = PN; J.cnlC = cnlC; J.PC = PC;
     J.deltaN = uN > 0.0 ? ldexp(uN, -52) : DBL_MIN;
     J.deltaC = uC > 0.0 ? ldexp(uC, -52) : DBL_MIN;
@@ -248,6 +261,13 @@ int oracle_pseudospectra_z(const ozc *U, int64_t ldu, int64_t m, const ozc *z,
     pthread_mutex_destroy(&J.mu);
     free(cnlN); free(cnlC); free(PN); free(PC);
     return 0;
+}
+
+int oracle_pseudospectra_z(const ozc *U, int64_t ldu, int64_t m, const ozc *z,
+                           int64_t npts, int iters, const ozc *v0, double *sigma,
+                           int32_t *flags, int nb, int nthreads)
+{
+    return oracle_spectral_cloud_z(U, ldu, m, z, npts, iters, 0.0, v0, sigma, flags, NULL, nb, nthreads);
 }
 
 /* Exposed for tests: the scalar helpers, so the pins can exercise them. */
