@@ -141,6 +141,34 @@ int pseudospectra_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstr
                     int64_t npts, int iters, const mstrsm_dcomplex *v0, double *sigma_min,
                     int32_t *flags, int nb);
 
+/* SpectralCloud: pseudospectra_z with per-point deflation.
+ * With tol > 0 a point leaves the batch after the first Lanczos step k >= 2 whose Ritz value
+ * theta_k = lambda_max(T_k) satisfies |theta_k - theta_{k-1}| <= tol theta_k (R33); the remaining
+ * columns are compacted so later solves run on fewer shifts (one host synchronisation per step).
+ * tol = 0: exactly pseudospectra_z with maxit steps.
+ *   sigma  npts doubles (device): sigma_min(U - z_p I) estimates
+ *   flags  nullable npts int32 (device): bit0 = rescaled solve (R25), bit1 = not settled within
+ *          maxit steps (tol > 0)
+ *   its    nullable npts int32 (device): Lanczos steps taken
+ * Errors: -i for argument i (tol must be >= 0), 1 CUDA error.                              */
+int spectral_cloud_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z,
+                     int64_t npts, int maxit, double tol, const mstrsm_dcomplex *v0, double *sigma,
+                     int32_t *flags, int32_t *its, int nb);
+
+/* SpectralWindow: SpectralCloud over the nx x ny grid x_i = linspace(x0, x1, nx),
+ * y_j = linspace(y0, y1, ny) (endpoint-inclusive, numpy.linspace arithmetic), point index
+ * i + nx j (R15).  sigma / flags / its have nx*ny entries.                                 */
+int spectral_window_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, double x0, double x1,
+                      int64_t nx, double y0, double y1, int64_t ny, int maxit, double tol,
+                      const mstrsm_dcomplex *v0, double *sigma, int32_t *flags, int32_t *its, int nb);
+
+/* SpectralPortrait: SpectralWindow over the automatic window (R34): the bounding box
+ * of diag(U) padded on each side by 0.25 max(box width, box height, 1e-2 ||U||_inf).
+ * window_host: nullable HOST pointer, receives (x0, x1, y0, y1).  Synchronises the stream.  */
+int spectral_portrait_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, int64_t nx, int64_t ny,
+                        int maxit, double tol, const mstrsm_dcomplex *v0, double *sigma,
+                        int32_t *flags, int32_t *its, double *window_host, int nb);
+
 /* ------------------------------------------------------------------------------------
  * Generalized multi-shift triangular solve, appendix Alg. 7 (safe = 0) and Alg. 8
  * (safe = 1): for j = 0..n-1 find x_j and c_j = 2^{e_j} in [0,1] with

@@ -25,6 +25,8 @@ __all__ = [
     "mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
+    "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
+    "spectral_portrait",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
@@ -58,6 +60,10 @@ def load():
         "trevc_z_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
+        "spectral_cloud_z": [P, c_i64, c_i64, P, c_i64, c_int, c_dbl, P, P, P, P, c_int],
+        "spectral_window_z": [P, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_dbl, c_dbl, c_i64, c_int, c_dbl, P, P, P, P,
+                              c_int],
+        "spectral_portrait_z": [P, c_i64, c_i64, c_i64, c_i64, c_int, c_dbl, P, P, P, P, P, c_int],
         "mstrsm_d_gen": [c_int, P, c_i64, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
         "mstrsm_z_gen": [c_int, P, c_i64, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int],
         "tgevc_d": [P, c_i64, P, c_i64, c_i64, P, c_i64, P, P, P, c_int],
@@ -214,6 +220,21 @@ def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
           _ptr(flags), nb)
 
 
+def spectral_cloud_z(U, ldu, m, z, npts, maxit, tol, v0, sigma, flags, its, nb):
+    _call("spectral_cloud_z", _ptr(U), ldu, m, _ptr(z), npts, maxit, float(tol), _ptr(v0), _ptr(sigma),
+          _ptr(flags), _ptr(its), nb)
+
+
+def spectral_window_z(U, ldu, m, x0, x1, nx, y0, y1, ny, maxit, tol, v0, sigma, flags, its, nb):
+    _call("spectral_window_z", _ptr(U), ldu, m, float(x0), float(x1), nx, float(y0), float(y1), ny, maxit,
+          float(tol), _ptr(v0), _ptr(sigma), _ptr(flags), _ptr(its), nb)
+
+
+def spectral_portrait_z(U, ldu, m, nx, ny, maxit, tol, v0, sigma, flags, its, window_host, nb):
+    _call("spectral_portrait_z", _ptr(U), ldu, m, nx, ny, maxit, float(tol), _ptr(v0), _ptr(sigma),
+          _ptr(flags), _ptr(its), window_host, nb)
+
+
 def mstrsm_status() -> int:
     lib = load()
     _bind_stream(lib)
@@ -367,6 +388,38 @@ def trevc_qz(T, Q, *, nb: int = 64):
     f = trevc_qz_z if T.dtype == torch.complex128 else trevc_qz_d
     f(T, _ld(T), m, Q, _ld(Q), X, _ld(X), scales, exps, nb)
     return X, scales, exps
+
+
+def _cloud_out(n, dev):
+    torch = _torch()
+    return (torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+            torch.empty(n, dtype=torch.int32, device=dev))
+
+
+def spectral_cloud(U, z, v0, *, maxit: int = 15, tol: float = 1e-10, nb: int = 64):
+    """SpectralCloud: sigma_min(U - z_p I) with per-point deflation (R33); returns
+    (sigma, flags, its) as CUDA tensors."""
+    m, npts = U.shape[0], z.shape[0]
+    sigma, flags, its = _cloud_out(npts, U.device)
+    spectral_cloud_z(U, _ld(U), m, z, npts, maxit, tol, v0, sigma, flags, its, nb)
+    return sigma, flags, its
+
+
+def spectral_window(U, x0, x1, nx, y0, y1, ny, v0, *, maxit: int = 15, tol: float = 1e-10, nb: int = 64):
+    """SpectralWindow over the nx x ny grid (R15 order); returns (sigma, flags, its)."""
+    m = U.shape[0]
+    sigma, flags, its = _cloud_out(nx * ny, U.device)
+    spectral_window_z(U, _ld(U), m, x0, x1, nx, y0, y1, ny, maxit, tol, v0, sigma, flags, its, nb)
+    return sigma, flags, its
+
+
+def spectral_portrait(U, nx, ny, v0, *, maxit: int = 15, tol: float = 1e-10, nb: int = 64):
+    """SpectralPortrait: the automatic window of R34; returns (sigma, flags, its, window)."""
+    m = U.shape[0]
+    sigma, flags, its = _cloud_out(nx * ny, U.device)
+    win = (ctypes.c_double * 4)()
+    spectral_portrait_z(U, _ld(U), m, nx, ny, maxit, tol, v0, sigma, flags, its, ctypes.cast(win, c_vp), nb)
+    return sigma, flags, its, tuple(win)
 
 
 def pseudospectra(U, z, v0, *, iters: int = 15, nb: int = 64):

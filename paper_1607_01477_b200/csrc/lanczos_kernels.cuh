@@ -6,12 +6,17 @@
 
 namespace mstrsm {
 
+// Vectors are stored by batch slot (columns 0..n_act-1 of V, Vp, W, Y); the per-point scalars by
+// point id p = pid[slot].  SpectralCloud deflation (R33) compacts the slots between steps.
 struct LanczosState {
-    cplx *V, *Vp, *W, *Y;        // m x npts each (column per point)
-    double *alpha, *beta;        // iters x npts
+    cplx *V, *Vp, *W, *Y;        // m x npts each (column per slot)
+    double *alpha, *beta;        // iters x npts, by point
     int *kdone, *active, *flags;
-    double *amax, *beta_prev, *sigma;
-    const int *e1, *e2;          // exponents of the two solves of this step
+    double *amax, *beta_prev, *sigma, *theta_prev;
+    const int *e1, *e2;          // exponents of the two solves of this step, by slot
+    const int *pid;              // slot -> point
+    int64_t npts;                // points in the problem (stride of alpha / beta)
+    double tol;                  // deflation tolerance (0: fixed iteration count)
 };
 
 // copy src -> dst for active points (m x npts, column-major), one warp per point
@@ -39,22 +44,24 @@ __global__ void lanczos_init_kernel(const cplx *__restrict__ v0, LanczosState st
         }
         if (lane == 0) {
             st.kdone[p] = 0; st.active[p] = 1; st.flags[p] = 0;
-            st.amax[p] = 0.0; st.beta_prev[p] = 0.0; st.sigma[p] = 0.0;
+            st.amax[p] = 0.0; st.beta_prev[p] = 0.0; st.sigma[p] = 0.0; st.theta_prev[p] = 0.0;
         }
     }
 }
 
 // One Lanczos step for every active point, after y = (U - zI)^{-1} v (in Y, exponent e1) and
 // w = (U - zI)^{-H} y (in W, exponent e2).
-__global__ void lanczos_step_kernel(LanczosState st, int64_t m, int64_t npts, int it, int iters) {
+__global__ void lanczos_step_kernel(LanczosState st, int64_t m, int64_t nslots, int it, int iters) {
     int lane = threadIdx.x & 31;
     int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t p = w; p < npts; p += nw) {
+    const int64_t npts = st.npts;
+    for (int64_t sl = w; sl < nslots; sl += nw) {
+        const int64_t p = st.pid[sl];
         if (!st.active[p]) continue;
-        cplx *V = st.V + p * m, *Vp = st.Vp + p * m, *W = st.W + p * m;
-        const cplx *Y = st.Y + p * m;
-        int e1 = st.e1[p], e2 = st.e2[p];
+        cplx *V = st.V + sl * m, *Vp = st.Vp + sl * m, *W = st.W + sl * m;
+        const cplx *Y = st.Y + sl * m;
+        int e1 = st.e1[sl], e2 = st.e2[sl];
         if (e1 < 0 || e2 < 0) {
             // near-singular point (R25): sigma <= c1 / ||y||_2, scaled 2-norm
             double s = 0.0;
@@ -126,35 +133,112 @@ __device__ inline int sturm_below_dev(const double *al, const double *be, int64_
     return cnt;
 }
 
+// lambda_max of the k x k tridiagonal (al[i * stride], be[i * stride]) by Sturm bisection (R14).
+__device__ inline double tridiag_lmax_dev(const double *al, const double *be, int64_t stride, int k) {
+    if (k == 1) return al[0];
+    double lo = 1.7976931348623157e308, hi = -1.7976931348623157e308, b2 = 0.0;
+    for (int i = 0; i < k; i++) {
+        double r = (i > 0 ? fabs(be[int64_t(i - 1) * stride]) : 0.0) + (i < k - 1 ? fabs(be[int64_t(i) * stride]) : 0.0);
+        double ai = al[int64_t(i) * stride];
+        lo = fmin(lo, ai - r);
+        hi = fmax(hi, ai + r);
+        if (i < k - 1) { double b = be[int64_t(i) * stride]; b2 = fmax(b2, b * b); }
+    }
+    double pivmin = 2.2250738585072014e-308 * fmax(b2, 1.0);
+    for (int itb = 0; itb < 400; itb++) {
+        double wd = fmax(fabs(lo), fabs(hi));
+        if (hi - lo <= 4.0 * 0x1p-52 * wd) break;
+        double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (sturm_below_dev(al, be, stride, k, mid, pivmin) == k) hi = mid; else lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
 __global__ void bisect_sigma_kernel(LanczosState st, int64_t npts) {
     int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= npts || st.flags[p]) return;
+    if (p >= npts || (st.flags[p] & 1)) return;
     int k = st.kdone[p];
-    const double *al = st.alpha + p, *be = st.beta + p;
-    double lmax;
     if (k <= 0) { st.sigma[p] = __longlong_as_double(0x7ff0000000000000ll); return; }
-    if (k == 1) {
-        lmax = al[0];
-    } else {
-        double lo = 1.7976931348623157e308, hi = -1.7976931348623157e308, b2 = 0.0;
-        for (int i = 0; i < k; i++) {
-            double r = (i > 0 ? fabs(be[int64_t(i - 1) * npts]) : 0.0) + (i < k - 1 ? fabs(be[int64_t(i) * npts]) : 0.0);
-            double ai = al[int64_t(i) * npts];
-            lo = fmin(lo, ai - r);
-            hi = fmax(hi, ai + r);
-            if (i < k - 1) { double b = be[int64_t(i) * npts]; b2 = fmax(b2, b * b); }
-        }
-        double pivmin = 2.2250738585072014e-308 * fmax(b2, 1.0);
-        for (int itb = 0; itb < 400; itb++) {
-            double wd = fmax(fabs(lo), fabs(hi));
-            if (hi - lo <= 4.0 * 0x1p-52 * wd) break;
-            double mid = 0.5 * (lo + hi);
-            if (mid <= lo || mid >= hi) break;
-            if (sturm_below_dev(al, be, npts, k, mid, pivmin) == k) hi = mid; else lo = mid;
-        }
-        lmax = 0.5 * (lo + hi);
-    }
+    const double lmax = tridiag_lmax_dev(st.alpha + p, st.beta + p, npts, k);
     st.sigma[p] = lmax > 0.0 ? 1.0 / sqrt(lmax) : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// SpectralCloud deflation (R33), one thread per slot: after step k (>= 2) a point whose Ritz value
+// moved by at most tol theta_k leaves the batch.
+__global__ void converge_kernel(LanczosState st, int64_t nslots) {
+    int64_t sl = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (sl >= nslots) return;
+    const int64_t p = st.pid[sl];
+    if (!st.active[p]) return;
+    const int k = st.kdone[p];
+    const double th = tridiag_lmax_dev(st.alpha + p, st.beta + p, st.npts, k);
+    if (k >= 2 && fabs(th - st.theta_prev[p]) <= st.tol * th) st.active[p] = 0;
+    else st.theta_prev[p] = th;
+}
+
+// Stable compaction of the active slots (one block): newpid[j] = pid[src[j]] for the j-th slot
+// still active, *count = number kept.
+__global__ void compact_slots_kernel(const int *__restrict__ pid, const int *__restrict__ active, int64_t nslots,
+                                     int *__restrict__ newpid, int *__restrict__ src, int *__restrict__ count) {
+    __shared__ int warp_tot[32];
+    __shared__ int base;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < nslots; c0 += blockDim.x) {
+        const int64_t sl = c0 + tid;
+        const int keep = sl < nslots && active[pid[sl]] ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        const int inwarp = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) warp_tot[wid] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < wid; w++) off += warp_tot[w];
+        if (keep) {
+            newpid[off + inwarp] = pid[sl];
+            src[off + inwarp] = int(sl);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int t = 0;
+            for (int w = 0; w < nwarp; w++) t += warp_tot[w];
+            base += t;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *count = base;
+}
+
+// dst(:, j) = src(:, idx[j]) for j < n (m x n complex columns), one warp per column
+__global__ void gather_cols_kernel(const cplx *__restrict__ srcv, cplx *__restrict__ dst, const int *__restrict__ idx,
+                                   int64_t m, int64_t n) {
+    int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t j = w; j < n; j += nw) {
+        const cplx *s = srcv + int64_t(idx[j]) * m;
+        cplx *d = dst + j * m;
+        for (int64_t i = lane; i < m; i += 32) d[i] = s[i];
+    }
+}
+
+__global__ void gather_z_kernel(const cplx *__restrict__ z, const int *__restrict__ pid, cplx *__restrict__ zc, int64_t n) {
+    int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) zc[j] = z[pid[j]];
+}
+
+__global__ void iota_kernel(int *__restrict__ v, int64_t n) {
+    int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) v[j] = int(j);
+}
+
+// flags bit1 (R33): deflation on and the point neither settled nor stopped; its = steps taken
+__global__ void cloud_finish_kernel(LanczosState st, int64_t npts, int32_t *__restrict__ its) {
+    int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= npts) return;
+    if (st.tol > 0.0 && st.active[p] && !(st.flags[p] & 1)) st.flags[p] |= 2;
+    if (its) its[p] = st.kdone[p];
 }
 
 }  // namespace mstrsm

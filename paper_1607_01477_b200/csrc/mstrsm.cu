@@ -530,19 +530,24 @@ int tgevc_impl(const T *Tm, int64_t ldt, const T *Sm, int64_t lds, int64_t m, T 
 }
 
 // ---------------------------------------------------------------- pseudospectra driver (a.7)
-int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int64_t npts, int iters,
-                       const cplx *v0, double *sigma, int32_t *flags, int nb) {
+// Alg. VL batched over all points.  tol > 0: SpectralCloud deflation
+// (R33) -- after every step the points whose Ritz value settled leave the batch and the remaining
+// columns are compacted (stable), so later solves run on fewer shifts; per-point results are
+// unchanged by the compaction (columns are independent).
+int spectral_cloud_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int64_t npts, int iters,
+                        double tol, const cplx *v0, double *sigma, int32_t *flags, int32_t *its, int nb) {
     if (m < 0) return -3;
     if (ldu < std::max<int64_t>(1, m)) return -2;
     if (npts < 0) return -5;
     if (iters < 1) return -6;
+    if (!(tol >= 0.0)) return -7;
     if (nb == 0) nb = 64;
-    if (nb < 1 || nb > 128) return -10;
+    if (nb < 1 || nb > 128) return -12;
     if (m == 0 || npts == 0) return 0;
     if (!U) return -1;
     if (!z) return -4;
-    if (!v0) return -7;
-    if (!sigma) return -8;
+    if (!v0) return -8;
+    if (!sigma) return -9;
     if (int rc = ensure_init()) return rc;
     Work wN, wC;
     if (int rc = alloc_work<cplx>(wN, m, npts, nb, false, false)) return rc;
@@ -554,7 +559,7 @@ int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int
     if (int rc = make_sum_planes<cplx>(spC, 1, U, ldu, m, npts, nb)) return rc;
     size_t vec = size_t(m) * npts * sizeof(cplx);
     size_t small = size_t(npts) * 8;
-    size_t total = 4 * vec + 2 * size_t(iters) * small + 8 * small + 1024;
+    size_t total = 4 * vec + 2 * size_t(iters) * small + 16 * small + 4096;
     char *buf = nullptr;
     CK(cudaMallocAsync(&buf, total, g_stream));
     size_t off = 0;
@@ -565,37 +570,152 @@ int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int
     st.kdone = (int *)take(npts * 4); st.active = (int *)take(npts * 4);
     st.flags = flags ? (int *)flags : (int *)take(npts * 4);
     st.amax = (double *)take(small); st.beta_prev = (double *)take(small); st.sigma = sigma;
+    st.theta_prev = (double *)take(small);
     int *e1 = (int *)take(npts * 4), *e2 = (int *)take(npts * 4);
     st.e1 = e1; st.e2 = e2;
+    int *pid = (int *)take(npts * 4), *pid2 = (int *)take(npts * 4), *src = (int *)take(npts * 4);
+    int *count = (int *)take(64);
+    cplx *zc = (cplx *)take(npts * 16), *zc2 = (cplx *)take(npts * 16);
+    st.pid = pid; st.npts = npts; st.tol = tol;
     int blocks = int(std::min<int64_t>(cdiv(npts, 8), int64_t(g_num_sms) * 16));
     if (blocks < 1) blocks = 1;
+    const int pblocks = int(cdiv(npts, 256));
     lanczos_init_kernel<<<blocks, 256, 0, g_stream>>>(v0, st, m, npts);
     CK_LAUNCH("lanczos_init_kernel");
+    iota_kernel<<<pblocks, 256, 0, g_stream>>>(pid, npts);
+    CK_LAUNCH("iota_kernel");
+    CK(cudaMemcpyAsync(zc, z, npts * 16, cudaMemcpyDeviceToDevice, g_stream));
+    int64_t nact = npts;
     int rc = 0;
-    for (int it = 0; it < iters && !rc; it++) {
-        copy_cols_kernel<<<blocks, 256, 0, g_stream>>>(st.V, st.Y, m, npts);
+    for (int it = 0; it < iters && !rc && nact > 0; it++) {
+        const int ab = int(std::min<int64_t>(cdiv(nact, 8), int64_t(g_num_sms) * 16));
+        copy_cols_kernel<<<ab, 256, 0, g_stream>>>(st.V, st.Y, m, nact);
         CK_LAUNCH("copy_cols_kernel");
-        init_rhs_kernel<cplx><<<blocks, 256, 0, g_stream>>>(st.Y, m, m, npts, nullptr, z, 1, wN.G, wN.e, g_flag);
+        init_rhs_kernel<cplx><<<ab, 256, 0, g_stream>>>(st.Y, m, m, nact, nullptr, zc, 1, wN.G, wN.e, g_flag);
         CK_LAUNCH("init_rhs_kernel");
-        rc = blocked_solve<cplx, true>(0, U, ldu, m, z, 1, st.Y, m, npts, nullptr, nullptr, nb, wN, spN.U, spN.X, spN.ldu, spN.ldx);
-        if (!rc) rc = finalize<cplx>(0, 1, st.Y, m, m, npts, nb, nullptr, nullptr, e1, nullptr, wN);
+        rc = blocked_solve<cplx, true>(0, U, ldu, m, zc, 1, st.Y, m, nact, nullptr, nullptr, nb, wN, spN.U, spN.X, spN.ldu, spN.ldx);
+        if (!rc) rc = finalize<cplx>(0, 1, st.Y, m, m, nact, nb, nullptr, nullptr, e1, nullptr, wN);
         if (rc) break;
-        copy_cols_kernel<<<blocks, 256, 0, g_stream>>>(st.Y, st.W, m, npts);
+        copy_cols_kernel<<<ab, 256, 0, g_stream>>>(st.Y, st.W, m, nact);
         CK_LAUNCH("copy_cols_kernel");
-        init_rhs_kernel<cplx><<<blocks, 256, 0, g_stream>>>(st.W, m, m, npts, nullptr, nullptr, 0, wC.G, wC.e, nullptr);
+        init_rhs_kernel<cplx><<<ab, 256, 0, g_stream>>>(st.W, m, m, nact, nullptr, nullptr, 0, wC.G, wC.e, nullptr);
         CK_LAUNCH("init_rhs_kernel");
-        rc = blocked_solve<cplx, true>(1, U, ldu, m, z, 1, st.W, m, npts, nullptr, nullptr, nb, wC, spC.U, spC.X, spC.ldu, spC.ldx);
-        if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, npts, nb, nullptr, nullptr, e2, nullptr, wC);
+        rc = blocked_solve<cplx, true>(1, U, ldu, m, zc, 1, st.W, m, nact, nullptr, nullptr, nb, wC, spC.U, spC.X, spC.ldu, spC.ldx);
+        if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, nact, nb, nullptr, nullptr, e2, nullptr, wC);
         if (rc) break;
-        lanczos_step_kernel<<<blocks, 256, 0, g_stream>>>(st, m, npts, it, iters);
+        lanczos_step_kernel<<<ab, 256, 0, g_stream>>>(st, m, nact, it, iters);
         CK_LAUNCH("lanczos_step_kernel");
+        if (tol > 0.0 && it + 1 < iters) {
+            converge_kernel<<<int(cdiv(nact, 128)), 128, 0, g_stream>>>(st, nact);
+            CK_LAUNCH("converge_kernel");
+            compact_slots_kernel<<<1, 1024, 0, g_stream>>>(pid, st.active, nact, pid2, src, count);
+            CK_LAUNCH("compact_slots_kernel");
+            int nnew = 0;
+            CK(cudaMemcpyAsync(&nnew, count, 4, cudaMemcpyDeviceToHost, g_stream));
+            CK(cudaStreamSynchronize(g_stream));
+            if (nnew < nact) {          // V -> Y, Vp -> W (scratch until the next step), then swap
+                const int gb = int(std::min<int64_t>(cdiv(std::max(nnew, 1), 8), int64_t(g_num_sms) * 16));
+                if (nnew > 0) {
+                    gather_cols_kernel<<<gb, 256, 0, g_stream>>>(st.V, st.Y, src, m, nnew);
+                    CK_LAUNCH("gather_cols_kernel");
+                    gather_cols_kernel<<<gb, 256, 0, g_stream>>>(st.Vp, st.W, src, m, nnew);
+                    CK_LAUNCH("gather_cols_kernel");
+                    gather_z_kernel<<<int(cdiv(nnew, 256)), 256, 0, g_stream>>>(z, pid2, zc2, nnew);
+                    CK_LAUNCH("gather_z_kernel");
+                }
+                std::swap(st.V, st.Y);
+                std::swap(st.Vp, st.W);
+                std::swap(pid, pid2);
+                std::swap(zc, zc2);
+                st.pid = pid;
+                nact = nnew;
+            }
+        } else if (tol > 0.0) {
+            converge_kernel<<<int(cdiv(nact, 128)), 128, 0, g_stream>>>(st, nact);
+            CK_LAUNCH("converge_kernel");
+        }
     }
     if (!rc) {
         bisect_sigma_kernel<<<int(cdiv(npts, 128)), 128, 0, g_stream>>>(st, npts);
         CK_LAUNCH("bisect_sigma_kernel");
+        cloud_finish_kernel<<<pblocks, 256, 0, g_stream>>>(st, npts, its);
+        CK_LAUNCH("cloud_finish_kernel");
     }
     cudaFreeAsync(buf, g_stream);
     return rc;
+}
+
+int pseudospectra_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, int64_t npts, int iters,
+                       const cplx *v0, double *sigma, int32_t *flags, int nb) {
+    int rc = spectral_cloud_impl(U, ldu, m, z, npts, iters, 0.0, v0, sigma, flags, nullptr, nb);
+    if (rc < 0) rc = rc == -12 ? -10 : (rc == -7 ? -6 : (rc <= -8 ? rc + 1 : rc));   // pseudospectra_z positions
+    return rc;
+}
+
+// SpectralWindow grid (R15, as numpy.linspace): x_i = i * step + x0 (no FMA), last point = x1
+__global__ void window_grid_kernel(double x0, double x1, int64_t nx, double y0, double y1, int64_t ny, cplx *z) {
+    int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= nx * ny) return;
+    const int64_t ix = q % nx, iy = q / nx;
+    auto lin = [](double a, double b, int64_t n, int64_t i) {
+        if (n > 1 && i == n - 1) return b;
+        const double step = n > 1 ? (b - a) / double(n - 1) : 0.0;
+        return __dadd_rn(__dmul_rn(double(i), step), a);
+    };
+    z[q] = make_double2(lin(x0, x1, nx, ix), lin(y0, y1, ny, iy));
+}
+
+int spectral_window_impl(const cplx *U, int64_t ldu, int64_t m, double x0, double x1, int64_t nx, double y0,
+                         double y1, int64_t ny, int iters, double tol, const cplx *v0, double *sigma,
+                         int32_t *flags, int32_t *its, int nb) {
+    if (nx < 0) return -6;
+    if (ny < 0) return -9;
+    if (!(std::isfinite(x0) && std::isfinite(x1))) return -4;
+    if (!(std::isfinite(y0) && std::isfinite(y1))) return -7;
+    if (m == 0 || nx == 0 || ny == 0) return m < 0 ? -3 : 0;
+    if (int rc = ensure_init()) return rc;
+    const int64_t npts = nx * ny;
+    cplx *z = nullptr;
+    CK(cudaMallocAsync(&z, npts * 16, g_stream));
+    window_grid_kernel<<<int(cdiv(npts, 256)), 256, 0, g_stream>>>(x0, x1, nx, y0, y1, ny, z);
+    CK_LAUNCH("window_grid_kernel");
+    int rc = spectral_cloud_impl(U, ldu, m, z, npts, iters, tol, v0, sigma, flags, its, nb);
+    if (rc < 0) {                                 // map spectral_cloud positions to spectral_window's
+        const int map[13] = {0, -1, -2, -3, -4, -5, -10, -11, -12, -13, -14, -15, -16};
+        rc = -rc < 13 ? map[-rc] : rc;
+    }
+    cudaFreeAsync(z, g_stream);
+    return rc;
+}
+
+// SpectralPortrait window (R34): bounding box of diag(U) padded by 0.25 max(width, height,
+// 1e-2 ||U||_inf) (||U||_inf as R4: max row sum of |U(i,k)|, k >= i).  Host synchronising.
+int portrait_window(const cplx *U, int64_t ldu, int64_t m, double win[4]) {
+    std::vector<cplx> d(m);
+    CK(cudaMemcpy2DAsync(d.data(), sizeof(cplx), U, size_t(ldu + 1) * sizeof(cplx), sizeof(cplx), size_t(m),
+                         cudaMemcpyDeviceToHost, g_stream));
+    const int64_t nchunks = cdiv(m, kRowsumChunk);
+    double *part = nullptr, *rs = nullptr;
+    CK(cudaMallocAsync(&part, size_t(nchunks) * m * 8, g_stream));
+    CK(cudaMallocAsync(&rs, size_t(m) * 8, g_stream));
+    rowsum_n_kernel<cplx><<<dim3(unsigned(cdiv(m, 128)), unsigned(nchunks)), 128, 0, g_stream>>>(U, ldu, m, part);
+    CK_LAUNCH("rowsum_n_kernel");
+    rowsum_reduce_kernel<<<int(cdiv(m, 256)), 256, 0, g_stream>>>(m, nchunks, part, rs);
+    CK_LAUNCH("rowsum_reduce_kernel");
+    std::vector<double> rsh(m);
+    CK(cudaMemcpyAsync(rsh.data(), rs, size_t(m) * 8, cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    cudaFreeAsync(part, g_stream);
+    cudaFreeAsync(rs, g_stream);
+    double xa = d[0].x, xb = d[0].x, ya = d[0].y, yb = d[0].y, un = 0.0;
+    for (int64_t i = 0; i < m; i++) {
+        xa = std::min(xa, d[i].x); xb = std::max(xb, d[i].x);
+        ya = std::min(ya, d[i].y); yb = std::max(yb, d[i].y);
+        un = std::max(un, rsh[i]);
+    }
+    const double pad = 0.25 * std::max(std::max(xb - xa, yb - ya), 1e-2 * un);
+    win[0] = xa - pad; win[1] = xb + pad; win[2] = ya - pad; win[3] = yb + pad;
+    return 0;
 }
 
 }  // namespace
@@ -661,6 +781,40 @@ int trevc_d_cols(const double *T, int64_t ldt, int64_t m, const int64_t *cols_ho
 int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
                  mstrsm_dcomplex *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
     return trevc_impl<cplx>((const cplx *)T, ldt, m, cols_host, ncols, (cplx *)Z, ldz, scales, scale_exp, nb);
+}
+
+int spectral_cloud_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z, int64_t npts,
+                     int maxit, double tol, const mstrsm_dcomplex *v0, double *sigma, int32_t *flags, int32_t *its,
+                     int nb) {
+    return spectral_cloud_impl((const cplx *)U, ldu, m, (const cplx *)z, npts, maxit, tol, (const cplx *)v0, sigma,
+                               flags, its, nb);
+}
+int spectral_window_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, double x0, double x1, int64_t nx, double y0,
+                      double y1, int64_t ny, int maxit, double tol, const mstrsm_dcomplex *v0, double *sigma,
+                      int32_t *flags, int32_t *its, int nb) {
+    return spectral_window_impl((const cplx *)U, ldu, m, x0, x1, nx, y0, y1, ny, maxit, tol, (const cplx *)v0, sigma,
+                                flags, its, nb);
+}
+int spectral_portrait_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, int64_t nx, int64_t ny, int maxit,
+                        double tol, const mstrsm_dcomplex *v0, double *sigma, int32_t *flags, int32_t *its,
+                        double *window_host, int nb) {
+    if (m < 0) return -3;
+    if (ldu < std::max<int64_t>(1, m)) return -2;
+    if (nx < 0) return -4;
+    if (ny < 0) return -5;
+    if (m == 0 || nx == 0 || ny == 0) return 0;
+    if (!U) return -1;
+    if (int rc = ensure_init()) return rc;
+    double win[4];
+    if (int rc = portrait_window((const cplx *)U, ldu, m, win)) return rc;
+    if (window_host) for (int i = 0; i < 4; i++) window_host[i] = win[i];
+    int rc = spectral_window_impl((const cplx *)U, ldu, m, win[0], win[1], nx, win[2], win[3], ny, maxit, tol,
+                                  (const cplx *)v0, sigma, flags, its, nb);
+    if (rc < 0) {                                 // positions of spectral_portrait_z
+        const int map[17] = {0, -1, -2, -3, 1, 1, -4, 1, 1, -5, -6, -7, -8, -9, -10, -11, -13};
+        rc = -rc < 17 ? map[-rc] : rc;
+    }
+    return rc;
 }
 
 int eig_backtransform_d(const double *Q, int64_t ldq, int64_t m, const double *Z, int64_t ldz, int64_t n,

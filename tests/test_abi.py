@@ -71,6 +71,12 @@ def test_invalid_arguments_are_rejected_without_cuda():
     assert lib.trevc_z(P, 3, 3, P, 3, P, P, 200) == -8
     # pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma, flags, nb)
     assert lib.pseudospectra_z(P, 4, 4, P, 1, 0, P, P, P, 0) == -6
+    # spectral_cloud_z(U, ldu, m, z, npts, maxit, tol, v0, sigma, flags, its, nb)
+    assert lib.spectral_cloud_z(P, 4, 4, P, 1, 15, ctypes.c_double(-1.0), P, P, P, P, 0) == -7
+    assert lib.spectral_cloud_z(P, 4, 4, P, 1, 0, ctypes.c_double(0.0), P, P, P, P, 0) == -6
+    assert lib.spectral_window_z(P, 4, 4, ctypes.c_double(0), ctypes.c_double(1), -1, ctypes.c_double(0),
+                                 ctypes.c_double(1), 2, 15, ctypes.c_double(0), P, P, P, P, 0) == -6
+    assert lib.spectral_portrait_z(P, 3, 4, 2, 2, 15, ctypes.c_double(0), P, P, P, P, P, 0) == -2
     # eig_backtransform_z(Q, ldq, m, Z, ldz, n, cols, X, ldx)
     assert lib.eig_backtransform_z(P, 3, 4, P, 4, 4, P, P, 4) == -2
     assert lib.eig_backtransform_z(P, 4, 4, P, 4, 5, P, P, 4) == -6      # n > m without row bounds
