@@ -147,6 +147,33 @@ def mstrsm(U, shifts, B, *, op: str = "N", safe: bool = True, nb: int = 64, row_
     return X, e
 
 
+def mstrsm_side(A, shifts, B, *, side: str = "L", uplo: str = "U", safe: bool = True, nb: int = 64,
+                nthreads: int = 0):
+    """The footnote family of P:58-62, each case written as the triangular system
+    it is, then solved by the (pinned) op N / op C oracle:
+
+      L,U: (A - s I) x = c b                       -> mstrsm(A, s, B, op N)
+      L,L: (A - s I) x = c b,  A lower              =  (A^H - conj(s) I)^H x = c b   -> op C on A^H
+      R,U: x^T (A - s I) = c b^T                    =  (A^T - s I) x = c b = (conj(A) - conj(s) I)^H x
+      R,L: x^T (A - s I) = c b^T,  A lower          =  (A^T - s I) x = c b, A^T upper -> op N on A^T
+
+    Right cases: B is n x m (row j = b_j^T) and so is the returned X.  Returns (X, e)."""
+    A = np.asarray(A)
+    s = np.asarray(shifts).reshape(-1)
+    B = np.asarray(B)
+    cx = np.iscomplexobj(A) or np.iscomplexobj(s) or np.iscomplexobj(B)
+    cj = (lambda v: np.conj(v)) if cx else (lambda v: v)
+    if side == "L" and uplo == "U":
+        return mstrsm(A, s, B, op="N", safe=safe, nb=nb, nthreads=nthreads)
+    if side == "L":
+        return mstrsm(np.triu(cj(A.T)), cj(s), B, op="C", safe=safe, nb=nb, nthreads=nthreads)
+    if uplo == "U":
+        X, e = mstrsm(np.triu(cj(A)), cj(s), B.T, op="C", safe=safe, nb=nb, nthreads=nthreads)
+    else:
+        X, e = mstrsm(np.triu(A.T), s, B.T, op="N", safe=safe, nb=nb, nthreads=nthreads)
+    return np.asfortranarray(X.T), e
+
+
 def norms(U, *, op: str = "N", nb: int = 64):
     """The norm pass: block-local column norms cnl, panel sums P, ||U||_inf (op N) or
     ||U^H||_inf (op C)."""
