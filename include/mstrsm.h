@@ -96,6 +96,25 @@ int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, i
                 int nb);
 
 /* ------------------------------------------------------------------------------------
+ * The footnote family of P:58-62: left/right, upper/lower.
+ *   side = LEFT : (A - s_j I) x_j = c_j b_j          B is m x n (ldb >= max(1,m)), column j = b_j
+ *   side = RIGHT: x_j^T (A - s_j I) = c_j b_j^T      B is n x m (ldb >= max(1,n)), row j = b_j^T
+ *   uplo = UPPER: A upper triangular (strictly lower part never read);
+ *   uplo = LOWER: A lower triangular (strictly upper part never read); lower = forward substitution.
+ * No conjugation on either side (X op(A) with op = identity).  Left-upper is mstrsm_*_ex op N;
+ * the others run the op N / op C kernels on a transformed copy of the triangle (A^H, A^T or
+ * conj A, library workspace) and, for RIGHT, on B^T.  Other arguments as
+ * mstrsm_*_ex (no row_end).  Errors: -i for argument i, 1 CUDA error.                     */
+typedef enum { MSTRSM_LEFT = 0, MSTRSM_RIGHT = 1 } mstrsm_side;
+typedef enum { MSTRSM_UPPER = 0, MSTRSM_LOWER = 1 } mstrsm_uplo;
+int mstrsm_d_side(int safe, mstrsm_side side, mstrsm_uplo uplo, const double *A, int64_t lda, int64_t m,
+                  const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
+                  double *scales, int32_t *scale_exp, int nb);
+int mstrsm_z_side(int safe, mstrsm_side side, mstrsm_uplo uplo, const mstrsm_dcomplex *A, int64_t lda,
+                  int64_t m, const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
+                  int64_t ldb, int64_t n, double *scales, int32_t *scale_exp, int nb);
+
+/* ------------------------------------------------------------------------------------
  * Triangular eigenvectors, Alg. 6 TriangEig: lambda = diag(T); Z := -T with
  * diag(Z) := 0; safe multi-shift solve with shifts lambda, shortcut to the strictly upper
  * RHS (R11); diag(Z) := s.  T Z = Z diag(lambda) backward-stably.

@@ -26,7 +26,7 @@ __all__ = [
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
-    "spectral_portrait",
+    "spectral_portrait", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
@@ -60,6 +60,8 @@ def load():
         "trevc_z_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
+        "mstrsm_d_side": [c_int, c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int],
+        "mstrsm_z_side": [c_int, c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int],
         "spectral_cloud_z": [P, c_i64, c_i64, P, c_i64, c_int, c_dbl, P, P, P, P, c_int],
         "spectral_window_z": [P, c_i64, c_i64, c_dbl, c_dbl, c_i64, c_dbl, c_dbl, c_i64, c_int, c_dbl, P, P, P, P,
                               c_int],
@@ -218,6 +220,33 @@ def tgevc_z(T, ldt, S, lds, m, Z, ldz, lam, scales, scale_exp, nb):
 def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
     _call("pseudospectra_z", _ptr(U), ldu, m, _ptr(z), npts, iters, _ptr(v0), _ptr(sigma_min),
           _ptr(flags), nb)
+
+
+def mstrsm_d_side(safe, side, uplo, A, lda, m, shifts, shift_stride, B, ldb, n, scales, scale_exp, nb):
+    _call("mstrsm_d_side", safe, side, uplo, _ptr(A), lda, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n,
+          _ptr(scales), _ptr(scale_exp), nb)
+
+
+def mstrsm_z_side(safe, side, uplo, A, lda, m, shifts, shift_stride, B, ldb, n, scales, scale_exp, nb):
+    _call("mstrsm_z_side", safe, side, uplo, _ptr(A), lda, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n,
+          _ptr(scales), _ptr(scale_exp), nb)
+
+
+def solve_side(A, shifts, B, *, side: str = "L", uplo: str = "U", safe: bool = True, nb: int = 64,
+               shift_stride: int = 1):
+    """In-place multi-shift solve of the P:58-62 family on column-major CUDA tensors: side "L":
+    (A - s_j I) x_j = c_j b_j (B m x n); side "R": x_j^T (A - s_j I) = c_j b_j^T (B n x m, row j);
+    uplo "U" / "L".  Returns (B, scales, scale_exp)."""
+    torch = _torch()
+    m = A.shape[0]
+    n = B.shape[1] if side == "L" else B.shape[0]
+    cplx = B.dtype == torch.complex128
+    scales = torch.empty(n, dtype=torch.float64, device=B.device)
+    exps = torch.empty(n, dtype=torch.int32, device=B.device)
+    f = mstrsm_z_side if cplx else mstrsm_d_side
+    f(1 if safe else 0, 0 if side == "L" else 1, 0 if uplo == "U" else 1, A, _ld(A), m, shifts, shift_stride, B,
+      _ld(B), n, scales, exps, nb)
+    return B, scales, exps
 
 
 def spectral_cloud_z(U, ldu, m, z, npts, maxit, tol, v0, sigma, flags, its, nb):

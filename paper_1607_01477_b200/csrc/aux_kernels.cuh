@@ -254,6 +254,59 @@ __global__ void init_tgevc_kernel(const T *__restrict__ Tm, int64_t ldt, const T
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Side / triangle variants (SURVEY §8f f4, P:58-62 footnote): operand transforms in 32 x 32
+// shared-memory tiles (coalesced both ways).
+//   tri_upper_kernel: U(i,k), i <= k, from A:  mode 0: conj(A(k,i)) (lower -> A^H),
+//                     mode 1: A(k,i) (lower -> A^T),  mode 2: conj(A(i,k)) (upper -> conj A).
+//   The other triangle of A is never read.
+template <typename T>
+__global__ void tri_upper_kernel(const T *__restrict__ A, int64_t lda, int64_t m, T *__restrict__ U,
+                                 int64_t ldu, int mode) {
+    __shared__ T tile[32][33];
+    const int64_t ti = int64_t(blockIdx.y) * 32, tk = int64_t(blockIdx.x) * 32;   // U tile rows ti.., cols tk..
+    if (ti > tk) return;                                                          // below the diagonal
+    const int tx = threadIdx.x, ty = threadIdx.y;                                 // 32 x 8 threads
+    for (int r = ty; r < 32; r += 8) {
+        if (mode == 2) {                      // no transpose: U(ti + tx, tk + r) = conj A(ti + tx, tk + r)
+            const int64_t i = ti + tx, k = tk + r;
+            if (i < m && k < m && i <= k) U[i + k * ldu] = S<T>::conj(A[i + k * lda]);
+        } else {                              // load A(tk + tx, ti + r) (lower: row >= col)
+            const int64_t ar = tk + tx, ac = ti + r;
+            if (ar < m && ac < m && ar >= ac) tile[r][tx] = A[ar + ac * lda];
+        }
+    }
+    if (mode == 2) return;
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {        // U(ti + tx, tk + r) = f(A(tk + r, ti + tx)) = f(tile[tx][r])
+        const int64_t i = ti + tx, k = tk + r;
+        if (i < m && k < m && i <= k) {
+            const T v = tile[tx][r];
+            U[i + k * ldu] = mode == 0 ? S<T>::conj(v) : v;
+        }
+    }
+}
+
+// dst(c, r) = src(r, c) for r < rows, c < cols (column-major, 32 x 32 tiles)
+template <typename T>
+__global__ void transpose_kernel(const T *__restrict__ src, int64_t lds, int64_t rows, int64_t cols,
+                                 T *__restrict__ dst, int64_t ldd) {
+    __shared__ T tile[32][33];
+    const int64_t r0 = int64_t(blockIdx.x) * 32, c0 = int64_t(blockIdx.y) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int c = ty; c < 32; c += 8)
+        if (r0 + tx < rows && c0 + c < cols) tile[c][tx] = src[(r0 + tx) + (c0 + c) * lds];
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8)
+        if (c0 + tx < cols && r0 + r < rows) dst[(c0 + tx) + (r0 + r) * ldd] = tile[tx][r];
+}
+
+template <typename T>
+__global__ void conj_strided_kernel(const T *__restrict__ s, int64_t stride, int64_t n, T *__restrict__ d) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) d[j] = S<T>::conj(s[j * stride]);
+}
+
 // X := -X on an m x n column-major array (the back-transformation's sign, mstrsm.cu)
 template <typename T>
 __global__ void negate_kernel(T *__restrict__ X, int64_t ldx, int64_t m, int64_t n) {

@@ -303,6 +303,87 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
     return rc;
 }
 
+// ---------------------------------------------------------------- side / triangle variants (f4)
+// The footnote family of P:58-62 on top of the two kernels the path has (op N: back substitution
+// on U; op C: forward substitution on U^H = lower):
+//   left  lower  (A - sI) x = c b            ==  op C on U = A^H,      shifts conj(s)
+//   right upper  x^T (A - sI) = c b^T        ==  op C on U = conj(A),  shifts conj(s), on B^T
+//   right lower  x^T (A - sI) = c b^T        ==  op N on U = A^T,      shifts s,       on B^T
+// (right: row j of the n x m array B is b_j^T).  The operand transforms are one tiled pass over
+// the triangle (and two over B for the right cases) into workspace; the solves are the hot path.
+template <typename T>
+int side_impl(int safe, int side, int uplo, const T *A, int64_t lda, int64_t m, const T *shifts, int64_t sstride,
+              T *B, int64_t ldb, int64_t n, double *scales, int32_t *scale_exp, int nb) {
+    if (safe != 0 && safe != 1) return -1;
+    if (side != 0 && side != 1) return -2;
+    if (uplo != 0 && uplo != 1) return -3;
+    if (m < 0) return -6;
+    if (lda < std::max<int64_t>(1, m)) return -5;
+    if (sstride < 0) return -8;
+    if (n < 0) return -11;
+    if (ldb < std::max<int64_t>(1, side == 0 ? m : n)) return -10;
+    if (nb != 0 && (nb < 1 || nb > 128)) return -14;
+    if (m == 0 || n == 0) return 0;
+    if (!A) return -4;
+    if (!shifts) return -7;
+    if (!B) return -9;
+    if (safe && !scales) return -12;
+    if (side == 0 && uplo == 0)
+        return mstrsm_ex_impl<T>(safe, 0, A, lda, m, shifts, sstride, B, ldb, n, nullptr, scales, scale_exp, nb);
+    if (int rc = ensure_init()) return rc;
+    const bool cplx_t = S<T>::cplx_;
+    // transformed triangle (real right-upper needs none: conj(A) = A)
+    const bool need_u = !(side == 1 && uplo == 0 && !cplx_t);
+    const int mode = (side == 0) ? 0 : (uplo == 0 ? 2 : 1);
+    const int op = (side == 1 && uplo == 1) ? 0 : 1;
+    const bool conj_s = op == 1 && cplx_t;
+    T *Uw = nullptr, *sw = nullptr, *Bt = nullptr;
+    auto cleanup = [&]() {
+        if (Uw) cudaFreeAsync(Uw, g_stream);
+        if (sw) cudaFreeAsync(sw, g_stream);
+        if (Bt) cudaFreeAsync(Bt, g_stream);
+    };
+    const T *Uuse = A;
+    int64_t lduse = lda;
+    if (need_u) {
+        CK(cudaMallocAsync(&Uw, size_t(m) * m * sizeof(T), g_stream));
+        const dim3 g(unsigned(cdiv(m, 32)), unsigned(cdiv(m, 32)));
+        tri_upper_kernel<T><<<g, dim3(32, 8), 0, g_stream>>>(A, lda, m, Uw, m, mode);
+        CK_LAUNCH("tri_upper_kernel");
+        Uuse = Uw;
+        lduse = m;
+    }
+    const T *suse = shifts;
+    int64_t sst = sstride;
+    if (conj_s) {
+        CK(cudaMallocAsync(&sw, size_t(n) * sizeof(T), g_stream));
+        conj_strided_kernel<T><<<int(cdiv(n, 256)), 256, 0, g_stream>>>(shifts, sstride, n, sw);
+        CK_LAUNCH("conj_strided_kernel");
+        suse = sw;
+        sst = 1;
+    }
+    T *Buse = B;
+    int64_t ldbuse = ldb;
+    if (side == 1) {                    // B is n x m: solve on B^T (m x n)
+        CK(cudaMallocAsync(&Bt, size_t(m) * n * sizeof(T), g_stream));
+        transpose_kernel<T><<<dim3(unsigned(cdiv(n, 32)), unsigned(cdiv(m, 32))), dim3(32, 8), 0, g_stream>>>(
+            B, ldb, n, m, Bt, m);
+        CK_LAUNCH("transpose_kernel");
+        Buse = Bt;
+        ldbuse = m;
+    }
+    int rc = mstrsm_ex_impl<T>(safe, op, Uuse, lduse, m, suse, sst, Buse, ldbuse, n, nullptr, scales, scale_exp, nb);
+    if (rc < 0) rc = 1;                 // arguments were validated above
+    if (!rc && side == 1) {
+        transpose_kernel<T><<<dim3(unsigned(cdiv(m, 32)), unsigned(cdiv(n, 32))), dim3(32, 8), 0, g_stream>>>(
+            Bt, m, m, n, B, ldb);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = set_cuda_error(e, "transpose_kernel");
+    }
+    cleanup();
+    return rc;
+}
+
 // ---------------------------------------------------------------- back-transformation (f2)
 // X := Q Z.  The update GEMM computes C <- C - A X, so X is zeroed, receives -Q Z
 // panel by panel and is negated once.  Panel p (columns [p0, p1)) only needs rows 0..cols[p1-1]
@@ -815,6 +896,19 @@ int spectral_portrait_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, int64_
         rc = -rc < 17 ? map[-rc] : rc;
     }
     return rc;
+}
+
+int mstrsm_d_side(int safe, mstrsm_side side, mstrsm_uplo uplo, const double *A, int64_t lda, int64_t m,
+                  const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n, double *scales,
+                  int32_t *scale_exp, int nb) {
+    return side_impl<double>(safe, int(side), int(uplo), A, lda, m, shifts, shift_stride, B, ldb, n, scales,
+                             scale_exp, nb);
+}
+int mstrsm_z_side(int safe, mstrsm_side side, mstrsm_uplo uplo, const mstrsm_dcomplex *A, int64_t lda, int64_t m,
+                  const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n,
+                  double *scales, int32_t *scale_exp, int nb) {
+    return side_impl<cplx>(safe, int(side), int(uplo), (const cplx *)A, lda, m, (const cplx *)shifts, shift_stride,
+                           (cplx *)B, ldb, n, scales, scale_exp, nb);
 }
 
 int eig_backtransform_d(const double *Q, int64_t ldq, int64_t m, const double *Z, int64_t ldz, int64_t n,

@@ -71,6 +71,12 @@ def test_invalid_arguments_are_rejected_without_cuda():
     assert lib.trevc_z(P, 3, 3, P, 3, P, P, 200) == -8
     # pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma, flags, nb)
     assert lib.pseudospectra_z(P, 4, 4, P, 1, 0, P, P, P, 0) == -6
+    # mstrsm_z_side(safe, side, uplo, A, lda, m, shifts, stride, B, ldb, n, scales, exp, nb)  (§8f f4)
+    assert lib.mstrsm_z_side(0, 2, 0, P, 4, 4, P, 1, P, 4, 1, P, P, 0) == -2
+    assert lib.mstrsm_z_side(0, 1, 0, P, 4, 4, P, 1, P, 1, 3, P, P, 0) == -10     # right: ldb >= n
+    assert lib.mstrsm_d_side(0, 0, 1, P, 3, 4, P, 1, P, 4, 1, P, P, 0) == -5
+    assert lib.mstrsm_d_side(1, 0, 1, ctypes.c_void_p(8), 4, 4, ctypes.c_void_p(8), 1, ctypes.c_void_p(8), 4, 1,
+                             P, P, 0) == -12                                      # safe needs scales
     # spectral_cloud_z(U, ldu, m, z, npts, maxit, tol, v0, sigma, flags, its, nb)
     assert lib.spectral_cloud_z(P, 4, 4, P, 1, 15, ctypes.c_double(-1.0), P, P, P, P, 0) == -7
     assert lib.spectral_cloud_z(P, 4, 4, P, 1, 0, ctypes.c_double(0.0), P, P, P, P, 0) == -6

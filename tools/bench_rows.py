@@ -28,7 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--only", default="c1,c2,c3,c4,c4d,g1,f2")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c4d,g1,f2,f4")
     a = ap.parse_args()
     import torch
     import paper_1607_01477_b200 as ms
@@ -63,6 +63,25 @@ def main():
                        15 * 2 * 4.0 * 1024 ** 2 * z.shape[0], z.shape[0], "points/s",
                        "c4d: c4 with SpectralCloud deflation (tol 1e-10, at most 15 steps; SURVEY §8f f3); "
                        "gflops counts the fixed 15-step work, so it is an effective rate")
+    if "f4" in a.only:
+        m4 = 4096
+        rng = np.random.default_rng(44)
+        A4 = np.tril(rng.standard_normal((m4, m4)) + 1j * rng.standard_normal((m4, m4))) / np.sqrt(m4)
+        A4[np.arange(m4), np.arange(m4)] = rng.uniform(1.0, 2.0, m4)
+        A4d = dev(A4)
+        s4 = dev(inputs.random_shifts(m4, True, 45, radius=0.5))
+        B40 = dev(np.asfortranarray(inputs.random_rhs(m4, m4, True, 46).T))
+        B4 = B40.clone()
+        work["f4"] = (lambda: (B4.copy_(B40), ms.solve_side(A4d, s4, B4, side="R", uplo="L", safe=True, nb=128)),
+                      4.0 * m4 * m4 * m4, m4, "shifts/s",
+                      "f4: right-side lower-triangular safe solve x^T (L - s I) = c b^T, complex m=n=4096, n_b=128 "
+                      "(transforms + op N solve; SURVEY §8f f4)")
+        U4u = dev(np.asfortranarray(A4.T))
+        B4u0 = dev(inputs.random_rhs(m4, m4, True, 46))
+        B4u = B4u0.clone()
+        work["f4_ref"] = (lambda: (B4u.copy_(B4u0), ms.solve(U4u, s4, B4u, safe=True, nb=128)),
+                          4.0 * m4 * m4 * m4, m4, "shifts/s",
+                          "f4_ref: the same system as a left-upper solve on L^T (no transforms), complex m=n=4096")
     if "g1" in a.only:
         Tg, Sg = inputs.g1_pencil(m=4096)
         Tgd, Sgd = dev(Tg), dev(Sg)
