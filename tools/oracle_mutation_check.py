@@ -17,6 +17,8 @@ MAIN = "oracle/mstrsm_oracle.c"
 SCAL = "oracle/oracle_scalar.h"
 GEN = "oracle/oracle_gen.inc"
 PINS, GPINS = "tests/test_oracle_pins.py", "tests/test_oracle_gen.py"
+INIT = "oracle/__init__.py"
+SPINS, BPINS, SIDEPINS = "tests/test_oracle_spectral.py", "tests/test_oracle_backtransform.py", "tests/test_oracle_side.py"
 
 MUTANTS = [
     ("growth bound uses cnl*|d| (eq. 5)", ALGO, "g = g * (1.0 + cnl[l] / ad);", "g = g * (1.0 + cnl[l] * ad);"),
@@ -67,6 +69,21 @@ MUTANTS = [
     ("gen: Z RHS ignores S diag(lambda) (P:987)", GEN,
      "Z[q * ldz + i] = i < k ? SUB(MUL(Sm[k * lds + i], lam[q]), T[k * ldt + i]) : ZERO();",
      "Z[q * ldz + i] = i < k ? NEG(T[k * ldt + i]) : ZERO();", GPINS),
+    # SURVEY §8f f2-f4 (Python / C oracle parts), each against its own pin file
+    ("cloud: absolute instead of relative settle test (R33)", MAIN, "fabs(theta - theta_prev) <= J->tol * theta",
+     "fabs(theta - theta_prev) <= J->tol", SPINS),
+    ("cloud: previous Ritz value never updated (R33)", MAIN, "                theta_prev = theta;\n", "", SPINS),
+    ("portrait: pad 0.5 instead of 0.25 (R34)", INIT, "pad = 0.25 * max(", "pad = 0.5 * max(", SPINS),
+    ("window: grid index iy + ny ix (R15)", INIT, "return (gx[None, :] + 1j * gy[:, None]).reshape(-1)",
+     "return (gx[:, None] + 1j * gy[None, :]).reshape(-1)", SPINS),
+    ("backtransform: Q^T Z (P:540)", INIT, "return np.asfortranarray(np.asarray(Q) @ np.asarray(Z))",
+     "return np.asfortranarray(np.asarray(Q).T @ np.asarray(Z))", BPINS),
+    ("side L,L: shifts not conjugated", INIT, 'return mstrsm(np.triu(cj(A.T)), cj(s), B, op="C"',
+     'return mstrsm(np.triu(cj(A.T)), s, B, op="C"', SIDEPINS),
+    ("side R,U: A not conjugated", INIT, 'X, e = mstrsm(np.triu(cj(A)), cj(s), B.T, op="C"',
+     'X, e = mstrsm(np.triu(A), cj(s), B.T, op="C"', SIDEPINS),
+    ("side R,L: A instead of A^T", INIT, 'X, e = mstrsm(np.triu(A.T), s, B.T, op="N"',
+     'X, e = mstrsm(np.triu(A), s, B.T, op="N"', SIDEPINS),
 ]
 
 
