@@ -145,6 +145,16 @@ int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t
 int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *Z_host,
                  int64_t ldz, double *scales_host, int32_t *scale_exp_host, int nb);
 
+/* Batched host entry: count independent TriangEig problems, HOST pointer arrays (each entry a
+ * HOST buffer, pinned for the copies to overlap).  Problem k+1's upload of T (upper triangle) and
+ * problem k-1's download of Z / scales / scale_exp run on two copy streams while problem k is
+ * solved, with two device buffer sets in flight.  scales_host / scale_exp_host: nullable arrays
+ * (or nullable entries).  Blocking.  Errors: -i for argument i (-9 also for a failed solve's
+ * argument check), 1 CUDA error.                                                          */
+int trevc_z_host_batch(const mstrsm_dcomplex *const *T_host, int64_t ldt, int64_t m,
+                       mstrsm_dcomplex *const *Z_host, int64_t ldz, double *const *scales_host,
+                       int32_t *const *scale_exp_host, int64_t count, int nb);
+
 /* ------------------------------------------------------------------------------------
  * Pseudospectra, Van Loan / Lui with multi-shift batching: for
  * every point z_p, sigma_min(U - z_p I) = 1/sqrt(lambda_max((U - zI)^{-H}(U - zI)^{-1}))

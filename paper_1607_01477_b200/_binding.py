@@ -23,7 +23,7 @@ c_i64, c_int, c_dbl, c_vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctype
 __all__ = [
     "load", "LIB_PATH", "MstrsmError",
     "mstrsm_d", "mstrsm_z", "mstrsm_d_safe", "mstrsm_z_safe", "mstrsm_d_ex", "mstrsm_z_ex",
-    "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
+    "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "trevc_z_host_batch", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
     "spectral_portrait", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
@@ -59,6 +59,7 @@ def load():
         "trevc_d_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_cols": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
+        "trevc_z_host_batch": [P, c_i64, c_i64, P, c_i64, P, P, c_i64, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
         "mstrsm_d_side": [c_int, c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int],
         "mstrsm_z_side": [c_int, c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int],
@@ -195,6 +196,19 @@ def trevc_z_host(T_host: np.ndarray, m: int, Z_host: np.ndarray, scales_host=Non
     ptr = lambda a: a.ctypes.data_as(c_vp) if a is not None else None
     _check(lib.trevc_z_host(ptr(T_host), T_host.shape[0], m, ptr(Z_host), Z_host.shape[0],
                             ptr(scales_host), ptr(exp_host), nb), "trevc_z_host")
+
+
+def trevc_z_host_batch(T_hosts, m: int, Z_hosts, scales_hosts=None, exp_hosts=None, nb=0):
+    """Batched host-buffer entry (lists of numpy complex128 Fortran arrays, blocking): problem
+    k's solve overlaps k+1's upload and k-1's download."""
+    lib = load()
+    _bind_stream(lib)
+    n = len(T_hosts)
+    assert len(Z_hosts) == n
+    arr = lambda lst: (c_vp * n)(*[a.ctypes.data if a is not None else None for a in lst]) if lst is not None else None
+    _check(lib.trevc_z_host_batch(arr(T_hosts), T_hosts[0].shape[0] if n else 1, m, arr(Z_hosts),
+                                  Z_hosts[0].shape[0] if n else 1, arr(scales_hosts), arr(exp_hosts), n, nb),
+           "trevc_z_host_batch")
 
 
 def mstrsm_d_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):

@@ -967,6 +967,93 @@ int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_d
     return rc;
 }
 
+// Batched host entry: problem k+1's H2D (copy stream 1) and problem k-1's D2H (copy stream 2)
+// overlap problem k's solve (library stream), with two device buffer sets in flight.
+int trevc_z_host_batch(const mstrsm_dcomplex *const *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *const *Z_host,
+                       int64_t ldz, double *const *scales_host, int32_t *const *scale_exp_host, int64_t count,
+                       int nb) {
+    if (m < 0) return -3;
+    if (ldt < std::max<int64_t>(1, m)) return -2;
+    if (ldz < std::max<int64_t>(1, m)) return -5;
+    if (count < 0) return -8;
+    if (nb != 0 && (nb < 1 || nb > 128)) return -9;
+    if (m == 0 || count == 0) return 0;
+    if (!T_host) return -1;
+    if (!Z_host) return -4;
+    for (int64_t k = 0; k < count; k++) {
+        if (!T_host[k]) return -1;
+        if (!Z_host[k]) return -4;
+    }
+    if (int rc = ensure_init()) return rc;
+    static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    if (!s_h2d) {
+        CK(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
+    }
+    const cudaStream_t cs = g_stream;
+    const size_t bytes = size_t(m) * m * sizeof(cplx);
+    cplx *dT[2] = {nullptr, nullptr}, *dZ[2] = {nullptr, nullptr};
+    double *ds[2] = {nullptr, nullptr};
+    int *de[2] = {nullptr, nullptr};
+    cudaEvent_t e_alloc, e_h2d[2], e_comp[2], e_d2h[2];
+    CK(cudaEventCreateWithFlags(&e_alloc, cudaEventDisableTiming));
+    for (int s = 0; s < 2; s++) {
+        CK(cudaEventCreateWithFlags(&e_h2d[s], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e_comp[s], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e_d2h[s], cudaEventDisableTiming));
+        if (s < count) {
+            CK(cudaMallocAsync(&dT[s], bytes, cs));
+            CK(cudaMallocAsync(&dZ[s], bytes, cs));
+            CK(cudaMallocAsync(&ds[s], m * 8, cs));
+            CK(cudaMallocAsync(&de[s], m * 4, cs));
+        }
+    }
+    CK(cudaEventRecord(e_alloc, cs));
+    CK(cudaStreamWaitEvent(s_h2d, e_alloc, 0));
+    CK(cudaStreamWaitEvent(s_d2h, e_alloc, 0));
+    int rc = 0;
+    for (int64_t k = 0; k < count && !rc; k++) {
+        const int s = int(k & 1);
+        if (k >= 2) CK(cudaStreamWaitEvent(s_h2d, e_comp[s], 0));   // dT[s] released by solve k-2
+        for (int64_t c0 = 0; c0 < m; c0 += 128) {                     // upper triangle, 128-column panels
+            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+            CK(cudaMemcpy2DAsync(dT[s] + c0 * m, m * sizeof(cplx), (const cplx *)T_host[k] + c0 * ldt,
+                                 ldt * sizeof(cplx), size_t(c1) * sizeof(cplx), size_t(c1 - c0),
+                                 cudaMemcpyHostToDevice, s_h2d));
+        }
+        CK(cudaEventRecord(e_h2d[s], s_h2d));
+        CK(cudaStreamWaitEvent(cs, e_h2d[s], 0));
+        if (k >= 2) CK(cudaStreamWaitEvent(cs, e_d2h[s], 0));         // dZ[s] read out by D2H k-2
+        rc = trevc_impl<cplx>(dT[s], m, m, nullptr, m, dZ[s], m, ds[s], de[s], nb);
+        if (rc < 0) rc = -9;
+        if (rc) break;
+        CK(cudaEventRecord(e_comp[s], cs));
+        CK(cudaStreamWaitEvent(s_d2h, e_comp[s], 0));
+        if (ldz == m) CK(cudaMemcpyAsync(Z_host[k], dZ[s], bytes, cudaMemcpyDeviceToHost, s_d2h));
+        else CK(cudaMemcpy2DAsync(Z_host[k], ldz * sizeof(cplx), dZ[s], m * sizeof(cplx), m * sizeof(cplx), m,
+                                  cudaMemcpyDeviceToHost, s_d2h));
+        if (scales_host && scales_host[k])
+            CK(cudaMemcpyAsync(scales_host[k], ds[s], m * 8, cudaMemcpyDeviceToHost, s_d2h));
+        if (scale_exp_host && scale_exp_host[k])
+            CK(cudaMemcpyAsync(scale_exp_host[k], de[s], m * 4, cudaMemcpyDeviceToHost, s_d2h));
+        CK(cudaEventRecord(e_d2h[s], s_d2h));
+    }
+    CK(cudaStreamSynchronize(s_h2d));
+    CK(cudaStreamSynchronize(s_d2h));
+    for (int s = 0; s < 2; s++) {
+        if (dT[s]) cudaFreeAsync(dT[s], cs);
+        if (dZ[s]) cudaFreeAsync(dZ[s], cs);
+        if (ds[s]) cudaFreeAsync(ds[s], cs);
+        if (de[s]) cudaFreeAsync(de[s], cs);
+        cudaEventDestroy(e_h2d[s]);
+        cudaEventDestroy(e_comp[s]);
+        cudaEventDestroy(e_d2h[s]);
+    }
+    cudaEventDestroy(e_alloc);
+    CK(cudaStreamSynchronize(cs));
+    return rc;
+}
+
 int mstrsm_d_gen(int safe, const double *U, int64_t ldu, const double *V, int64_t ldv, int64_t m,
                  const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
                  const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb) {
