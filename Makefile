@@ -18,7 +18,7 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 $(PKG)/libmstrsm.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
-oracle/liboracle.so: oracle/mstrsm_oracle.c oracle/oracle_algo.inc oracle/oracle_scalar.h
+oracle/liboracle.so: oracle/mstrsm_oracle.c oracle/oracle_algo.inc oracle/oracle_gen.inc oracle/oracle_scalar.h
 	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread -o $@ oracle/mstrsm_oracle.c -lm
 
 clean:

@@ -38,7 +38,7 @@ c_vp = ctypes.c_void_p
 def build(force: bool = False) -> str:
     """Compile liboracle.so (plain C, no FMA contraction, no fast-math)."""
     src = [os.path.join(_HERE, "mstrsm_oracle.c")]
-    deps = src + [os.path.join(_HERE, f) for f in ("oracle_algo.inc", "oracle_scalar.h")]
+    deps = src + [os.path.join(_HERE, f) for f in ("oracle_algo.inc", "oracle_gen.inc", "oracle_scalar.h")]
     if not force and os.path.exists(_LIB_PATH):
         lib_m = os.path.getmtime(_LIB_PATH)
         if all(os.path.getmtime(d) <= lib_m for d in deps):

@@ -178,7 +178,7 @@ static void *ps_worker(void *arg)
         ozc z = J->z[p];
         for (int64_t i = 0; i < m; i++) { v[i] = J->v0[i]; vp[i] = z_zero(); }
         double beta_prev = 0.0, amax = 0.0, sigma = 0.0, theta_prev = 0.0;
-        int k = 0, flag = 0, conv = 0;
+        int k = 0, flag = 0, conv = 0, brk = 0;
         for (int it = 0; it < J->iters; it++) {
             for (int64_t i = 0; i < m; i++) y[i] = v[i];
             int e1 = col_N_z(J->U, J->ldu, m, z, y, m, 1, J->nb, J->cnlN, J->PN, J->deltaN);
@@ -204,7 +204,7 @@ static void *ps_worker(void *arg)
             double b = sqrt(bsq);
             al[k] = a; be[k] = b; k++;
             if (a > amax) amax = a;
-            if (b <= (double)m * 0x1p-52 * amax) break;     /* Krylov space exhausted */
+            if (b <= (double)m * 0x1p-52 * amax) { brk = 1; break; }   /* Krylov space exhausted */
             if (J->tol > 0.0) {       /* R33: the point leaves the batch when its estimate settles */
                 double theta = oracle_tridiag_lmax(al, be, k);
                 if (k >= 2 && fabs(theta - theta_prev) <= J->tol * theta) { conv = 1; break; }
@@ -223,7 +223,7 @@ static void *ps_worker(void *arg)
         }
         J->sigma[p] = sigma;
         /* bit1: tol > 0 and neither converged nor exhausted within iters steps */
-        if (J->tol > 0.0 && !flag && !conv && k == J->iters) flag |= 2;
+        if (J->tol > 0.0 && !flag && !conv && !brk) flag |= 2;
         if (J->flags) J->flags[p] = flag;
         if (J->its) J->its[p] = k;
     }
