@@ -76,24 +76,36 @@ int launch_gemm(const GemmArgs<T> &g) {
         return 0;
     }
     if constexpr (S<T>::cplx_) {
-        if (gemm_variant() == 0 && !OPC && g.As && g.Xsum && g.a_r0 % 2 == 0 && g.ldas % 2 == 0 &&
-            g.ldxs % 2 == 0) {                   // sums precomputed: bulk-copy producer, LDS + DMMA
-            // X: rows x_r0.. (as 2K doubles) x columns col0.., X+: K x N doubles
-            CUtensorMap tmX, tmXs;
+        if (gemm_variant() == 0 && g.As && g.Xsum && g.a_r0 % 2 == 0 && g.ldas % 2 == 0 &&
+            g.ldxs % 2 == 0) {                   // sums precomputed: copy-engine producer, LDS + DMMA
+            // X: rows x_r0.. (as 2K doubles) x columns col0.., X+: K x N doubles; op C: A = rows a_r0..
+            // (2K doubles) x columns a_c0.. (M) of U, A+ likewise in the plane
+            CUtensorMap tmX, tmXs, tmA, tmAs;
             if (!encode_2d(&tmX, g.X + g.x_r0 + g.col0 * g.ldx, uint64_t(2 * g.K), uint64_t(g.N), uint64_t(2 * g.ldx),
                            2 * k3mBK, k3mBN, CU_TENSOR_MAP_SWIZZLE_128B) ||
                 !encode_2d(&tmXs, g.Xsum + g.col0 * g.ldxs, uint64_t(g.K), uint64_t(g.N), uint64_t(g.ldxs), k3mBK,
                            k3mBN, CU_TENSOR_MAP_SWIZZLE_64B))
                 return set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (3M update operands)");
+            if (OPC) {
+                if (!encode_2d(&tmA, g.U + g.a_r0 + g.a_c0 * g.ldu, uint64_t(2 * g.K), uint64_t(g.M),
+                               uint64_t(2 * g.ldu), 2 * k3mBK, k3mBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+                    !encode_2d(&tmAs, g.As + g.a_r0 + g.a_c0 * g.ldas, uint64_t(g.K), uint64_t(g.M), uint64_t(g.ldas),
+                               k3mBK, k3mBM, CU_TENSOR_MAP_SWIZZLE_64B))
+                    return set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (3M op C operands)");
+            } else {
+                tmA = tmX;
+                tmAs = tmXs;
+            }
+            auto kern = gemm_ws3p_kernel<OPC>;
             static bool attrp = false;
             if (!attrp) {
-                CK(cudaFuncSetAttribute(gemm_ws3p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k3pSmemBytes));
+                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3pSmemBytes));
                 attrp = true;
             }
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
             const int grid = int(std::min<int64_t>(nt, g_num_sms));
             ProfScope ps(PK_GEMM, flops);
-            gemm_ws3p_kernel<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs);
+            kern<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs);
             CK_LAUNCH("gemm_ws3p_kernel");
             return 0;
         }

@@ -13,7 +13,8 @@
 // columns of 8 rows each) are one tensor-map box each (UTMALDG, swizzled, zero fill past K and N).
 // Bulk copies land unswizzled, so A / A+ / C use padded strides; X / X+ use the TMA swizzles with
 // a column permutation of the B fragment (sig8) -- every fragment read is conflict-free
-// (DESIGN §7.2).  Op N only (op C keeps gemm_ws3m_kernel).
+// (DESIGN §7.2).  Op C (A = conj(U)^T, k contiguous in U): A and A+ are tensor-map boxes too, with
+// the same row permutation on the A fragment (sig8; the epilogue maps rows back).
 #pragma once
 #include <cuda.h>   // CUtensorMap
 
@@ -26,14 +27,22 @@ namespace mstrsm {
 //   X+ [nn][8] f64    dense 64-B rows,  TMA SWIZZLE_64B  (16-B chunk k/2 at k/2 ^ ((nn >> 1) & 3))
 //   A  [k][kPA] cplx  bulk copies, padded rows;  A+ [k][kPAs] f64 likewise
 // A C quarter [colq][kPC] cplx (bulk copies) reuses a whole stage.
-constexpr int kPA = 50, kPAs = 52, kPC = 50;
+constexpr int kPA = 50, kPAs = 52;
+// C quarter column stride: op N rows are lane groups 2p, 2p+1 (32p, 32p+16 B), op C rows are the
+// sig8-permuted p, p+4 (16p, 16p+64 B); 800 B resp. 784 B columns keep the epilogue reads
+// conflict-free.
+template <bool OPC> constexpr int k3p_pc() { return OPC ? 49 : 50; }
 constexpr int k3pOffXs = k3mBN * k3mBK * 16;                     // 8192
 constexpr int k3pOffA = k3pOffXs + k3mBN * k3mBK * 8;            // 12288
 constexpr int k3pOffAs = k3pOffA + k3mBK * kPA * 16;             // 18688
+// op C: A (48 rows x 8 k, k contiguous) and A+ come as tensor-map boxes: A [mm][8] cplx dense
+// 128-B rows (128-B swizzle), A+ [mm][8] f64 64-B rows (64-B swizzle), rows sig8-permuted
+constexpr int k3pOffAsC = k3pOffA + k3mBM * k3mBK * 16;           // 18432
 constexpr int k3pStage = (k3pOffAs + k3mBK * kPAs * 8 + 1023) & ~1023;
 constexpr int k3pRing = (227 * 1024 - 4096 - 1024) / (2 * k3pStage);
 constexpr int k3pSmemBytes = 2 * k3pRing * k3pStage + 1024;      // + 1024: base alignment
-static_assert(16 * kPC * 16 <= k3pStage, "a C quarter must fit in one stage");
+static_assert(16 * 50 * 16 <= k3pStage, "a C quarter must fit in one stage");
+static_assert(k3pOffA % 1024 == 0 && k3pOffAsC % 512 == 0 && k3pOffAsC + k3mBM * k3mBK * 8 <= k3pStage, "");
 static_assert(k3pOffA % 16 == 0 && k3pOffAs % 16 == 0 && k3pOffXs % 512 == 0, "");
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t bytes) {
@@ -57,9 +66,13 @@ __device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *tm, int c0,
 // the swizzled 128-B / 64-B rows.  Accumulator column 2 tq + c is then column tq + 4 c.
 __device__ __forceinline__ int sig8(int gq) { return (gq >> 1) | ((gq & 1) << 2); }
 
+template <bool OPC>
 __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx> g, int tiles_m, int ntiles,
                                                                   const __grid_constant__ CUtensorMap tmX,
-                                                                  const __grid_constant__ CUtensorMap tmXs) {
+                                                                  const __grid_constant__ CUtensorMap tmXs,
+                                                                  const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmAs) {
+    constexpr int kPC = k3p_pc<OPC>();
     constexpr int BM = k3mBM, BN = k3mBN, BK = k3mBK, RS = k3pRing;
     constexpr int MI = k3mMI, NI = 4;
     extern __shared__ __align__(1024) unsigned char smem_dyn[];
@@ -115,6 +128,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
                         mbar_arrive_expect_tx(fb, BN * BK * 24);
                         tma_2d(st, &tmX, 2 * k0, int(n0), fb);
                         tma_2d(st + k3pOffXs, &tmXs, k0, int(n0), fb);
+                    } else {
+                        mbar_arrive(fb);
+                    }
+                } else if (OPC) {               // A = conj(U)^T, A+: one tensor-map box each
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(fb, BM * BK * 24);
+                        tma_2d(st + k3pOffA, &tmA, 2 * k0, int(m0), fb);
+                        tma_2d(st + k3pOffAsC, &tmAs, k0, int(m0), fb);
                     } else {
                         mbar_arrive(fb);
                     }
@@ -193,6 +214,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
             const cplx *As = reinterpret_cast<const cplx *>(st + k3pOffA) + wm * 8 * MI + gq;
             const double *Ass = reinterpret_cast<const double *>(st + k3pOffAs) + wm * 8 * MI + gq;
             const unsigned char *Xb = st + (wn * 32 + sg) * 128, *Xsb = st + k3pOffXs + (wn * 32 + sg) * 64;
+            const unsigned char *Ab = st + k3pOffA + (wm * 8 * MI + sg) * 128;
+            const unsigned char *Asb = st + k3pOffAsC + (wm * 8 * MI + sg) * 64;
 #pragma unroll
             for (int kk = 0; kk < BK / 4; kk++) {
                 const int k = kk * 4 + tq;
@@ -200,10 +223,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
                 double ar[MI], ai[MI], as[MI], br[NI], bi[NI], bs[NI];
 #pragma unroll
                 for (int i = 0; i < MI; i++) {
-                    const cplx v = As[k * kPA + i * 8];
-                    ar[i] = v.x;
-                    ai[i] = v.y;
-                    as[i] = Ass[k * kPAs + i * 8];
+                    if constexpr (OPC) {        // rows wm 24 + 8 i + sig8(gq), conj at use
+                        const cplx v = *reinterpret_cast<const cplx *>(Ab + i * 8 * 128 + xo);
+                        ar[i] = v.x;
+                        ai[i] = -v.y;
+                        as[i] = *reinterpret_cast<const double *>(Asb + i * 8 * 64 + xso);
+                    } else {
+                        const cplx v = As[k * kPA + i * 8];
+                        ar[i] = v.x;
+                        ai[i] = v.y;
+                        as[i] = Ass[k * kPAs + i * 8];
+                    }
                 }
 #pragma unroll
                 for (int jn = 0; jn < NI; jn++) {
@@ -254,7 +284,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
                     cplx *colp = g.B + g.c_r0 + (g.col0 + gj) * g.ldb;
 #pragma unroll
                     for (int i = 0; i < MI; i++) {
-                        const int row = wm * 8 * MI + i * 8 + gq;
+                        const int row = wm * 8 * MI + i * 8 + (OPC ? sg : gq);
                         const int64_t gi = m0 + row;
                         const cplx old = Cs[colq * kPC + row];
                         const double re = __dsub_rn(p1[i][jn][c], p2[i][jn][c]);

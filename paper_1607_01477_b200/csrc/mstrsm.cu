@@ -171,8 +171,7 @@ template <typename T>
 int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, int64_t n, int nb) {
     if constexpr (!S<T>::cplx_) return 0;
     else {
-        // op C keeps the in-register sums (its A operand is k-contiguous)
-        if (gemm_variant() != 0 || m == 0 || op != 0 || !gemm_presum_enabled()) return 0;
+        if (gemm_variant() != 0 || m == 0 || !gemm_presum_enabled()) return 0;
         sp.st = g_stream;
         // even leading dimensions (16-byte aligned bulk copies), ldu > m so that a copy rounded
         // up to 16 bytes past the last row of a column stays inside that column
