@@ -95,6 +95,22 @@ int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, i
                 int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
                 int nb);
 
+/* Caller-managed workspace: as mstrsm_*_ex, with every device allocation of the
+ * solve carved from `workspace` (device, 256-byte aligned, caller-owned, not touched after the
+ * work enqueued by the call completes) instead of the stream-ordered pool.  workspace = NULL
+ * behaves as mstrsm_*_ex.  mstrsm_workspace_size returns a sufficient size (bytes) for the
+ * given problem (0 for an empty problem or an invalid nb).  Errors as mstrsm_*_ex, plus -15
+ * (misaligned workspace) and -16 (workspace_bytes too small).                               */
+size_t mstrsm_workspace_size(int64_t m, int64_t n, int nb, int is_complex, int safe);
+int mstrsm_d_ex_ws(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m,
+                   const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
+                   const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb,
+                   void *workspace, size_t workspace_bytes);
+int mstrsm_z_ex_ws(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
+                   const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
+                   int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales,
+                   int32_t *scale_exp, int nb, void *workspace, size_t workspace_bytes);
+
 /* ------------------------------------------------------------------------------------
  * The footnote family of P:58-62: left/right, upper/lower.
  *   side = LEFT : (A - s_j I) x_j = c_j b_j          B is m x n (ldb >= max(1,m)), column j = b_j

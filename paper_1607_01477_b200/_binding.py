@@ -26,7 +26,7 @@ __all__ = [
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "trevc_z_host_batch", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
-    "spectral_portrait", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
+    "spectral_portrait", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
@@ -61,6 +61,10 @@ def load():
         "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_host_batch": [P, c_i64, c_i64, P, c_i64, P, P, c_i64, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
+        "mstrsm_d_ex_ws": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int, P,
+                           ctypes.c_size_t],
+        "mstrsm_z_ex_ws": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int, P,
+                           ctypes.c_size_t],
         "mstrsm_d_side": [c_int, c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int],
         "mstrsm_z_side": [c_int, c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int],
         "spectral_cloud_z": [P, c_i64, c_i64, P, c_i64, c_int, c_dbl, P, P, P, P, c_int],
@@ -89,6 +93,8 @@ def load():
         f.argtypes = args
         f.restype = c_int
     lib.mstrsm_launch_count.restype = c_i64
+    lib.mstrsm_workspace_size.restype = ctypes.c_size_t
+    lib.mstrsm_workspace_size.argtypes = [c_i64, c_i64, c_int, c_int, c_int]
     lib.mstrsm_error_string.restype = ctypes.c_char_p
     lib.mstrsm_get_stream.restype = c_vp
     _lib = lib
@@ -234,6 +240,24 @@ def tgevc_z(T, ldt, S, lds, m, Z, ldz, lam, scales, scale_exp, nb):
 def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
     _call("pseudospectra_z", _ptr(U), ldu, m, _ptr(z), npts, iters, _ptr(v0), _ptr(sigma_min),
           _ptr(flags), nb)
+
+
+def mstrsm_workspace_size(m: int, n: int, nb: int, is_complex: bool, safe: bool) -> int:
+    return int(load().mstrsm_workspace_size(m, n, nb, int(is_complex), int(safe)))
+
+
+def mstrsm_d_ex_ws(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb,
+                   workspace, workspace_bytes):
+    arr, p = _host_i64(row_end_host)
+    _call("mstrsm_d_ex_ws", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
+          _ptr(scales), _ptr(scale_exp), nb, _ptr(workspace), workspace_bytes)
+
+
+def mstrsm_z_ex_ws(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb,
+                   workspace, workspace_bytes):
+    arr, p = _host_i64(row_end_host)
+    _call("mstrsm_z_ex_ws", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
+          _ptr(scales), _ptr(scale_exp), nb, _ptr(workspace), workspace_bytes)
 
 
 def mstrsm_d_side(safe, side, uplo, A, lda, m, shifts, shift_stride, B, ldb, n, scales, scale_exp, nb):

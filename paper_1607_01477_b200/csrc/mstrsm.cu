@@ -29,6 +29,32 @@ using namespace mstrsm::rt;
 namespace {
 
 // Device workspace for one solve, carved out of one stream-ordered allocation.
+// Caller-provided workspace (mstrsm_*_ex_ws): while a call runs with an arena, every device
+// allocation of the solve is carved from it (256-B aligned) and never freed; otherwise
+// allocations are stream-ordered from the device pool.
+struct Arena {
+    char *base = nullptr;
+    size_t size = 0, off = 0;
+    bool active = false;
+};
+thread_local Arena g_arena;
+cudaError_t ws_malloc(void **p, size_t bytes) {
+    if (g_arena.active) {
+        const size_t o = (g_arena.off + 255) & ~size_t(255);
+        if (o + bytes > g_arena.size) return cudaErrorMemoryAllocation;
+        *p = g_arena.base + o;
+        g_arena.off = o + bytes;
+        return cudaSuccess;
+    }
+    return cudaMallocAsync(p, bytes, g_stream);
+}
+void ws_free(void *p, cudaStream_t st) {
+    if (!p) return;
+    const char *c = static_cast<const char *>(p);
+    if (g_arena.active && c >= g_arena.base && c < g_arena.base + g_arena.size) return;
+    cudaFreeAsync(p, st);
+}
+
 struct Work {
     void *base = nullptr;
     double *cnl = nullptr, *part = nullptr, *P = nullptr, *delta = nullptr, *G = nullptr;
@@ -37,11 +63,11 @@ struct Work {
     int64_t *rowend = nullptr;
     void *shifts = nullptr;            // trevc: gathered diag(T)
     cudaStream_t st = nullptr;
-    ~Work() { if (base) cudaFreeAsync(base, st); }
+    ~Work() { ws_free(base, st); }
 };
 
 template <typename T>
-int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool need_shifts) {
+int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool need_shifts, size_t *bytes_only = nullptr) {
     int64_t nblk = cdiv(m, nb);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
@@ -50,8 +76,9 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
            o_E = take(std::max<int64_t>(nblk, 1) * n * 4), o_r = take(need_rowend ? n * 8 : 0),
            o_fl = take(n * 4), o_fc = take(std::max<int64_t>(nblk, 1) * 4),
            o_s = take(need_shifts ? n * sizeof(T) : 0);
+    if (bytes_only) { *bytes_only = off; return 0; }
     w.st = g_stream;
-    CK(cudaMallocAsync(&w.base, off, g_stream));
+    CK(ws_malloc(&w.base, off));
     char *b = static_cast<char *>(w.base);
     w.cnl = (double *)(b + o_cnl); w.part = (double *)(b + o_part); w.P = (double *)(b + o_P);
     w.delta = (double *)(b + o_delta); w.G = (double *)(b + o_G); w.e = (int *)(b + o_e);
@@ -81,12 +108,12 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w) {
         CK_LAUNCH("panel_sum_kernel");
         int64_t nch = cdiv(m, kRowsumChunk);
         double *part2 = nullptr;
-        CK(cudaMallocAsync(&part2, size_t(nch) * m * 8, g_stream));
+        CK(ws_malloc((void **)&part2, size_t(nch) * m * 8));
         rowsum_n_kernel<T><<<dim3(unsigned(cdiv(m, 128)), unsigned(nch)), 128, 0, g_stream>>>(U, ldu, m, part2);
         CK_LAUNCH("rowsum_n_kernel");
         rowsum_reduce_kernel<<<int(cdiv(m, 128)), 128, 0, g_stream>>>(m, nch, part2, w.part);
         CK_LAUNCH("rowsum_reduce_kernel");
-        CK(cudaFreeAsync(part2, g_stream));
+        ws_free(part2, g_stream);
     } else {
         norm_rows_c_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
         CK_LAUNCH("norm_rows_c_kernel");
@@ -165,7 +192,7 @@ struct SumPlanes {
     int64_t ldu = 0;
     int ldx = 0;
     cudaStream_t st = nullptr;
-    ~SumPlanes() { if (U) cudaFreeAsync(U, st); if (X) cudaFreeAsync(X, st); }
+    ~SumPlanes() { ws_free(U, st); ws_free(X, st); }
 };
 template <typename T>
 int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, int64_t n, int nb) {
@@ -177,8 +204,8 @@ int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, i
         // up to 16 bytes past the last row of a column stays inside that column
         sp.ldu = (m + 2) & ~int64_t(1);
         sp.ldx = (nb + 1) & ~1;
-        CK(cudaMallocAsync(&sp.U, size_t(sp.ldu) * m * 8, g_stream));
-        CK(cudaMallocAsync(&sp.X, size_t(sp.ldx) * std::max<int64_t>(n, 1) * 8, g_stream));
+        CK(ws_malloc((void **)&sp.U, size_t(sp.ldu) * m * 8));
+        CK(ws_malloc((void **)&sp.X, size_t(sp.ldx) * std::max<int64_t>(n, 1) * 8));
         int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
         presum_kernel<<<blocks, 256, 0, g_stream>>>(U, ldu, m, sp.U, sp.ldu, op == 0 ? 1.0 : -1.0);
         CK_LAUNCH("presum_kernel");
@@ -811,6 +838,24 @@ static int short_pos(int rc) {
     }
 }
 
+template <typename T>
+int ex_ws_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride, T *B,
+               int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb,
+               void *workspace, size_t workspace_bytes) {
+    if (!workspace)                                  // NULL: the library allocates (as mstrsm_*_ex)
+        return mstrsm_ex_impl<T>(safe, op, U, ldu, m, shifts, sstride, B, ldb, n, row_end_host, scales,
+                                 scale_exp, nb);
+    if (reinterpret_cast<uintptr_t>(workspace) % 256) return -15;
+    g_arena.base = static_cast<char *>(workspace);
+    g_arena.size = workspace_bytes;
+    g_arena.off = 0;
+    g_arena.active = true;
+    int rc = mstrsm_ex_impl<T>(safe, op, U, ldu, m, shifts, sstride, B, ldb, n, row_end_host, scales, scale_exp, nb);
+    g_arena.active = false;
+    if (rc == 1 && last_cuda_error() == cudaErrorMemoryAllocation) rc = -16;   // workspace too small
+    return rc;
+}
+
 extern "C" {
 
 int mstrsm_d(const double *U, int64_t ldu, int64_t m, const double *shifts, double *B, int64_t ldb,
@@ -842,6 +887,35 @@ int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, i
                 double *scales, int32_t *scale_exp, int nb) {
     return mstrsm_ex_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride,
                                 (cplx *)B, ldb, n, row_end_host, scales, scale_exp, nb);
+}
+
+size_t mstrsm_workspace_size(int64_t m, int64_t n, int nb, int is_complex, int safe) {
+    if (m <= 0 || n <= 0) return 0;
+    if (nb == 0) nb = 64;
+    if (nb < 1 || nb > 128) return 0;
+    Work w;
+    size_t work = 0;
+    if (is_complex) alloc_work<cplx>(w, m, n, nb, true, false, &work);
+    else alloc_work<double>(w, m, n, nb, true, false, &work);
+    size_t total = work + 256;
+    if (safe) total += size_t(cdiv(m, kRowsumChunk)) * m * 8 + 256;              // norm pass partials
+    if (is_complex && gemm_variant() == 0 && gemm_presum_enabled())            // 3M operand-sum planes
+        total += size_t((m + 2) & ~int64_t(1)) * m * 8 + size_t((nb + 1) & ~1) * n * 8 + 512;
+    return total;
+}
+
+int mstrsm_d_ex_ws(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
+                   int64_t shift_stride, double *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                   double *scales, int32_t *scale_exp, int nb, void *workspace, size_t workspace_bytes) {
+    return ex_ws_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales,
+                              scale_exp, nb, workspace, workspace_bytes);
+}
+int mstrsm_z_ex_ws(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
+                   const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n,
+                   const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb, void *workspace,
+                   size_t workspace_bytes) {
+    return ex_ws_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride, (cplx *)B,
+                            ldb, n, row_end_host, scales, scale_exp, nb, workspace, workspace_bytes);
 }
 
 int trevc_d(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,

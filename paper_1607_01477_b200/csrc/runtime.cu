@@ -21,10 +21,13 @@ bool g_prof = false;
 std::vector<ProfRec> g_prof_recs;
 std::vector<cudaEvent_t> g_ev_pool;
 
+static thread_local cudaError_t g_last_err = cudaSuccess;
 int set_cuda_error(cudaError_t e, const char *where) {
     snprintf(g_errmsg, sizeof(g_errmsg), "CUDA error in %s: %s", where, cudaGetErrorString(e));
+    g_last_err = e;
     return 1;
 }
+cudaError_t last_cuda_error() { return g_last_err; }
 
 int ensure_init() {
     std::lock_guard<std::mutex> lk(g_mu);

@@ -24,6 +24,7 @@ extern bool g_debug_sync;
 extern int g_diag_force_fb;
 
 int set_cuda_error(cudaError_t e, const char *where);
+cudaError_t last_cuda_error();   // the error recorded by the last set_cuda_error on this thread
 int ensure_init();
 
 #define CK(call)                                                       \

@@ -105,6 +105,17 @@ def test_empty_problems_return_zero_without_cuda():
     assert lib.trevc_qz_d(P, 1, 0, P, 1, P, 1, P, P, 0) == 0
 
 
+def test_workspace_size_without_cuda():
+    lib = _lib()
+    small = lib.mstrsm_workspace_size(100, 10, 32, 0, 1)
+    big = lib.mstrsm_workspace_size(1000, 100, 32, 1, 1)
+    assert 0 < small < big
+    assert lib.mstrsm_workspace_size(100, 10, 200, 0, 1) == 0          # invalid nb
+    assert lib.mstrsm_workspace_size(0, 10, 32, 0, 1) == 0             # empty problem
+    assert lib.mstrsm_z_ex_ws(0, 0, None, 4, 4, None, 1, None, 4, 1, None, None, None, 0,
+                              ctypes.c_void_p(256), 1) == -3               # U NULL, checked before CUDA
+
+
 def test_error_strings():
     lib = _lib()
     assert lib.mstrsm_error_string(0) == b"success"
