@@ -39,47 +39,96 @@ def max_shard(m: int, P: int, g: int = 16) -> int:
 
 def unpack(gathered, m: int, P: int, g: int = 16):
     """gathered[r][q, :] = eigenvector shard_cols(m, P, r)[q] (rows padded to max_shard) ->
-    (m x m) column-major tensor Z with Z[:, k] = eigenvector k.  Works on torch tensors."""
+    (m x m) column-major tensor Z with Z[:, k] = eigenvector k.  Works on torch tensors.
+    `gathered` is a list of P (max_shard x m) tensors or one (P * max_shard x m) tensor."""
     import torch
-    first = gathered[0]
-    Z = torch.empty((m, m), dtype=first.dtype, device=first.device).t()   # column-major view
+    if isinstance(gathered, (list, tuple)):
+        gathered = torch.cat(list(gathered), 0)
+    perm = torch.from_numpy(gather_perm(m, P, g)).to(gathered.device)
+    return gathered.index_select(0, perm).t()          # row k = eigenvector k -> column-major Z
+
+
+def gather_perm(m: int, P: int, g: int = 16) -> np.ndarray:
+    """Row of the gathered (P * max_shard x m) array holding eigenvector k, for k = 0..m-1."""
+    mc = max_shard(m, P, g)
+    perm = np.empty(m, dtype=np.int64)
     for r in range(P):
-        cols = torch.from_numpy(shard_cols(m, P, r, g)).to(first.device)
-        Z[:, cols] = gathered[r][: len(cols)].t()
-    return Z
+        cols = shard_cols(m, P, r, g)
+        perm[cols] = r * mc + np.arange(len(cols))
+    return perm
+
+
+def _panels(m: int, w: int):
+    return [(c0, min(m, c0 + w)) for c0 in range(0, m, w)]
+
+
+def pack_upper(T, m: int, w: int = 128):
+    """The upper triangle of T as w-column panels T[0:c1, c0:c1] (rows up to the panel end, column
+    by column) in one contiguous buffer: what the solve reads (the strictly lower triangle never
+    is), ~m^2/2 elements instead of m^2."""
+    import torch
+    sizes = [c1 * (c1 - c0) for c0, c1 in _panels(m, w)]
+    buf = torch.empty(sum(sizes), dtype=T.dtype, device=T.device)
+    off = 0
+    for (c0, c1), n in zip(_panels(m, w), sizes):
+        buf[off:off + n].view(c1 - c0, c1).copy_(T[:c1, c0:c1].t())
+        off += n
+    return buf
+
+
+def unpack_upper(buf, T, m: int, w: int = 128) -> None:
+    off = 0
+    for c0, c1 in _panels(m, w):
+        n = c1 * (c1 - c0)
+        T[:c1, c0:c1].copy_(buf[off:off + n].view(c1 - c0, c1).t())
+        off += n
 
 
 def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, group=None):
-    """Broadcast T from rank 0, solve this rank's block-cyclic column shard with `solve_cols`,
-    all-gather the shards (vectors + int32 exponents) and unpack on every rank.
+    """Broadcast T's upper triangle from rank 0, solve this rank's block-cyclic column shard with
+    `solve_cols`, all-gather the shards (vectors + int32 exponents) and unpack on every rank.
 
-    T: (m x m) tensor on every rank (contents only needed on rank 0; overwritten elsewhere).
-    solve_cols(T, cols) -> (Z_local (m x ncols, column q = eigenvector cols[q]), e_local (ncols,)).
+    T: (m x m) tensor on every rank (contents only needed on rank 0; its upper triangle is
+    overwritten elsewhere, the strictly lower triangle is not sent).
+    solve_cols(T, cols, out) writes eigenvector cols[q] into column q of `out` (an m x ncols
+    column-major view into this rank's all-gather send buffer, so no copy is needed) and returns
+    the int32 exponents (ncols,).
     Returns (Z (m x m, column-major), e (m,) int32), identical on every rank."""
     import torch
     import torch.distributed as dist
     if world > 1:
-        buf = T if T.is_contiguous() else T.t()          # column-major (m x m) views are .t() of a
-        assert buf.is_contiguous()                       # contiguous buffer: send the storage
+        buf = pack_upper(T, m) if rank == 0 else None
+        if rank != 0:
+            n = sum(c1 * (c1 - c0) for c0, c1 in _panels(m, 128))
+            buf = torch.empty(n, dtype=T.dtype, device=T.device)
         dist.broadcast(buf, src=0, group=group)
+        if rank != 0:
+            unpack_upper(buf, T, m)
+        del buf
     cols = shard_cols(m, world, rank, g)
-    Zl, el = solve_cols(T, cols)
+    mc = max_shard(m, world, g) if world > 1 else len(cols)
+    send = torch.empty((mc, m), dtype=T.dtype, device=T.device)           # row q = eigenvector q
+    # (rows >= ncols are padding: sent, never unpacked)
+    el = solve_cols(T, cols, send[: len(cols)].t())
     if world == 1:
         e = torch.empty(m, dtype=torch.int32, device=el.device)
         e[torch.from_numpy(cols).to(el.device)] = el
-        return Zl, e
-    mc = max_shard(m, world, g)
-    pad = torch.zeros((mc, m), dtype=Zl.dtype, device=Zl.device)           # row q = eigenvector q
-    pad[: len(cols)] = Zl.t()
-    epad = torch.zeros(mc, dtype=torch.int32, device=el.device)
+        return send.t(), e
+    epad = torch.empty(mc, dtype=torch.int32, device=el.device)
     epad[: len(cols)] = el
-    outs = [torch.empty_like(pad) for _ in range(world)]
-    eouts = [torch.empty_like(epad) for _ in range(world)]
-    dist.all_gather(outs, pad, group=group)
-    dist.all_gather(eouts, epad, group=group)
-    Z = unpack(outs, m, world, g)
-    e = torch.empty(m, dtype=torch.int32, device=el.device)
-    for r in range(world):
-        c = torch.from_numpy(shard_cols(m, world, r, g)).to(el.device)
-        e[c] = eouts[r][: len(c)]
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        out = torch.empty((world * mc, m), dtype=send.dtype, device=send.device)
+        eout = torch.empty(world * mc, dtype=torch.int32, device=el.device)
+        dist.all_gather_into_tensor(out, send, group=group)
+        dist.all_gather_into_tensor(eout, epad, group=group)
+    else:                                                                   # gloo (CPU tests)
+        outs = [torch.empty_like(send) for _ in range(world)]
+        eouts = [torch.empty_like(epad) for _ in range(world)]
+        dist.all_gather(outs, send, group=group)
+        dist.all_gather(eouts, epad, group=group)
+        out, eout = torch.cat(outs, 0), torch.cat(eouts, 0)
+    perm = torch.from_numpy(gather_perm(m, world, g)).to(out.device)
+    Z = out.index_select(0, perm).t()
+    e = eout.index_select(0, perm.to(eout.device))
     return Z, e

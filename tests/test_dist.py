@@ -46,6 +46,16 @@ def test_unpack_inverts_the_shard_layout():
     assert torch.equal(pdist.unpack(gathered, m, P, g), Z)
 
 
+def test_pack_upper_roundtrip_keeps_the_upper_triangle():
+    m = 300
+    T = torch.arange(m * m, dtype=torch.float64).reshape(m, m).t().contiguous().t()   # column-major
+    buf = pdist.pack_upper(T, m, 128)
+    assert buf.numel() == sum(min(m, c + 128) * (min(m, c + 128) - c) for c in range(0, m, 128))
+    R = torch.full((m, m), -1.0, dtype=torch.float64).t()
+    pdist.unpack_upper(buf, R, m, 128)
+    assert torch.equal(torch.triu(R), torch.triu(T))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -65,9 +75,10 @@ def _worker(rank, world, port, m, nb, cplx, out):
         else:
             T = torch.zeros((m, m), dtype=dtype)
 
-        def solve_cols(Tt, cols):
+        def solve_cols(Tt, cols, out):
             Zl, el = oracle.trevc(Tt.numpy(), nb=nb, cols=cols, nthreads=1)
-            return torch.from_numpy(Zl), torch.from_numpy(el)
+            out.copy_(torch.from_numpy(Zl))
+            return torch.from_numpy(el)
 
         Z, e = pdist.trevc_sharded(T, m, solve_cols, rank=rank, world=world, g=4)
         out[rank] = (Z.contiguous().numpy().copy(), e.numpy().copy())
