@@ -8,7 +8,7 @@
 
 #include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
 
-#include "gemm_ws3p.cuh"
+#include "gemm_ws3q.cuh"
 #include "runtime.cuh"
 
 namespace mstrsm {
@@ -55,6 +55,16 @@ static bool encode_2d(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MSTRSM_3M_GROUPS=3: three consumer warpgroups (gemm_ws3q.cuh) instead of two
+static int gemm_3m_groups() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_3M_GROUPS");
+        v = (e && !strcmp(e, "3")) ? 3 : 2;
+    }
+    return v;
+}
+
 static bool use_classic() { return gemm_variant() == 1; }
 
 template <typename T, bool OPC>
@@ -86,15 +96,31 @@ int launch_gemm(const GemmArgs<T> &g) {
                 !encode_2d(&tmXs, g.Xsum + g.col0 * g.ldxs, uint64_t(g.K), uint64_t(g.N), uint64_t(g.ldxs), k3mBK,
                            k3mBN, CU_TENSOR_MAP_SWIZZLE_64B))
                 return set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (3M update operands)");
+            const bool q3 = gemm_3m_groups() == 3;
+            const uint32_t bm = q3 ? k3qBM : k3mBM;
             if (OPC) {
                 if (!encode_2d(&tmA, g.U + g.a_r0 + g.a_c0 * g.ldu, uint64_t(2 * g.K), uint64_t(g.M),
-                               uint64_t(2 * g.ldu), 2 * k3mBK, k3mBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+                               uint64_t(2 * g.ldu), 2 * k3mBK, bm, CU_TENSOR_MAP_SWIZZLE_128B) ||
                     !encode_2d(&tmAs, g.As + g.a_r0 + g.a_c0 * g.ldas, uint64_t(g.K), uint64_t(g.M), uint64_t(g.ldas),
-                               k3mBK, k3mBM, CU_TENSOR_MAP_SWIZZLE_64B))
+                               k3mBK, bm, CU_TENSOR_MAP_SWIZZLE_64B))
                     return set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (3M op C operands)");
             } else {
                 tmA = tmX;
                 tmAs = tmXs;
+            }
+            if (q3) {
+                auto kq = gemm_ws3q_kernel<OPC>;
+                static bool attrq = false;
+                if (!attrq) {
+                    CK(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, k3qSmemBytes));
+                    attrq = true;
+                }
+                const int64_t tm = cdiv(g.M, k3qBM), tn = cdiv(g.N, k3qBN), nt = tm * tn;
+                const int grid = int(std::min<int64_t>(nt, g_num_sms));
+                ProfScope ps(PK_GEMM, flops);
+                kq<<<grid, k3qThreads, k3qSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs);
+                CK_LAUNCH("gemm_ws3q_kernel");
+                return 0;
             }
             auto kern = gemm_ws3p_kernel<OPC>;
             static bool attrp = false;
