@@ -268,6 +268,30 @@ int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dc
                mstrsm_dcomplex *X, int64_t ldx, double *scales, int32_t *scale_exp, int nb);
 
 /* ------------------------------------------------------------------------------------
+ * Multi-GPU: one process per GPU, an NCCL communicator over the ranks.
+ *   mstrsm_comm_unique_id  rank 0 draws the 128-byte NCCL id (host buffer); the caller hands it
+ *                          to every rank (e.g. over its torch process group)
+ *   mstrsm_comm_init       every rank, on its current device; replaces a previous communicator
+ *   mstrsm_dist_shard      host only: the eigenvector indices rank `rank` of `nranks` owns
+ *                          (groups of 16 columns dealt serpentine block-cyclically, balancing the
+ *                          ~(k-1)^2 cost); returns the count, fills cols_out (nullable) ascending
+ *   trevc_*_dist           TriangEig over all ranks: T (device) is read on `root` only (other
+ *                          ranks may pass NULL / any ldt), its upper triangle is broadcast, each
+ *                          rank solves its shard, the shards (+ scales, exponents) are all-gathered
+ *                          and every rank receives the full Z (m x m, ldz), scales and scale_exp
+ *                          (nullable, m entries) in natural order -- bit-identical to trevc_*.
+ *                          Collective: every rank must call it.  Errors: -i for argument i, 1
+ *                          CUDA error, 3 communication error (or no communicator).           */
+int     mstrsm_comm_unique_id(void *id_out);
+int     mstrsm_comm_init(int nranks, int rank, const void *unique_id);
+int     mstrsm_comm_destroy(void);
+int64_t mstrsm_dist_shard(int64_t m, int nranks, int rank, int64_t *cols_out);
+int trevc_d_dist(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,
+                 int32_t *scale_exp, int nb, int root);
+int trevc_z_dist(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, mstrsm_dcomplex *Z, int64_t ldz,
+                 double *scales, int32_t *scale_exp, int nb, int root);
+
+/* ------------------------------------------------------------------------------------
  * Runtime helpers */
 int         mstrsm_set_stream(void *cuda_stream);  /* cudaStream_t; NULL = legacy stream */
 void       *mstrsm_get_stream(void);

@@ -26,7 +26,7 @@ __all__ = [
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "trevc_z_host_batch", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
-    "spectral_portrait", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
+    "spectral_portrait", "comm_init", "comm_destroy", "dist_shard", "trevc_dist", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
@@ -61,6 +61,11 @@ def load():
         "trevc_z_host": [P, c_i64, c_i64, P, c_i64, P, P, c_int],
         "trevc_z_host_batch": [P, c_i64, c_i64, P, c_i64, P, P, c_i64, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
+        "mstrsm_comm_unique_id": [P],
+        "mstrsm_comm_init": [c_int, c_int, P],
+        "mstrsm_comm_destroy": [],
+        "trevc_d_dist": [P, c_i64, c_i64, P, c_i64, P, P, c_int, c_int],
+        "trevc_z_dist": [P, c_i64, c_i64, P, c_i64, P, P, c_int, c_int],
         "mstrsm_d_ex_ws": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int, P,
                            ctypes.c_size_t],
         "mstrsm_z_ex_ws": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int, P,
@@ -93,6 +98,8 @@ def load():
         f.argtypes = args
         f.restype = c_int
     lib.mstrsm_launch_count.restype = c_i64
+    lib.mstrsm_dist_shard.restype = c_i64
+    lib.mstrsm_dist_shard.argtypes = [c_i64, c_int, c_int, P]
     lib.mstrsm_workspace_size.restype = ctypes.c_size_t
     lib.mstrsm_workspace_size.argtypes = [c_i64, c_i64, c_int, c_int, c_int]
     lib.mstrsm_error_string.restype = ctypes.c_char_p
@@ -240,6 +247,54 @@ def tgevc_z(T, ldt, S, lds, m, Z, ldz, lam, scales, scale_exp, nb):
 def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
     _call("pseudospectra_z", _ptr(U), ldu, m, _ptr(z), npts, iters, _ptr(v0), _ptr(sigma_min),
           _ptr(flags), nb)
+
+
+def dist_shard(m: int, nranks: int, rank: int) -> np.ndarray:
+    """Eigenvector indices rank `rank` owns (the library's serpentine block-cyclic map)."""
+    lib = load()
+    n = int(lib.mstrsm_dist_shard(m, nranks, rank, None))
+    if n < 0:
+        raise MstrsmError("mstrsm_dist_shard: invalid arguments")
+    out = np.empty(max(n, 1), dtype=np.int64)
+    lib.mstrsm_dist_shard(m, nranks, rank, out.ctypes.data_as(c_vp))
+    return out[:n]
+
+
+def comm_init(nranks: int, rank: int, group=None):
+    """NCCL communicator of the library over `nranks` processes (one per GPU): rank 0 draws the
+    id, torch.distributed broadcasts it (nranks = 1 needs no process group)."""
+    lib = load()
+    _bind_stream(lib)
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        _check(lib.mstrsm_comm_unique_id(uid), "mstrsm_comm_unique_id")
+    if nranks > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).clone()
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=group)
+        uid = ctypes.create_string_buffer(bytes(t.cpu().numpy().tobytes()), 128)
+    _check(lib.mstrsm_comm_init(nranks, rank, uid), "mstrsm_comm_init")
+
+
+def comm_destroy():
+    _check(load().mstrsm_comm_destroy(), "mstrsm_comm_destroy")
+
+
+def trevc_dist(T, m: int, *, nb: int = 64, root: int = 0):
+    """TriangEig over every rank of the library communicator: T (column-major CUDA tensor) read on
+    `root`; returns (Z, scales, scale_exp) on every rank."""
+    torch = _torch()
+    dtype = T.dtype if T is not None else torch.complex128
+    dev = T.device if T is not None else torch.device("cuda")
+    Z = torch.empty((m, m), dtype=dtype, device=dev).t()
+    scales = torch.empty(m, dtype=torch.float64, device=dev)
+    exps = torch.empty(m, dtype=torch.int32, device=dev)
+    name = "trevc_z_dist" if dtype == torch.complex128 else "trevc_d_dist"
+    _call(name, _ptr(T), _ld(T) if T is not None else 1, m, _ptr(Z), _ld(Z), _ptr(scales), _ptr(exps), nb, root)
+    return Z, scales, exps
 
 
 def mstrsm_workspace_size(m: int, n: int, nb: int, is_complex: bool, safe: bool) -> int:

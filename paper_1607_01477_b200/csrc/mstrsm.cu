@@ -1277,3 +1277,206 @@ extern "C" int mstrsm_fp64_peak(double ms, double *dmma_tflops, double *dfma_tfl
     cudaFree(out);
     return 0;
 }
+
+// ================================================================ multi-GPU
+// One process per GPU; an NCCL communicator bootstrapped by the caller (rank 0 draws the unique
+// id, the caller distributes it, e.g. over its torch process group).  trevc_*_dist replicates the
+// upper triangle of T from `root` (packed 128-column panels, one ncclBroadcast), solves this
+// rank's serpentine block-cyclic column shard (groups of 16; trevc_*_cols), all-gathers the
+// shards with their scales and exponents and unpacks them into natural order on every rank.
+// Bit-identical to the single-GPU trevc_* (columns are independent).
+#include <nccl.h>
+
+namespace {
+ncclComm_t g_comm = nullptr;
+int g_comm_n = 0, g_comm_r = 0;
+constexpr int kShardGroup = 16;
+
+int64_t shard_of(int64_t m, int P, int r, int g, int64_t *cols) {
+    int64_t n = 0;
+    for (int64_t k = 0; k < m; k++) {
+        const int64_t q = k / g;
+        const int c = int(q % P);
+        const int own = ((q / P) % 2 == 0) ? c : P - 1 - c;
+        if (own == r) {
+            if (cols) cols[n] = k;
+            n++;
+        }
+    }
+    return n;
+}
+
+template <typename T>
+__global__ void gather_dist_kernel(const T *__restrict__ Za, int64_t m, const int64_t *__restrict__ perm,
+                                   int64_t n, T *__restrict__ Z, int64_t ldz, const double *__restrict__ sa,
+                                   const int *__restrict__ ea, double *__restrict__ scales, int *__restrict__ exps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w; k < n; k += nw) {
+        const int64_t p = perm[k];
+        const T *src = Za + p * m;
+        T *dst = Z + k * ldz;
+        for (int64_t i = lane; i < m; i += 32) dst[i] = src[i];
+        if (lane == 0) {
+            if (scales) scales[k] = sa[p];
+            if (exps) exps[k] = ea[p];
+        }
+    }
+}
+
+#define NCK(call)                                                                             \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) {                                                              \
+            snprintf(g_errmsg, sizeof(g_errmsg), "NCCL error in %s: %s", #call, ncclGetErrorString(r_)); \
+            return 3;                                                                         \
+        }                                                                                     \
+    } while (0)
+
+template <typename T>
+int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, double *scales, int32_t *scale_exp,
+                    int nb, int root) {
+    if (m < 0) return -3;
+    if (ldz < std::max<int64_t>(1, m)) return -5;
+    if (nb != 0 && (nb < 1 || nb > 128)) return -8;
+    if (!g_comm) {
+        snprintf(g_errmsg, sizeof(g_errmsg), "trevc_*_dist: no communicator (mstrsm_comm_init)");
+        return 3;
+    }
+    const int P = g_comm_n, r = g_comm_r;
+    if (root < 0 || root >= P) return -9;
+    if (r == root && ldt < std::max<int64_t>(1, m)) return -2;
+    if (m == 0) return 0;
+    if (r == root && !Tm) return -1;
+    if (!Z) return -4;
+    if (int rc = ensure_init()) return rc;
+    const size_t es = sizeof(T), ndbl = es / 8;
+    // 1. the upper triangle from root, packed by 128-column panels (rows 0 .. panel end)
+    size_t packed = 0;
+    for (int64_t c0 = 0; c0 < m; c0 += 128) {
+        const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+        packed += size_t(c1) * size_t(c1 - c0);
+    }
+    T *pack = nullptr, *Tw = nullptr;
+    CK(cudaMallocAsync(&pack, packed * es, g_stream));
+    if (r == root) {
+        size_t off = 0;
+        for (int64_t c0 = 0; c0 < m; c0 += 128) {
+            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+            CK(cudaMemcpy2DAsync(pack + off, c1 * es, Tm + c0 * ldt, ldt * es, c1 * es, c1 - c0,
+                                 cudaMemcpyDeviceToDevice, g_stream));
+            off += size_t(c1) * size_t(c1 - c0);
+        }
+    }
+    NCK(ncclBroadcast(pack, pack, packed * ndbl, ncclDouble, root, g_comm, g_stream));
+    const T *Tuse = Tm;
+    int64_t lduse = ldt;
+    if (r != root) {
+        CK(cudaMallocAsync(&Tw, size_t(m) * m * es, g_stream));
+        size_t off = 0;
+        for (int64_t c0 = 0; c0 < m; c0 += 128) {
+            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+            CK(cudaMemcpy2DAsync(Tw + c0 * m, m * es, pack + off, c1 * es, c1 * es, c1 - c0,
+                                 cudaMemcpyDeviceToDevice, g_stream));
+            off += size_t(c1) * size_t(c1 - c0);
+        }
+        Tuse = Tw;
+        lduse = m;
+    }
+    // 2. this rank's shard, written into the all-gather send buffer (m x mc, padded)
+    int64_t mc = 0;
+    for (int q = 0; q < P; q++) mc = std::max(mc, shard_of(m, P, q, kShardGroup, nullptr));
+    std::vector<int64_t> cols(std::max<int64_t>(mc, 1));
+    const int64_t ncols = shard_of(m, P, r, kShardGroup, cols.data());
+    T *Zs = nullptr, *Za = nullptr;
+    double *ss = nullptr, *sa = nullptr;
+    int *es_ = nullptr, *ea = nullptr;
+    int64_t *perm_d = nullptr;
+    CK(cudaMallocAsync(&Zs, size_t(m) * mc * es, g_stream));
+    CK(cudaMallocAsync(&ss, size_t(mc) * 8, g_stream));
+    CK(cudaMallocAsync(&es_, size_t(mc) * 4, g_stream));
+    CK(cudaMallocAsync(&Za, size_t(m) * mc * P * es, g_stream));
+    CK(cudaMallocAsync(&sa, size_t(mc) * P * 8, g_stream));
+    CK(cudaMallocAsync(&ea, size_t(mc) * P * 4, g_stream));
+    CK(cudaMallocAsync(&perm_d, size_t(m) * 8, g_stream));
+    int rc = ncols > 0 ? trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb) : 0;
+    if (rc < 0) rc = 1;
+    if (!rc) {
+        // 3. gather every shard (vectors, scales, exponents)
+        NCK(ncclGroupStart());
+        NCK(ncclAllGather(Zs, Za, size_t(m) * mc * ndbl, ncclDouble, g_comm, g_stream));
+        NCK(ncclAllGather(ss, sa, size_t(mc), ncclDouble, g_comm, g_stream));
+        NCK(ncclAllGather(es_, ea, size_t(mc), ncclInt32, g_comm, g_stream));
+        NCK(ncclGroupEnd());
+        // 4. natural order: eigenvector k is row-block slot q of rank owner(k)
+        std::vector<int64_t> perm(m);
+        for (int q = 0; q < P; q++) {
+            const int64_t nq = shard_of(m, P, q, kShardGroup, cols.data());
+            for (int64_t i = 0; i < nq; i++) perm[cols[i]] = int64_t(q) * mc + i;
+        }
+        CK(cudaMemcpyAsync(perm_d, perm.data(), size_t(m) * 8, cudaMemcpyHostToDevice, g_stream));
+        CK(cudaStreamSynchronize(g_stream));       // perm's host buffer goes out of scope below
+        const int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
+        gather_dist_kernel<T><<<blocks, 256, 0, g_stream>>>(Za, m, perm_d, m, Z, ldz, sa, ea, scales,
+                                                            reinterpret_cast<int *>(scale_exp));
+        CK_LAUNCH("gather_dist_kernel");
+    }
+    for (void *p : {(void *)pack, (void *)Tw, (void *)Zs, (void *)ss, (void *)es_, (void *)Za, (void *)sa,
+                    (void *)ea, (void *)perm_d})
+        if (p) cudaFreeAsync(p, g_stream);
+    return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int mstrsm_comm_unique_id(void *id_out) {
+    if (!id_out) return -1;
+    ncclUniqueId id;
+    NCK(ncclGetUniqueId(&id));
+    memcpy(id_out, &id, sizeof(id));
+    return 0;
+}
+
+int mstrsm_comm_init(int nranks, int rank, const void *unique_id) {
+    if (nranks < 1) return -1;
+    if (rank < 0 || rank >= nranks) return -2;
+    if (!unique_id) return -3;
+    if (int rc = ensure_init()) return rc;
+    if (g_comm) {
+        ncclCommDestroy(g_comm);
+        g_comm = nullptr;
+    }
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    NCK(ncclCommInitRank(&g_comm, nranks, id, rank));
+    g_comm_n = nranks;
+    g_comm_r = rank;
+    return 0;
+}
+
+int mstrsm_comm_destroy(void) {
+    if (g_comm) {
+        NCK(ncclCommDestroy(g_comm));
+        g_comm = nullptr;
+    }
+    g_comm_n = g_comm_r = 0;
+    return 0;
+}
+
+int64_t mstrsm_dist_shard(int64_t m, int nranks, int rank, int64_t *cols_out) {
+    if (m < 0 || nranks < 1 || rank < 0 || rank >= nranks) return -1;
+    return shard_of(m, nranks, rank, kShardGroup, cols_out);
+}
+
+int trevc_d_dist(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,
+                 int32_t *scale_exp, int nb, int root) {
+    return trevc_dist_impl<double>(T, ldt, m, Z, ldz, scales, scale_exp, nb, root);
+}
+int trevc_z_dist(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, mstrsm_dcomplex *Z, int64_t ldz,
+                 double *scales, int32_t *scale_exp, int nb, int root) {
+    return trevc_dist_impl<cplx>((const cplx *)T, ldt, m, (cplx *)Z, ldz, scales, scale_exp, nb, root);
+}
+
+}  // extern "C"

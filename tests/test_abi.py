@@ -27,7 +27,8 @@ def test_header_declares_the_survey_boundary():
                      "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "pseudospectra_z",
                      "mstrsm_set_stream", "mstrsm_get_stream", "mstrsm_error_string", "mstrsm_status",
                      "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d",
-                     "tgevc_z", "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z"]:
+                     "tgevc_z", "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z",
+                     "mstrsm_comm_init", "mstrsm_comm_destroy", "trevc_z_dist", "mstrsm_workspace_size"]:
         assert required in names
 
 

@@ -33,6 +33,16 @@ def test_shard_cols_partition_and_balance():
     assert np.sum(last.astype(float) ** 2) / np.sum(np.arange(m, dtype=float) ** 2) > 0.3
 
 
+def test_library_shard_map_is_the_driver_map():
+    """libmstrsm's native multi-GPU entry (trevc_*_dist) deals columns exactly as dist.py does."""
+    import paper_1607_01477_b200 as ms
+    for m, P in [(1, 1), (37, 2), (1000, 3), (2048, 8), (16384, 8), (5000, 7)]:
+        for r in range(P):
+            assert np.array_equal(ms.dist_shard(m, P, r), pdist.shard_cols(m, P, r, 16))
+    lib = ms.load()
+    assert lib.mstrsm_dist_shard(10, 2, 2, None) == -1 and lib.mstrsm_dist_shard(-1, 1, 0, None) == -1
+
+
 def test_unpack_inverts_the_shard_layout():
     m, P, g = 50, 3, 4
     Z = torch.arange(m * m, dtype=torch.float64).reshape(m, m).t()        # column-major

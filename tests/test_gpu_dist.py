@@ -1,0 +1,45 @@
+"""GPU tests (-m gpu) of the native multi-GPU entries (trevc_*_dist over an NCCL communicator of
+the library).  Only one GPU is available to this build, so the collectives run with nranks = 1
+(broadcast, all-gather and unpack all execute); the shard map for nranks > 1 is tested on CPU
+against dist.py (tests/test_dist.py) and the multi-rank host logic with gloo."""
+import numpy as np
+import pytest
+
+from paper_1607_01477_b200 import inputs
+from tests.gpu_util import dev, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ms():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a GPU"
+    import paper_1607_01477_b200 as m
+    m.load()
+    return m
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_trevc_dist_single_rank_equals_trevc(ms, cplx):
+    import torch
+    m = 600
+    T = inputs.c5_grcar_like(m) if cplx else inputs.c2_trevc_real(m)
+    ms.comm_init(1, 0)
+    try:
+        Td = dev(T)
+        Z1, s1, e1 = ms.trevc_dist(Td, m, nb=128)
+        Z2, s2, e2 = ms.trevc(Td, nb=128)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(Z1), host(Z2))
+        assert np.array_equal(host(s1), host(s2)) and np.array_equal(host(e1), host(e2))
+        if cplx:
+            assert (host(e1) < -100).any()
+    finally:
+        ms.comm_destroy()
+
+
+def test_trevc_dist_needs_a_communicator(ms):
+    T = dev(inputs.c3_trevc_complex(64))
+    with pytest.raises(ms.MstrsmError):
+        ms.trevc_dist(T, 64, nb=32)
