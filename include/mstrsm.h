@@ -288,6 +288,16 @@ int     mstrsm_comm_destroy(void);
 int64_t mstrsm_dist_shard(int64_t m, int nranks, int rank, int64_t *cols_out);
 int trevc_d_dist(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,
                  int32_t *scale_exp, int nb, int root);
+/* Dense right-hand sides sharded by column (shifts / B / scales / scale_exp hold this rank's n
+ * columns): U (device) is read on `root` only and its upper triangle broadcast; every rank then
+ * runs mstrsm_*_ex on its own columns (no gather).  Collective.  Arguments as mstrsm_*_ex (no
+ * row_end), root last.                                                                       */
+int mstrsm_d_dist(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
+                  int64_t shift_stride, double *B, int64_t ldb, int64_t n, double *scales,
+                  int32_t *scale_exp, int nb, int root);
+int mstrsm_z_dist(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
+                  const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb,
+                  int64_t n, double *scales, int32_t *scale_exp, int nb, int root);
 int trevc_z_dist(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, mstrsm_dcomplex *Z, int64_t ldz,
                  double *scales, int32_t *scale_exp, int nb, int root);
 

@@ -26,7 +26,7 @@ __all__ = [
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "trevc_z_host_batch", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
-    "spectral_portrait", "comm_init", "comm_destroy", "dist_shard", "trevc_dist", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
+    "spectral_portrait", "comm_init", "comm_destroy", "dist_shard", "trevc_dist", "solve_dist", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
@@ -65,6 +65,8 @@ def load():
         "mstrsm_comm_init": [c_int, c_int, P],
         "mstrsm_comm_destroy": [],
         "trevc_d_dist": [P, c_i64, c_i64, P, c_i64, P, P, c_int, c_int],
+        "mstrsm_d_dist": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int, c_int],
+        "mstrsm_z_dist": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, c_int, c_int],
         "trevc_z_dist": [P, c_i64, c_i64, P, c_i64, P, P, c_int, c_int],
         "mstrsm_d_ex_ws": [c_int, c_int, P, c_i64, c_i64, P, c_i64, P, c_i64, c_i64, P, P, P, c_int, P,
                            ctypes.c_size_t],
@@ -295,6 +297,20 @@ def trevc_dist(T, m: int, *, nb: int = 64, root: int = 0):
     name = "trevc_z_dist" if dtype == torch.complex128 else "trevc_d_dist"
     _call(name, _ptr(T), _ld(T) if T is not None else 1, m, _ptr(Z), _ld(Z), _ptr(scales), _ptr(exps), nb, root)
     return Z, scales, exps
+
+
+def solve_dist(U, shifts, B, m: int, *, safe: bool = True, op: str = "N", nb: int = 64, root: int = 0):
+    """This rank's columns of a multi-shift solve over the library communicator (U read on root,
+    its upper triangle broadcast); B (m x n_local, column-major CUDA) solved in place.  Returns
+    (B, scales, scale_exp)."""
+    torch = _torch()
+    n = B.shape[1]
+    scales = torch.empty(n, dtype=torch.float64, device=B.device)
+    exps = torch.empty(n, dtype=torch.int32, device=B.device)
+    name = "mstrsm_z_dist" if B.dtype == torch.complex128 else "mstrsm_d_dist"
+    _call(name, 1 if safe else 0, 0 if op == "N" else 1, _ptr(U), _ld(U) if U is not None else 1, m, _ptr(shifts), 1,
+          _ptr(B), _ld(B), n, _ptr(scales), _ptr(exps), nb, root)
+    return B, scales, exps
 
 
 def mstrsm_workspace_size(m: int, n: int, nb: int, is_complex: bool, safe: bool) -> int:

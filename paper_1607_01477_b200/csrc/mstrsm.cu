@@ -1334,6 +1334,76 @@ __global__ void gather_dist_kernel(const T *__restrict__ Za, int64_t m, const in
         }                                                                                     \
     } while (0)
 
+// The upper triangle of root's T on every rank: packed by 128-column panels (rows 0 .. panel
+// end), one ncclBroadcast, unpacked into a workspace copy on the other ranks.  *pack / *Tw are
+// stream-ordered allocations the caller frees.
+template <typename T>
+int replicate_upper(const T *Tm, int64_t ldt, int64_t m, int root, T **pack_out, T **Tw_out, const T **Tuse,
+                    int64_t *lduse) {
+    const size_t es = sizeof(T), ndbl = es / 8;
+    const int r = g_comm_r;
+    size_t packed = 0;
+    for (int64_t c0 = 0; c0 < m; c0 += 128) {
+        const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+        packed += size_t(c1) * size_t(c1 - c0);
+    }
+    T *pack = nullptr, *Tw = nullptr;
+    CK(cudaMallocAsync(&pack, packed * es, g_stream));
+    *pack_out = pack;
+    if (r == root) {
+        size_t off = 0;
+        for (int64_t c0 = 0; c0 < m; c0 += 128) {
+            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+            CK(cudaMemcpy2DAsync(pack + off, c1 * es, Tm + c0 * ldt, ldt * es, c1 * es, c1 - c0,
+                                 cudaMemcpyDeviceToDevice, g_stream));
+            off += size_t(c1) * size_t(c1 - c0);
+        }
+    }
+    NCK(ncclBroadcast(pack, pack, packed * ndbl, ncclDouble, root, g_comm, g_stream));
+    *Tuse = Tm;
+    *lduse = ldt;
+    if (r != root) {
+        CK(cudaMallocAsync(&Tw, size_t(m) * m * es, g_stream));
+        *Tw_out = Tw;
+        size_t off = 0;
+        for (int64_t c0 = 0; c0 < m; c0 += 128) {
+            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+            CK(cudaMemcpy2DAsync(Tw + c0 * m, m * es, pack + off, c1 * es, c1 * es, c1 - c0,
+                                 cudaMemcpyDeviceToDevice, g_stream));
+            off += size_t(c1) * size_t(c1 - c0);
+        }
+        *Tuse = Tw;
+        *lduse = m;
+    }
+    return 0;
+}
+
+// Dense right-hand sides (SURVEY §8b mstrsm_z_safe_dist): U from root, every rank solves its own
+// columns of B (its shard of shifts); no gather.
+template <typename T>
+int ex_dist_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride, T *B,
+                 int64_t ldb, int64_t n, double *scales, int32_t *scale_exp, int nb, int root) {
+    if (!g_comm) {
+        snprintf(g_errmsg, sizeof(g_errmsg), "mstrsm_*_dist: no communicator (mstrsm_comm_init)");
+        return 3;
+    }
+    if (root < 0 || root >= g_comm_n) return -15;
+    if (m < 0) return -5;
+    if (g_comm_r == root && ldu < std::max<int64_t>(1, m)) return -4;
+    if (m == 0) return 0;
+    if (g_comm_r == root && !U) return -3;
+    if (int rc = ensure_init()) return rc;
+    T *pack = nullptr, *Tw = nullptr;
+    const T *Uuse = U;
+    int64_t lduse = ldu;
+    int rc = replicate_upper<T>(U, ldu, m, root, &pack, &Tw, &Uuse, &lduse);
+    if (!rc)      // the collective is done on every rank; an empty local shard just returns
+        rc = mstrsm_ex_impl<T>(safe, op, Uuse, lduse, m, shifts, sstride, B, ldb, n, nullptr, scales, scale_exp, nb);
+    if (pack) cudaFreeAsync(pack, g_stream);
+    if (Tw) cudaFreeAsync(Tw, g_stream);
+    return rc;
+}
+
 template <typename T>
 int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, double *scales, int32_t *scale_exp,
                     int nb, int root) {
@@ -1352,38 +1422,10 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     if (!Z) return -4;
     if (int rc = ensure_init()) return rc;
     const size_t es = sizeof(T), ndbl = es / 8;
-    // 1. the upper triangle from root, packed by 128-column panels (rows 0 .. panel end)
-    size_t packed = 0;
-    for (int64_t c0 = 0; c0 < m; c0 += 128) {
-        const int64_t c1 = std::min<int64_t>(m, c0 + 128);
-        packed += size_t(c1) * size_t(c1 - c0);
-    }
     T *pack = nullptr, *Tw = nullptr;
-    CK(cudaMallocAsync(&pack, packed * es, g_stream));
-    if (r == root) {
-        size_t off = 0;
-        for (int64_t c0 = 0; c0 < m; c0 += 128) {
-            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
-            CK(cudaMemcpy2DAsync(pack + off, c1 * es, Tm + c0 * ldt, ldt * es, c1 * es, c1 - c0,
-                                 cudaMemcpyDeviceToDevice, g_stream));
-            off += size_t(c1) * size_t(c1 - c0);
-        }
-    }
-    NCK(ncclBroadcast(pack, pack, packed * ndbl, ncclDouble, root, g_comm, g_stream));
     const T *Tuse = Tm;
     int64_t lduse = ldt;
-    if (r != root) {
-        CK(cudaMallocAsync(&Tw, size_t(m) * m * es, g_stream));
-        size_t off = 0;
-        for (int64_t c0 = 0; c0 < m; c0 += 128) {
-            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
-            CK(cudaMemcpy2DAsync(Tw + c0 * m, m * es, pack + off, c1 * es, c1 * es, c1 - c0,
-                                 cudaMemcpyDeviceToDevice, g_stream));
-            off += size_t(c1) * size_t(c1 - c0);
-        }
-        Tuse = Tw;
-        lduse = m;
-    }
+    if (int rc = replicate_upper<T>(Tm, ldt, m, root, &pack, &Tw, &Tuse, &lduse)) return rc;
     // 2. this rank's shard, written into the all-gather send buffer (m x mc, padded)
     int64_t mc = 0;
     for (int q = 0; q < P; q++) mc = std::max(mc, shard_of(m, P, q, kShardGroup, nullptr));
@@ -1468,6 +1510,19 @@ int mstrsm_comm_destroy(void) {
 int64_t mstrsm_dist_shard(int64_t m, int nranks, int rank, int64_t *cols_out) {
     if (m < 0 || nranks < 1 || rank < 0 || rank >= nranks) return -1;
     return shard_of(m, nranks, rank, kShardGroup, cols_out);
+}
+
+int mstrsm_d_dist(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
+                  int64_t shift_stride, double *B, int64_t ldb, int64_t n, double *scales, int32_t *scale_exp,
+                  int nb, int root) {
+    return ex_dist_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, scales, scale_exp, nb,
+                                root);
+}
+int mstrsm_z_dist(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
+                  const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n,
+                  double *scales, int32_t *scale_exp, int nb, int root) {
+    return ex_dist_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride,
+                              (cplx *)B, ldb, n, scales, scale_exp, nb, root);
 }
 
 int trevc_d_dist(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,

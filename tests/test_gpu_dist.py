@@ -43,3 +43,24 @@ def test_trevc_dist_needs_a_communicator(ms):
     T = dev(inputs.c3_trevc_complex(64))
     with pytest.raises(ms.MstrsmError):
         ms.trevc_dist(T, 64, nb=32)
+
+
+@pytest.mark.parametrize("op", ["N", "C"])
+def test_solve_dist_single_rank_equals_solve(ms, op):
+    import torch
+    m, n = 300, 90
+    rng = np.random.default_rng(8)
+    U = np.triu(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))) * 3.0
+    U[np.arange(m), np.arange(m)] = rng.uniform(-1e-2, 1e-2, m)
+    s = inputs.random_shifts(n, True, 9, radius=1e-2)
+    B = inputs.random_rhs(m, n, True, 10)
+    ms.comm_init(1, 0)
+    try:
+        Ud, sd = dev(np.asfortranarray(U)), dev(np.ascontiguousarray(s))
+        X1, _, e1 = ms.solve_dist(Ud, sd, dev(B), m, op=op, nb=64)
+        X2, _, e2 = ms.solve(Ud, sd, dev(B), safe=True, op=op, nb=64)
+        torch.cuda.synchronize()
+        assert (host(e2) < 0).any()
+        assert np.array_equal(host(X1), host(X2)) and np.array_equal(host(e1), host(e2))
+    finally:
+        ms.comm_destroy()
