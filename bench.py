@@ -142,6 +142,41 @@ def ncu_traffic(kernel: str = "gemm_ws_kernel"):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cublas_fp64_ceiling(n: int = 8192):
+    """SURVEY §8d.5's third peak figure: cuBLAS DGEMM / ZGEMM via torch.matmul at n^3, best of 3
+    (context for the roofline; the denominator stays the DMMA microbenchmark)."""
+    import torch
+    out = {}
+    for name, dt, fl in (("dgemm", torch.float64, 2.0), ("zgemm", torch.complex128, 8.0)):
+        a = torch.randn(n, n, dtype=dt, device="cuda")
+        b = torch.randn(n, n, dtype=dt, device="cuda")
+        torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name + "_tflops"] = fl * n ** 3 / (best * 1e-3) / 1e12
+        del a, b
+    torch.cuda.empty_cache()
+    out["note"] = f"torch.matmul {n}^3 (cuBLAS), best of 3; zgemm counted at 8 n^3 (4 real products)"
+    return out
+
+
 def cpu_baseline(T: np.ndarray, cfg: dict, budget_s: float = 15.0):
     """The oracle, as it stands, on a bounded sample of the same workload's columns (the oracle
     is never tuned for this).  Columns are independent, so the sample is exact per column."""
@@ -169,6 +204,7 @@ def cpu_baseline(T: np.ndarray, cfg: dict, budget_s: float = 15.0):
     dt = time.perf_counter() - t0
     fl = algorithmic_flops_cols(cols, cplx)
     return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{len(cols)} of {m} eigenvectors (evenly spaced k in [1, {m - 1}], "
                       f"{fl:.3e} algorithmic flops) in {dt:.1f} s",
             "eigvecs_per_s_sample": len(cols) / dt, "seconds": dt}
@@ -204,6 +240,7 @@ def run_reference(args, cfgname):
                        "sample_per_step": f"{len(cols)} evenly spaced eigenvectors"},
             "eigvecs_per_s": len(cols) / dt,
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"{len(cols)} of {m} eigenvectors per step"},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -252,6 +289,7 @@ def run_cuda(args, cfgname):
 
     # ---- FP64 roofline denominators (measured on this GPU, before timing)
     dmma_tf, dfma_tf = ms.fp64_peak(100.0)
+    cublas = cublas_fp64_ceiling() if rank == 0 else None
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -321,6 +359,8 @@ def run_cuda(args, cfgname):
                 "peak_source": "measured: register-resident DMMA loop on all SMs (mstrsm_fp64_peak), "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "dfma_peak": dfma_tf,
+                "derived_peak_tflops_at_max_clock": 148 * 64 * 2 * 1.965e9 / 1e12,
+                "cublas_fp64": cublas,
                 "gemm_launches": g_n, "gemm_ms_per_step": g_ms / args.steps,
                 "gemm_share_of_step": (g_ms / args.steps) / ms_per_step,
                 "diag_ms_per_step": d_ms / args.steps, "other_ms_per_step": o_ms / args.steps,

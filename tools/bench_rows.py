@@ -28,7 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--only", default="c1,c2,c3,c4,c4d,g1,f2,f4")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c4d,g1,f2,f4,trsm")
     a = ap.parse_args()
     import torch
     import paper_1607_01477_b200 as ms
@@ -63,6 +63,26 @@ def main():
                        15 * 2 * 4.0 * 1024 ** 2 * z.shape[0], z.shape[0], "points/s",
                        "c4d: c4 with SpectralCloud deflation (tol 1e-10, at most 15 steps; SURVEY §8f f3); "
                        "gflops counts the fixed 15-step work, so it is an effective rate")
+    if "trsm" in a.only:
+        # SURVEY §8d.5 paper analogue (context only): the multi-shift solve at zero shift against
+        # cuBLAS trsm (torch.linalg.solve_triangular) on the same upper-triangular system
+        for mt, cx in ((256, False), (4096, True)):
+            rng = np.random.default_rng(77)
+            Ut = np.triu(rng.standard_normal((mt, mt)) + (1j * rng.standard_normal((mt, mt)) if cx else 0)) / np.sqrt(mt)
+            Ut[np.arange(mt), np.arange(mt)] = rng.uniform(1.0, 2.0, mt)
+            nt = 64 if mt == 256 else mt
+            Bt0 = dev(inputs.random_rhs(mt, nt, cx, 78))
+            Utd = dev(Ut)
+            zt = dev(np.zeros(nt, dtype=np.complex128 if cx else np.float64))
+            Btw = Bt0.clone()
+            nbt = 32 if mt == 256 else 128
+            fl = (4.0 if cx else 1.0) * mt * mt * nt
+            tag = f"{'z' if cx else 'd'}{mt}"
+            work[f"trsm_ours_{tag}"] = (lambda U_=Utd, z_=zt, B0=Bt0, Bw=Btw, nb_=nbt: (Bw.copy_(B0),
+                                        ms.solve(U_, z_, Bw, safe=False, nb=nb_)), fl, nt, "rhs/s",
+                                        f"multi-shift solve at zero shift (plain), {tag}, n={nt}")
+            work[f"trsm_cublas_{tag}"] = (lambda U_=Utd, B0=Bt0: torch.linalg.solve_triangular(U_, B0, upper=True),
+                                          fl, nt, "rhs/s", f"cuBLAS trsm (torch.linalg.solve_triangular), {tag}, n={nt}")
     if "f4" in a.only:
         m4 = 4096
         rng = np.random.default_rng(44)
