@@ -275,10 +275,20 @@ def run_cuda(args, cfgname):
     scales = torch.empty(ncols, dtype=torch.float64, device="cuda")
     exps = torch.empty(ncols, dtype=torch.int32, device="cuda")
 
+    solve_evs = []          # (start, end) CUDA events around the local solve of each timed step
+
     def solve_cols(T, c, out):
         fn = ms.trevc_z_cols if cplx else ms.trevc_d_cols
+        if timing["on"]:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
         fn(T, m, m, c, len(c), out, m, scales, exps, nb)
+        if timing["on"]:
+            e1.record(stream)
+            solve_evs.append((e0, e1))
         return exps
+
+    timing = {"on": False}
 
     last = {}
 
@@ -302,6 +312,7 @@ def run_cuda(args, cfgname):
     ms.mstrsm_profile(1)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
+    timing["on"] = True
     with sampler:
         t_wall0 = time.perf_counter()
         for i in range(args.steps):
@@ -310,9 +321,11 @@ def run_cuda(args, cfgname):
             evs[i][1].record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
+    timing["on"] = False
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
+    solve_ms = float(np.sum([a.elapsed_time(b) for a, b in solve_evs]))
     launches = ms.launch_count(0)
     g_ms, g_n, g_fl = ms.mstrsm_profile_read(0)
     d_ms, d_n, d_fl = ms.mstrsm_profile_read(1)
@@ -320,9 +333,9 @@ def run_cuda(args, cfgname):
     ms.mstrsm_profile(0)
     total_ms = float(np.sum(step_ms))
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, solve_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms, solve_ms = float(t[0].item()), float(t[1].item())
     ms_per_step = total_ms / args.steps
 
     # correctness spot check of the timed output (cheap, outside the timed region)
@@ -378,7 +391,10 @@ def run_cuda(args, cfgname):
             "pct_fp64_peak": 100.0 * value / 1e3 / (peak_tf * ws) if peak_tf else None,
             "gflops_nominal_m2n": nominal_flops(m, m, cplx) / (ms_per_step * 1e-3) / 1e9,
             "roofline": roofline, "clocks": clocks, "gpu_launches": launches,
-            "wall_s_timed": t_wall, "output_finite": ok_finite}
+            "wall_s_timed": t_wall, "output_finite": ok_finite,
+            "solve_only_ms_per_step": solve_ms / args.steps,
+            "solve_only_note": "the local trevc_*_cols call alone (CUDA events, max over ranks); ms_per_step "
+                               "is end to end: broadcast + solve + all-gather + unpack (SURVEY §8d.5)"}
 
     if ws == 1 and cplx and not args.no_e2e:
         line["e2e"] = e2e_host(ms, T_host, m, nb, args)
