@@ -113,7 +113,10 @@ def test_gpu_c1_plain_and_safe(ms):
 
 
 # ------------------------------------------------------------------------------- ragged shapes
-SHAPES = [(1, 1, 8), (7, 3, 8), (100, 37, 32), (129, 64, 64), (333, 130, 64), (300, 70, 128), (257, 129, 128)]
+# odd n_b: ragged k-tiles in every update and, for op C, odd block offsets (the 3M kernel's
+# sum-plane alignment fails and the register-sum kernel takes over)
+SHAPES = [(1, 1, 8), (7, 3, 8), (100, 37, 32), (129, 64, 64), (333, 130, 64), (300, 70, 128), (257, 129, 128),
+          (200, 50, 7), (97, 40, 1), (150, 33, 13)]
 
 
 @pytest.mark.parametrize("m,n,nb", SHAPES)
