@@ -217,6 +217,57 @@ __global__ void init_trevc_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t
     }
 }
 
+// a.1 + a.2 (column part) + the 3M sum plane fused for TriangEig over all m columns (column q =
+// eigenvector q): one read of T(0:k, k) per column gives cnl / pcol (norm_cols_n_kernel), Z and
+// G / rowend / shifts / e (init_trevc_kernel; G = max(cnl, pcol) = max_{l<k} |T(l,k)|) and, when
+// P is non-null, the plane P(l,k) = Re + Im (presum_kernel) -- |T(l,k)| evaluated once.
+template <typename T>
+__global__ void trevc_prepass_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t m, int nb,
+                                     double *__restrict__ cnl, double *__restrict__ pcol,
+                                     T *__restrict__ Z, int64_t ldz, T *__restrict__ shifts,
+                                     int64_t *__restrict__ rowend, double *__restrict__ G, int *__restrict__ e,
+                                     double *__restrict__ P, int64_t ldp, int *__restrict__ nonfinite) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w; k < m; k += nw) {
+        const int64_t b = (m - 1 - k) / nb;
+        const Blk bl = block_rows(0, m, nb, b);
+        const T *tc = Tm + k * ldt;
+        T *z = Z + k * ldz;
+        double c = 0.0, p = 0.0;
+        bool bad = false;
+        for (int64_t l = lane; l < m; l += 32) {
+            if (l < k) {
+                const T v = tc[l];
+                const double a = S<T>::mod(v);
+                bad |= !(a <= 1.7976931348623157e308);
+                if (l < bl.lo) p = fmax(p, a);
+                else c = fmax(c, a);
+                z[l] = S<T>::neg(v);
+                if constexpr (S<T>::cplx_) {
+                    if (P) P[l + k * ldp] = __dadd_rn(v.x, v.y);
+                }
+            } else {
+                z[l] = S<T>::zero();
+            }
+        }
+        c = warp_max(c);
+        p = warp_max(p);
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            const T d = tc[k];
+            cnl[k] = c;
+            pcol[k] = p;
+            shifts[k] = d;
+            rowend[k] = k;
+            G[k] = fmax(c, p);
+            e[k] = 0;
+            if (bad || !(S<T>::mod(d) <= 1.7976931348623157e308)) atomicExch(nonfinite, 1);
+        }
+    }
+}
+
 // a.1 init for GeneralizedTriangEig (Alg. 9).  Column q holds eigenvector k = q:
 //   lambda_q = T(k,k) / S(k,k);  Z(l,q) = S(l,k) lambda_q - T(l,k) for l < k, 0 for l >= k;
 //   G_q = max_{l<k} |Z(l,q)|;  row_end_q = k.

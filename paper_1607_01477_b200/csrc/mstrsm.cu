@@ -98,12 +98,14 @@ int occupancy(K kern, int threads, size_t smem) {
 
 // ---------------------------------------------------------------- norm pass (a.2)
 template <typename T>
-int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w) {
+int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w, bool cols_done = false) {
     int64_t nblk = cdiv(m, nb);
     if (op == 0) {
         int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
-        norm_cols_n_kernel<T><<<blocks, 256, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
-        CK_LAUNCH("norm_cols_n_kernel");
+        if (!cols_done) {       // (trevc's fused prepass has produced cnl / pcol already)
+            norm_cols_n_kernel<T><<<blocks, 256, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
+            CK_LAUNCH("norm_cols_n_kernel");
+        }
         panel_sum_kernel<<<int(cdiv(nblk, 128)), 128, 0, g_stream>>>(0, m, nb, nblk, w.part, w.P);
         CK_LAUNCH("panel_sum_kernel");
         int64_t nch = cdiv(m, kRowsumChunk);
@@ -195,7 +197,7 @@ struct SumPlanes {
     ~SumPlanes() { ws_free(U, st); ws_free(X, st); }
 };
 template <typename T>
-int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, int64_t n, int nb) {
+int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, int64_t n, int nb, bool fill = true) {
     if constexpr (!S<T>::cplx_) return 0;
     else {
         if (gemm_variant() != 0 || m == 0 || !gemm_presum_enabled()) return 0;
@@ -206,6 +208,7 @@ int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, i
         sp.ldx = (nb + 1) & ~1;
         CK(ws_malloc((void **)&sp.U, size_t(sp.ldu) * m * 8));
         CK(ws_malloc((void **)&sp.X, size_t(sp.ldx) * std::max<int64_t>(n, 1) * 8));
+        if (!fill) return 0;                        // the caller's kernel writes the plane
         int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
         presum_kernel<<<blocks, 256, 0, g_stream>>>(U, ldu, m, sp.U, sp.ldu, op == 0 ? 1.0 : -1.0);
         CK_LAUNCH("presum_kernel");
@@ -315,14 +318,25 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
         CK(cudaMemcpyAsync(cols_dev, cols.data(), ncols * 8, cudaMemcpyHostToDevice, g_stream));
     }
     T *sh = static_cast<T *>(w.shifts);
-    if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w)) return rc;
-    int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
-    init_trevc_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, cols_dev, ncols, Z, ldz, sh,
-                                                        w.rowend, w.G, w.e, g_flag);
-    CK_LAUNCH("init_trevc_kernel");
-    // row_end_q = cols[q] (the P:503-508 shortcut), sorted ascending
     SumPlanes sp;
-    if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb)) return rc;
+    const bool all_cols = ncols == m && cols.back() == m - 1;      // strictly increasing: the identity
+    if (all_cols) {
+        // one pass over T for the column norms, Z / G / row_end / shifts and the 3M sum plane
+        if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb, /*fill=*/false)) return rc;
+        int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
+        trevc_prepass_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, nb, w.cnl, w.part, Z, ldz, sh, w.rowend,
+                                                               w.G, w.e, sp.U, sp.ldu, g_flag);
+        CK_LAUNCH("trevc_prepass_kernel");
+        if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w, /*cols_done=*/true)) return rc;
+    } else {
+        if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w)) return rc;
+        int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
+        init_trevc_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, cols_dev, ncols, Z, ldz, sh,
+                                                            w.rowend, w.G, w.e, g_flag);
+        CK_LAUNCH("init_trevc_kernel");
+        // row_end_q = cols[q] (the P:503-508 shortcut), sorted ascending
+        if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb)) return rc;
+    }
     int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
     if (cols_dev) cudaFreeAsync(cols_dev, g_stream);
