@@ -60,13 +60,21 @@ int launch_diag(const DiagArgs<T> &a, int nb) {
     // Whole passes of the grid over the columns: a pass of the RPL = 16 layout takes about 1.2x
     // one of the RPL = 8 layout (c5 launch list, profiles/r01), so pick the cheaper pass count.
     auto passes = [&](int lpc, int rpl) {
-        const int64_t per_pass = int64_t(g_num_sms) * (rpl >= 16 ? DiagThreads<T, 16>::value : DiagThreads<T, 8>::value) / 32 * (32 / lpc);
+        const int64_t per_pass = int64_t(g_num_sms) * (rpl >= 16 ? DiagThreads<T, 16>::value : DiagThreads<T, 8>::value) / 32 * (32 / lpc);   // (RPL 4 uses RPL 8's CTA size)
         return cdiv(a.ncols, per_pass);
     };
     auto few = [&](int lpc16) { return 10 * passes(2 * lpc16, 8) < 12 * passes(lpc16, 16); };
     if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP, false>(a);
     if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP, false>(a);
     if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 4, 16, SAFE, OP, false>(a);
+#ifndef MSTRSM_DIAG_RPL4_COST
+#define MSTRSM_DIAG_RPL4_COST 7      // pass cost of the RPL = 4 layout in tenths of an RPL = 8 pass
+#endif
+    // very few columns (the first blocks of TriangEig, every block of a multi-GPU shard): a whole
+    // warp per column, 4 rows per lane -- the shortest per-row chain
+    if (MSTRSM_DIAG_RPL4_COST * passes(32, 4) < 10 * passes(16, 8) &&
+        MSTRSM_DIAG_RPL4_COST * passes(32, 4) < 12 * passes(8, 16))
+        return launch_diag_pair<T, 32, 4, SAFE, OP, false>(a);
     return few(8) ? launch_diag_pair<T, 16, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 8, 16, SAFE, OP, false>(a);
 }
 
