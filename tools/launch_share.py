@@ -2,7 +2,7 @@
 
     python tools/launch_share.py <launches.csv> "<command description>" > profiles/r01/launch_share_<tag>.txt
 
-Steps are delimited by the norm pass (norm_cols_n_kernel) launches; the last step is reported (libmstrsm kernels only)."""
+Steps are delimited by the first kernel of a TriangEig (trevc_prepass_kernel, or the norm pass); the last step is reported (libmstrsm kernels only)."""
 import collections
 import csv
 import sys
@@ -18,8 +18,11 @@ def main():
         if len(r) < len(h) or r[I("Metric Name")] != "gpu__time_duration.sum":
             continue
         launches.append((r[I("Kernel Name")].split("(")[0], float(r[I("Metric Value")].replace(",", "")) / 1e6))
-    begins = [i for i, (n, _) in enumerate(launches) if "norm_cols_n_kernel" in n] or \
-        [i for i, (n, _) in enumerate(launches) if "init_trevc_kernel" in n]
+    begins = []
+    for marker in ("trevc_prepass_kernel", "norm_cols_n_kernel", "init_trevc_kernel"):
+        begins = [i for i, (n, _) in enumerate(launches) if marker in n]
+        if begins:
+            break
     step = [x for x in launches[begins[-1]:] if "mstrsm::" in x[0]]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for n, v in step:
