@@ -312,34 +312,30 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
     if (int rc = ensure_init()) return rc;
     Work w;
     if (int rc = alloc_work<T>(w, m, ncols, nb, true, true)) return rc;
-    int64_t *cols_dev = nullptr;
-    if (cols_host) {
-        CK(cudaMallocAsync(&cols_dev, ncols * 8, g_stream));
-        CK(cudaMemcpyAsync(cols_dev, cols.data(), ncols * 8, cudaMemcpyHostToDevice, g_stream));
-    }
     T *sh = static_cast<T *>(w.shifts);
     SumPlanes sp;
+    // one pass over T for the column norms (all columns), Z / G / row_end / shifts of the requested
+    // columns and the 3M sum plane
     const bool all_cols = ncols == m && cols.back() == m - 1;      // strictly increasing: the identity
-    if (all_cols) {
-        // one pass over T for the column norms, Z / G / row_end / shifts and the 3M sum plane
-        if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb, /*fill=*/false)) return rc;
+    int *qof = nullptr;
+    std::vector<int> qh;
+    if (!all_cols) {                    // eigenvector k -> column q of Z (or -1)
+        qh.assign(m, -1);
+        for (int64_t q = 0; q < ncols; q++) qh[cols[q]] = int(q);
+        CK(cudaMallocAsync(&qof, size_t(m) * 4, g_stream));
+        CK(cudaMemcpyAsync(qof, qh.data(), size_t(m) * 4, cudaMemcpyHostToDevice, g_stream));
+    }
+    if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb, /*fill=*/false)) return rc;
+    {
         int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
         trevc_prepass_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, nb, w.cnl, w.part, Z, ldz, sh, w.rowend,
-                                                               w.G, w.e, sp.U, sp.ldu, g_flag);
+                                                               w.G, w.e, sp.U, sp.ldu, g_flag, qof);
         CK_LAUNCH("trevc_prepass_kernel");
-        if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w, /*cols_done=*/true)) return rc;
-    } else {
-        if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w)) return rc;
-        int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
-        init_trevc_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, cols_dev, ncols, Z, ldz, sh,
-                                                            w.rowend, w.G, w.e, g_flag);
-        CK_LAUNCH("init_trevc_kernel");
-        // row_end_q = cols[q] (the P:503-508 shortcut), sorted ascending
-        if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb)) return rc;
     }
+    if (qof) cudaFreeAsync(qof, g_stream);
+    if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w, /*cols_done=*/true)) return rc;
     int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
-    if (cols_dev) cudaFreeAsync(cols_dev, g_stream);
     return rc;
 }
 
