@@ -269,14 +269,15 @@ __device__ __forceinline__ void diag_subst(T (&y)[RPL], PivF pivot, const Acc &u
 #pragma unroll kDiagRrUnroll
         for (int rr = rr_hi; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
+            // rows sc >= nrow (past this column's row end) need no masking: their y starts at 0,
+            // nothing updates them before their turn (they are solved first) and their pivot is 1,
+            // so x_l = 0 there and every update below is exact
             const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);          // P:82 / P:297
-            const bool in = sc < nrow;
-            const T xr = in ? xl : ST::zero();
             const int col = (sc * (sc - 1)) / 2;
-            const T upd = ST::fnms(y[t], xr, ua(col + rl + LPC * t));
-            y[t] = rl < rr ? upd : ((rl == rr && in) ? xl : y[t]);
+            const T upd = ST::fnms(y[t], xl, ua(col + rl + LPC * t));
+            y[t] = rl < rr ? upd : (rl == rr ? xl : y[t]);
 #pragma unroll
-            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xl, ua(col + rl + LPC * t2));
         }
     }
 }
@@ -338,14 +339,12 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
 #pragma unroll kDiagRrUnroll
         for (int rr = rr_hi; rr >= 0; rr--) {
             const int sc = t * LPC + rr;
-            const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);
-            const bool in = sc < nrow;
-            const T xr = in ? xl : ST::zero();
+            const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);          // P:297 (x_l = 0 past row end)
             const int col = (sc * (sc - 1)) / 2;
-            const T upd = ST::fnms(y[t], xr, ua(col + rl + LPC * t));      // (index in the padded triangle)
-            y[t] = rl < rr ? upd : ((rl == rr && in) ? xl : y[t]);
+            const T upd = ST::fnms(y[t], xl, ua(col + rl + LPC * t));      // (index in the padded triangle)
+            y[t] = rl < rr ? upd : (rl == rr ? xl : y[t]);
 #pragma unroll
-            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xr, ua(col + rl + LPC * t2));
+            for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xl, ua(col + rl + LPC * t2));
             {                                                              // replay row sc + LAG
                 const bool prev = rr + LAG >= LPC;
                 const int src = (rr + LAG) & (LPC - 1);
