@@ -22,11 +22,12 @@ int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
     const size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T), GEN));
     int occ1 = occupancy(kern, kMaxThreads, smem);
     int64_t groups = cdiv(ncols_max, G);
-    int64_t wpc = cdiv(groups, int64_t(g_num_sms) * std::max(occ1, 1));
+    const int64_t sms = g_cta_cap > 0 ? g_cta_cap : g_num_sms;
+    int64_t wpc = cdiv(groups, sms * std::max(occ1, 1));
     wpc = std::max<int64_t>(1, std::min<int64_t>(kMaxThreads / 32, wpc));
     const int threads = int(wpc * 32);
     int occ = occupancy(kern, threads, smem);
-    int grid = int(std::min<int64_t>(cdiv(groups, wpc), int64_t(occ) * g_num_sms));
+    int grid = int(std::min<int64_t>(cdiv(groups, wpc), int64_t(occ) * sms));
     if (grid < 1) grid = 1;
     double fl = FB ? 0.0 : double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
     ProfScope ps(PK_DIAG, fl);
@@ -67,6 +68,7 @@ int launch_diag(const DiagArgs<T> &a, int nb) {
     if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP, false>(a);
     if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP, false>(a);
     if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 4, 16, SAFE, OP, false>(a);
+    if (g_cta_cap > 0) return launch_diag_pair<T, 8, 16, SAFE, OP, false>(a);   // look-ahead: densest layout
 #ifndef MSTRSM_DIAG_RPL4_COST
 #define MSTRSM_DIAG_RPL4_COST 7      // pass cost of the RPL = 4 layout in tenths of an RPL = 8 pass
 #endif

@@ -116,7 +116,7 @@ int launch_gemm(const GemmArgs<T> &g) {
                     attrq = true;
                 }
                 const int64_t tm = cdiv(g.M, k3qBM), tn = cdiv(g.N, k3qBN), nt = tm * tn;
-                const int grid = int(std::min<int64_t>(nt, g_num_sms));
+                const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
                 ProfScope ps(PK_GEMM, flops);
                 kq<<<grid, k3qThreads, k3qSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs);
                 CK_LAUNCH("gemm_ws3q_kernel");
@@ -129,7 +129,7 @@ int launch_gemm(const GemmArgs<T> &g) {
                 attrp = true;
             }
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
-            const int grid = int(std::min<int64_t>(nt, g_num_sms));
+            const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
             ProfScope ps(PK_GEMM, flops);
             kern<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs);
             CK_LAUNCH("gemm_ws3p_kernel");
@@ -143,7 +143,7 @@ int launch_gemm(const GemmArgs<T> &g) {
                 attr3 = true;
             }
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
-            const int grid = int(std::min<int64_t>(nt, g_num_sms));
+            const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
             ProfScope ps(PK_GEMM, flops);
             kern<<<grid, kWsThreads, k3mSmemBytes, g_stream>>>(g, int(tm), int(nt));
             CK_LAUNCH("gemm_ws3m_kernel");
@@ -158,7 +158,7 @@ int launch_gemm(const GemmArgs<T> &g) {
         attr_set = true;
     }
     const int64_t ntiles = tiles_m * tiles_n;
-    const int grid = int(std::min<int64_t>(ntiles, g_num_sms));
+    const int grid = int(std::min<int64_t>(ntiles, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
     ProfScope ps(PK_GEMM, flops);
     kern<<<grid, kWsThreads, smem, g_stream>>>(g, int(tiles_m), int(ntiles));
     CK_LAUNCH("gemm_ws_kernel");

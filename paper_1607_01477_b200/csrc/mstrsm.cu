@@ -58,7 +58,7 @@ void ws_free(void *p, cudaStream_t st) {
 struct Work {
     void *base = nullptr;
     double *cnl = nullptr, *part = nullptr, *P = nullptr, *delta = nullptr, *G = nullptr;
-    int *e = nullptr, *dblk = nullptr, *Etab = nullptr;
+    int *e = nullptr, *dblk = nullptr, *dblk2 = nullptr, *Etab = nullptr;
     int *fb_list = nullptr, *fb_count = nullptr;   // diag fallback: column list, count per block
     int64_t *rowend = nullptr;
     void *shifts = nullptr;            // trevc: gathered diag(T)
@@ -72,7 +72,7 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     size_t o_cnl = take(m * 8), o_part = take(m * 8), o_P = take(std::max<int64_t>(nblk, 1) * 8),
-           o_delta = take(16), o_G = take(n * 8), o_e = take(n * 4), o_d = take(n * 4),
+           o_delta = take(16), o_G = take(n * 8), o_e = take(n * 4), o_d = take(n * 4), o_d2 = take(n * 4),
            o_E = take(std::max<int64_t>(nblk, 1) * n * 4), o_r = take(need_rowend ? n * 8 : 0),
            o_fl = take(n * 4), o_fc = take(std::max<int64_t>(nblk, 1) * 4),
            o_s = take(need_shifts ? n * sizeof(T) : 0);
@@ -82,7 +82,7 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
     char *b = static_cast<char *>(w.base);
     w.cnl = (double *)(b + o_cnl); w.part = (double *)(b + o_part); w.P = (double *)(b + o_P);
     w.delta = (double *)(b + o_delta); w.G = (double *)(b + o_G); w.e = (int *)(b + o_e);
-    w.dblk = (int *)(b + o_d); w.Etab = (int *)(b + o_E);
+    w.dblk = (int *)(b + o_d); w.dblk2 = (int *)(b + o_d2); w.Etab = (int *)(b + o_E);
     w.fb_list = (int *)(b + o_fl); w.fb_count = (int *)(b + o_fc);
     w.rowend = need_rowend ? (int64_t *)(b + o_r) : nullptr;
     w.shifts = need_shifts ? (void *)(b + o_s) : nullptr;
@@ -129,6 +129,27 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w, bool 
     return 0;
 }
 
+// ---------------------------------------------------------------- look-ahead (op N, safe)
+// Look-ahead (default; MSTRSM_LOOKAHEAD=0 disables): block b's update is split into its top n_b rows (the next diagonal block,
+// on the library stream) and the rest (on a side stream, on fewer SMs), so that the next
+// diagonal step -- latency-bound, and the per-block floor of a multi-GPU shard -- runs on the
+// SMs the rest leaves free.  dblk and the X+ plane are double-buffered by block
+// parity (the rest of block b still reads them while the diagonal step of b+1 writes).  A block
+// overlaps only when the model says it pays (the next diagonal pass outlasts what the rest loses
+// on the SMs it gives up); the others run as in blocked_solve.
+bool lookahead_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_LOOKAHEAD");
+        v = (e && !strcmp(e, "0")) ? 0 : 1;
+    }
+    return v == 1;
+}
+template <typename T>
+int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride, T *B, int64_t ldb,
+                     int64_t n, const int64_t *rowend_dev, const std::vector<int64_t> *rowend_sorted_host, int nb,
+                     Work &w, const double *Usum, double *Xsum, int64_t ldus, int ldxs);
+
 // ---------------------------------------------------------------- the blocked solve
 // State (G, e) must be initialised by the caller (init kernels).  active_from(b) gives the first
 // active column of block b when row ends are known on the host and sorted.
@@ -137,6 +158,11 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
                   T *B, int64_t ldb, int64_t n, const int64_t *rowend_dev,
                   const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w,
                   const double *Usum = nullptr, double *Xsum = nullptr, int64_t ldus = 0, int ldxs = 0) {
+    if constexpr (SAFE) {
+        if (op == 0 && lookahead_enabled())
+            return blocked_solve_la<T>(U, ldu, m, shifts, sstride, B, ldb, n, rowend_dev, rowend_sorted_host, nb, w,
+                                       Usum, Xsum, ldus, ldxs);
+    }
     int64_t nblk = cdiv(m, nb);
     if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));   // diag fallback counts
     for (int64_t b = 0; b < nblk; b++) {
@@ -185,6 +211,112 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         }
     }
     return 0;
+}
+
+template <typename T>
+int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride, T *B, int64_t ldb,
+                     int64_t n, const int64_t *rowend_dev, const std::vector<int64_t> *rowend_sorted_host, int nb,
+                     Work &w, const double *Usum, double *Xsum, int64_t ldus, int ldxs) {
+    static cudaStream_t side = nullptr;
+    if (!side) CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    static cudaEvent_t ev_d = nullptr, ev_rest = nullptr;
+    if (!ev_d) {
+        CK(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
+    }
+    const cudaStream_t main_st = g_stream;
+    const int64_t nblk = cdiv(m, nb);
+    CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));
+    double *Xsum2 = nullptr;
+    if (Xsum) CK(ws_malloc((void **)&Xsum2, size_t(ldxs) * std::max<int64_t>(n, 1) * 8));
+    auto c0_of = [&](const Blk &bl) -> int64_t {
+        if (!rowend_sorted_host) return 0;
+        const auto &re = *rowend_sorted_host;
+        return std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();
+    };
+    constexpr int kColsPerCta = 48;            // RPL = 16 layout: 12 warps x 4 columns
+    const int cap_max = g_num_sms / 3;
+    bool rest_pending = false;
+    int diag_cap = 0;                          // CTAs the next diagonal step may use (0: all)
+    int rc = 0;
+    for (int64_t b = 0; b < nblk && !rc; b++) {
+        const Blk bl = block_rows(0, m, nb, b);
+        const int64_t c0 = c0_of(bl), ncols = n - c0;
+        if (ncols <= 0) { diag_cap = 0; continue; }
+        const int par = int(b & 1);
+        int *dblk = par ? w.dblk2 : w.dblk;
+        double *xs = Xsum ? (par ? Xsum2 : Xsum) : nullptr;
+        DiagArgs<T> a{};
+        a.U = U; a.ldu = ldu; a.m = m; a.shifts = shifts; a.sstride = sstride;
+        a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
+        a.rowend = rowend_dev;
+        a.lo = bl.lo; a.hi = bl.hi; a.b = b;
+        a.cnl = w.cnl; a.P = w.P; a.delta = w.delta;
+        a.G = w.G; a.e = w.e; a.dblk = dblk; a.Etab = w.Etab;
+        a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
+        a.force_fb = g_diag_force_fb;
+        a.Xsum = xs; a.ldxs = ldxs;
+        if (xs && rowend_dev && !rowend_sorted_host)          // inactive columns in range: zero rows
+            CK(cudaMemsetAsync(xs + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
+        g_cta_cap = diag_cap;
+        rc = launch_diag<T, true, 0>(a, nb);
+        g_cta_cap = 0;
+        if (rc) break;
+        diag_cap = 0;
+        const int64_t M = bl.lo;
+        if (M <= 0) continue;
+        GemmArgs<T> g{};
+        g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
+        g.N = ncols; g.K = int(bl.hi - bl.lo);
+        g.a_c0 = bl.lo; g.x_r0 = bl.lo; g.col0 = c0;
+        g.X = B; g.ldx = ldb;
+        if (Usum && xs) { g.As = Usum; g.ldas = ldus; g.Xsum = xs; g.ldxs = ldxs; }
+        g.dblk = dblk;
+        // the next block: rows [bn.lo, M) of this update; how many SMs would its diagonal step need?
+        const Blk bn = block_rows(0, m, nb, b + 1);
+        const int64_t Mtop = M - bn.lo;
+        const int64_t ncols_next = n - c0_of(bn);
+        const int X = int(cdiv(std::max<int64_t>(ncols_next, 1), kColsPerCta));
+        // pays when the next diagonal step (one pass, ~100 us at n_b = 128) outlasts what the rest
+        // of this update loses on the SMs it gives up (update at ~30 TF/s executed on all SMs)
+        const double t_gemm = 6.0 * double(M) * double(ncols) * double(g.K) / 30e12;
+        const double t_diag = 100e-6 * double(bn.hi - bn.lo) / 128.0;
+        const bool overlap = Mtop < M && X <= cap_max && X < g_num_sms &&
+                             t_diag > t_gemm * double(X) / double(g_num_sms - X) + 10e-6;
+        if (!overlap) {                        // as blocked_solve
+            if (rest_pending) { CK(cudaStreamWaitEvent(main_st, ev_rest, 0)); rest_pending = false; }
+            g.M = M; g.a_r0 = 0; g.c_r0 = 0;
+            rc = launch_gemm<T, false>(g);
+            continue;
+        }
+        CK(cudaEventRecord(ev_d, main_st));                 // diagonal step b done
+        if (rest_pending) CK(cudaStreamWaitEvent(main_st, ev_rest, 0));   // rows of b+1 fully updated
+        // top: the next diagonal block's rows, on the SMs its diagonal step will use
+        GemmArgs<T> gt = g;
+        gt.M = Mtop; gt.a_r0 = M - Mtop; gt.c_r0 = M - Mtop;
+        g_cta_cap = X;
+        rc = launch_gemm<T, false>(gt);
+        g_cta_cap = 0;
+        if (rc) break;
+        // rest: rows [0, M - Mtop) on the side stream, on the other SMs
+        CK(cudaStreamWaitEvent(side, ev_d, 0));
+        GemmArgs<T> gr = g;
+        gr.M = M - Mtop; gr.a_r0 = 0; gr.c_r0 = 0;
+        g_stream = side;
+        g_cta_cap = g_num_sms - X;
+        rc = launch_gemm<T, false>(gr);
+        g_cta_cap = 0;
+        g_stream = main_st;
+        if (rc) break;
+        CK(cudaEventRecord(ev_rest, side));
+        rest_pending = true;
+        diag_cap = X;
+    }
+    g_stream = main_st;
+    g_cta_cap = 0;
+    if (rest_pending) CK(cudaStreamWaitEvent(main_st, ev_rest, 0));
+    if (Xsum2) ws_free(Xsum2, main_st);
+    return rc;
 }
 
 // Sum planes for the complex 3M update (nullptr when the 3-product kernel is not in use or T is
@@ -910,7 +1042,7 @@ size_t mstrsm_workspace_size(int64_t m, int64_t n, int nb, int is_complex, int s
     size_t total = work + 256;
     if (safe) total += size_t(cdiv(m, kRowsumChunk)) * m * 8 + 256;              // norm pass partials
     if (is_complex && gemm_variant() == 0 && gemm_presum_enabled())            // 3M operand-sum planes
-        total += size_t((m + 2) & ~int64_t(1)) * m * 8 + size_t((nb + 1) & ~1) * n * 8 + 512;
+        total += size_t((m + 2) & ~int64_t(1)) * m * 8 + 2 * size_t((nb + 1) & ~1) * n * 8 + 768;
     return total;
 }
 

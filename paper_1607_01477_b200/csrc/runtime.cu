@@ -10,6 +10,7 @@ namespace mstrsm {
 namespace rt {
 
 cudaStream_t g_stream = nullptr;
+int g_cta_cap = 0;
 std::atomic<int64_t> g_launches{0};
 int *g_flag = nullptr;                 // device: non-finite input seen
 char g_errmsg[512] = "no error";

@@ -16,6 +16,9 @@ namespace mstrsm {
 namespace rt {
 
 extern cudaStream_t g_stream;
+// > 0: launches of the update GEMM and the diagonal kernel use at most this many CTAs (one per
+// SM), leaving the other SMs to a kernel running concurrently on another stream (look-ahead)
+extern int g_cta_cap;
 extern std::atomic<int64_t> g_launches;
 extern int *g_flag;
 extern char g_errmsg[512];
