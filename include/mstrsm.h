@@ -282,6 +282,21 @@ int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dc
  *                          (nullable, m entries) in natural order -- bit-identical to trevc_*.
  *                          Collective: every rank must call it.  Errors: -i for argument i, 1
  *                          CUDA error, 3 communication error (or no communicator).           */
+/* Triangular shard packing for the all-gather (eigenvector k is zero below row k):
+ *   pack:   out[offsets[q] .. + heights[q]) = Z(0 : heights[q], src_cols[q])   (src_cols
+ *           nullable: q), q < n
+ *   unpack: Z(0 : heights[q], dst_cols[q]) = in[offsets[q] ..], rows heights[q] .. m-1 of that
+ *           column set to 0, q < n
+ * All pointers DEVICE; heights / offsets / cols int64.  Errors: -i for argument i.           */
+int mstrsm_d_pack_cols(const double *Z, int64_t ldz, int64_t n, const int64_t *src_cols,
+                       const int64_t *heights, const int64_t *offsets, double *out);
+int mstrsm_z_pack_cols(const mstrsm_dcomplex *Z, int64_t ldz, int64_t n, const int64_t *src_cols,
+                       const int64_t *heights, const int64_t *offsets, mstrsm_dcomplex *out);
+int mstrsm_d_unpack_cols(const double *in, int64_t n, const int64_t *heights, const int64_t *offsets,
+                         const int64_t *dst_cols, int64_t m, double *Z, int64_t ldz);
+int mstrsm_z_unpack_cols(const mstrsm_dcomplex *in, int64_t n, const int64_t *heights,
+                         const int64_t *offsets, const int64_t *dst_cols, int64_t m,
+                         mstrsm_dcomplex *Z, int64_t ldz);
 int     mstrsm_comm_unique_id(void *id_out);
 int     mstrsm_comm_init(int nranks, int rank, const void *unique_id);
 int     mstrsm_comm_destroy(void);

@@ -26,7 +26,7 @@ __all__ = [
     "trevc_d", "trevc_z", "trevc_d_cols", "trevc_z_cols", "trevc_z_host", "trevc_z_host_batch", "pseudospectra_z",
     "mstrsm_d_gen", "mstrsm_z_gen", "tgevc_d", "tgevc_z", "solve_gen", "tgevc",
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
-    "spectral_portrait", "comm_init", "comm_destroy", "dist_shard", "trevc_dist", "solve_dist", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
+    "spectral_portrait", "comm_init", "comm_destroy", "dist_shard", "trevc_dist", "solve_dist", "pack_cols", "unpack_cols", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
     "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
@@ -62,6 +62,10 @@ def load():
         "trevc_z_host_batch": [P, c_i64, c_i64, P, c_i64, P, P, c_i64, c_int],
         "pseudospectra_z": [P, c_i64, c_i64, P, c_i64, c_int, P, P, P, c_int],
         "mstrsm_comm_unique_id": [P],
+        "mstrsm_d_pack_cols": [P, c_i64, c_i64, P, P, P, P],
+        "mstrsm_z_pack_cols": [P, c_i64, c_i64, P, P, P, P],
+        "mstrsm_d_unpack_cols": [P, c_i64, P, P, P, c_i64, P, c_i64],
+        "mstrsm_z_unpack_cols": [P, c_i64, P, P, P, c_i64, P, c_i64],
         "mstrsm_comm_init": [c_int, c_int, P],
         "mstrsm_comm_destroy": [],
         "trevc_d_dist": [P, c_i64, c_i64, P, c_i64, P, P, c_int, c_int],
@@ -249,6 +253,20 @@ def tgevc_z(T, ldt, S, lds, m, Z, ldz, lam, scales, scale_exp, nb):
 def pseudospectra_z(U, ldu, m, z, npts, iters, v0, sigma_min, flags, nb):
     _call("pseudospectra_z", _ptr(U), ldu, m, _ptr(z), npts, iters, _ptr(v0), _ptr(sigma_min),
           _ptr(flags), nb)
+
+
+def pack_cols(Z, heights, offsets, out, src_cols=None):
+    """out[offsets[q]:+heights[q]] = Z[:heights[q], src_cols[q]] (CUDA tensors, int64 index tensors)."""
+    torch = _torch()
+    name = "mstrsm_z_pack_cols" if Z.dtype == torch.complex128 else "mstrsm_d_pack_cols"
+    _call(name, _ptr(Z), _ld(Z), heights.shape[0], _ptr(src_cols), _ptr(heights), _ptr(offsets), _ptr(out))
+
+
+def unpack_cols(inp, heights, offsets, dst_cols, m: int, Z):
+    """Z[:heights[q], dst_cols[q]] = inp[offsets[q]:...], rows below set to 0 (CUDA tensors)."""
+    torch = _torch()
+    name = "mstrsm_z_unpack_cols" if Z.dtype == torch.complex128 else "mstrsm_d_unpack_cols"
+    _call(name, _ptr(inp), heights.shape[0], _ptr(heights), _ptr(offsets), _ptr(dst_cols), m, _ptr(Z), _ld(Z))
 
 
 def dist_shard(m: int, nranks: int, rank: int) -> np.ndarray:

@@ -1420,6 +1420,89 @@ extern "C" int mstrsm_fp64_peak(double ms, double *dmma_tflops, double *dfma_tfl
     return 0;
 }
 
+// ---------------------------------------------------------------- triangular shard packing
+// Eigenvector k is zero below row k, so a shard travels as its columns' rows 0 .. k only
+// (≈ half the bytes of the m x ncols block): column q goes to out[offsets[q] .. + heights[q]).
+template <typename T>
+__global__ void pack_cols_kernel(const T *__restrict__ Z, int64_t ldz, int64_t n, const int64_t *__restrict__ src,
+                                 const int64_t *__restrict__ heights, const int64_t *__restrict__ offsets,
+                                 T *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = w; q < n; q += nw) {
+        const T *z = Z + (src ? src[q] : q) * ldz;
+        T *o = out + offsets[q];
+        for (int64_t i = lane; i < heights[q]; i += 32) o[i] = z[i];
+    }
+}
+template <typename T>
+__global__ void unpack_cols_kernel(const T *__restrict__ in, int64_t n, const int64_t *__restrict__ heights,
+                                   const int64_t *__restrict__ offsets, const int64_t *__restrict__ dst, int64_t m,
+                                   T *__restrict__ Z, int64_t ldz) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t q = w; q < n; q += nw) {
+        const T *s = in + offsets[q];
+        T *z = Z + dst[q] * ldz;
+        const int64_t h = heights[q];
+        for (int64_t i = lane; i < m; i += 32) z[i] = i < h ? s[i] : S<T>::zero();
+    }
+}
+template <typename T>
+int pack_cols_impl(const T *Z, int64_t ldz, int64_t n, const int64_t *src, const int64_t *heights,
+                   const int64_t *offsets, T *out) {
+    if (n < 0) return -3;
+    if (n == 0) return 0;
+    if (!Z) return -1;
+    if (!heights) return -5;
+    if (!offsets) return -6;
+    if (!out) return -7;
+    if (int rc = ensure_init()) return rc;
+    const int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
+    pack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(Z, ldz, n, src, heights, offsets, out);
+    CK_LAUNCH("pack_cols_kernel");
+    return 0;
+}
+template <typename T>
+int unpack_cols_impl(const T *in, int64_t n, const int64_t *heights, const int64_t *offsets, const int64_t *dst,
+                     int64_t m, T *Z, int64_t ldz) {
+    if (n < 0) return -2;
+    if (m < 0) return -6;
+    if (ldz < std::max<int64_t>(1, m)) return -8;
+    if (n == 0 || m == 0) return 0;
+    if (!in) return -1;
+    if (!heights) return -3;
+    if (!offsets) return -4;
+    if (!dst) return -5;
+    if (!Z) return -7;
+    if (int rc = ensure_init()) return rc;
+    const int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
+    unpack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(in, n, heights, offsets, dst, m, Z, ldz);
+    CK_LAUNCH("unpack_cols_kernel");
+    return 0;
+}
+
+extern "C" {
+int mstrsm_d_pack_cols(const double *Z, int64_t ldz, int64_t n, const int64_t *src_cols, const int64_t *heights,
+                       const int64_t *offsets, double *out) {
+    return pack_cols_impl<double>(Z, ldz, n, src_cols, heights, offsets, out);
+}
+int mstrsm_z_pack_cols(const mstrsm_dcomplex *Z, int64_t ldz, int64_t n, const int64_t *src_cols,
+                       const int64_t *heights, const int64_t *offsets, mstrsm_dcomplex *out) {
+    return pack_cols_impl<cplx>((const cplx *)Z, ldz, n, src_cols, heights, offsets, (cplx *)out);
+}
+int mstrsm_d_unpack_cols(const double *in, int64_t n, const int64_t *heights, const int64_t *offsets,
+                         const int64_t *dst_cols, int64_t m, double *Z, int64_t ldz) {
+    return unpack_cols_impl<double>(in, n, heights, offsets, dst_cols, m, Z, ldz);
+}
+int mstrsm_z_unpack_cols(const mstrsm_dcomplex *in, int64_t n, const int64_t *heights, const int64_t *offsets,
+                         const int64_t *dst_cols, int64_t m, mstrsm_dcomplex *Z, int64_t ldz) {
+    return unpack_cols_impl<cplx>((const cplx *)in, n, heights, offsets, dst_cols, m, (cplx *)Z, ldz);
+}
+}  // extern "C"
+
 // ================================================================ multi-GPU
 // One process per GPU; an NCCL communicator bootstrapped by the caller (rank 0 draws the unique
 // id, the caller distributes it, e.g. over its torch process group).  trevc_*_dist replicates the

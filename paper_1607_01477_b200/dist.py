@@ -58,6 +58,41 @@ def gather_perm(m: int, P: int, g: int = 16) -> np.ndarray:
     return perm
 
 
+def tri_layout(m: int, P: int, g: int = 16):
+    """Triangular all-gather layout: rank r sends the rows 0..k of each of its eigenvectors k
+    (column k is zero below row k), packed back to back.  Returns (per-rank (cols, heights,
+    offsets) arrays, L = the longest rank's packed length), balanced by the serpentine map."""
+    lay = []
+    for r in range(P):
+        c = shard_cols(m, P, r, g)
+        h = c + 1
+        off = np.concatenate([[0], np.cumsum(h)[:-1]]).astype(np.int64)
+        lay.append((c, h.astype(np.int64), off))
+    L = max(int(h.sum()) for _, h, _ in lay)
+    return lay, L
+
+
+def _pack(Zl, heights, offsets, out):
+    if Zl.is_cuda:
+        import paper_1607_01477_b200 as ms
+        ms.pack_cols(Zl, heights, offsets, out)
+    else:                                                     # CPU tensors (gloo tests)
+        for q in range(heights.shape[0]):
+            o, h = int(offsets[q]), int(heights[q])
+            out[o:o + h] = Zl[:h, q]
+
+
+def _unpack(inp, heights, offsets, dst, m, Z):
+    if Z.is_cuda:
+        import paper_1607_01477_b200 as ms
+        ms.unpack_cols(inp, heights, offsets, dst, m, Z)
+    else:
+        for q in range(heights.shape[0]):
+            o, h, k = int(offsets[q]), int(heights[q]), int(dst[q])
+            Z[:h, k] = inp[o:o + h]
+            Z[h:, k] = 0
+
+
 def _panels(m: int, w: int):
     return [(c0, min(m, c0 + w)) for c0 in range(0, m, w)]
 
@@ -90,9 +125,9 @@ def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, 
 
     T: (m x m) tensor on every rank (contents only needed on rank 0; its upper triangle is
     overwritten elsewhere, the strictly lower triangle is not sent).
-    solve_cols(T, cols, out) writes eigenvector cols[q] into column q of `out` (an m x ncols
-    column-major view into this rank's all-gather send buffer, so no copy is needed) and returns
-    the int32 exponents (ncols,).
+    solve_cols(T, cols, out) writes eigenvector cols[q] into column q of `out` (m x ncols,
+    column-major) and returns the int32 exponents (ncols,).  Only rows 0..k of eigenvector k
+    travel in the all-gather (tri_layout; the rest is zero by construction).
     Returns (Z (m x m, column-major), e (m,) int32), identical on every rank."""
     import torch
     import torch.distributed as dist
@@ -106,19 +141,26 @@ def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, 
             unpack_upper(buf, T, m)
         del buf
     cols = shard_cols(m, world, rank, g)
-    mc = max_shard(m, world, g) if world > 1 else len(cols)
-    send = torch.empty((mc, m), dtype=T.dtype, device=T.device)           # row q = eigenvector q
-    # (rows >= ncols are padding: sent, never unpacked)
-    el = solve_cols(T, cols, send[: len(cols)].t())
     if world == 1:
+        send = torch.empty((len(cols), m), dtype=T.dtype, device=T.device)   # row q = eigenvector q
+        el = solve_cols(T, cols, send.t())
         e = torch.empty(m, dtype=torch.int32, device=el.device)
         e[torch.from_numpy(cols).to(el.device)] = el
         return send.t(), e
-    epad = torch.empty(mc, dtype=torch.int32, device=el.device)
+    # this rank's shard, then only its upper-triangular part travels (≈ half the bytes)
+    Zl = torch.empty((len(cols), m), dtype=T.dtype, device=T.device).t()   # m x ncols column-major
+    el = solve_cols(T, cols, Zl)
+    lay, L = tri_layout(m, world, g)
+    dev = T.device
+    _, h_r, off_r = lay[rank]
+    send = torch.empty(L, dtype=T.dtype, device=dev)
+    _pack(Zl, torch.from_numpy(h_r).to(dev), torch.from_numpy(off_r).to(dev), send)
+    mc = max_shard(m, world, g)
+    epad = torch.zeros(mc, dtype=torch.int32, device=el.device)
     epad[: len(cols)] = el
     backend = dist.get_backend(group)
     if backend == "nccl":
-        out = torch.empty((world * mc, m), dtype=send.dtype, device=send.device)
+        out = torch.empty(world * L, dtype=send.dtype, device=dev)
         eout = torch.empty(world * mc, dtype=torch.int32, device=el.device)
         dist.all_gather_into_tensor(out, send, group=group)
         dist.all_gather_into_tensor(eout, epad, group=group)
@@ -128,7 +170,12 @@ def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, 
         dist.all_gather(outs, send, group=group)
         dist.all_gather(eouts, epad, group=group)
         out, eout = torch.cat(outs, 0), torch.cat(eouts, 0)
-    perm = torch.from_numpy(gather_perm(m, world, g)).to(out.device)
-    Z = out.index_select(0, perm).t()
-    e = eout.index_select(0, perm.to(eout.device))
+    heights = np.concatenate([h for _, h, _ in lay])
+    offsets = np.concatenate([off + r * L for r, (_, _, off) in enumerate(lay)])
+    dst = np.concatenate([c for c, _, _ in lay]).astype(np.int64)
+    Z = torch.empty((m, m), dtype=T.dtype, device=dev).t()
+    _unpack(out, torch.from_numpy(heights).to(dev), torch.from_numpy(offsets).to(dev),
+            torch.from_numpy(dst).to(dev), m, Z)
+    perm = torch.from_numpy(gather_perm(m, world, g)).to(eout.device)
+    e = eout.index_select(0, perm)
     return Z, e
