@@ -1540,9 +1540,11 @@ __global__ void gather_dist_kernel(const T *__restrict__ Za, int64_t m, const in
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t k = w; k < n; k += nw) {
         const int64_t p = perm[k];
-        const T *src = Za + p * m;
-        T *dst = Z + k * ldz;
-        for (int64_t i = lane; i < m; i += 32) dst[i] = src[i];
+        if (Za) {                              // (NULL: vectors unpacked elsewhere)
+            const T *src = Za + p * m;
+            T *dst = Z + k * ldz;
+            for (int64_t i = lane; i < m; i += 32) dst[i] = src[i];
+        }
         if (lane == 0) {
             if (scales) scales[k] = sa[p];
             if (exps) exps[k] = ea[p];
@@ -1660,35 +1662,82 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     double *ss = nullptr, *sa = nullptr;
     int *es_ = nullptr, *ea = nullptr;
     int64_t *perm_d = nullptr;
+    // triangular all-gather layout: rows 0 .. k of eigenvector k (zero below), packed per rank
+    std::vector<std::vector<int64_t>> rc_cols(P);
+    int64_t L = 0;
+    for (int q = 0; q < P; q++) {
+        rc_cols[q].resize(size_t(std::max<int64_t>(shard_of(m, P, q, kShardGroup, nullptr), 1)));
+        const int64_t nq = shard_of(m, P, q, kShardGroup, rc_cols[q].data());
+        rc_cols[q].resize(size_t(nq));
+        int64_t tot = 0;
+        for (int64_t i = 0; i < nq; i++) tot += rc_cols[q][i] + 1;
+        L = std::max(L, tot);
+    }
+    std::vector<int64_t> hh, oo, dd;                // all ranks: heights, offsets (in Za), columns
+    for (int q = 0; q < P; q++) {
+        int64_t off = int64_t(q) * L;
+        for (int64_t k : rc_cols[q]) {
+            hh.push_back(k + 1);
+            oo.push_back(off);
+            dd.push_back(k);
+            off += k + 1;
+        }
+    }
+    int64_t *meta = nullptr;                        // [heights | offsets | cols] for all m eigenvectors
     CK(cudaMallocAsync(&Zs, size_t(m) * mc * es, g_stream));
     CK(cudaMallocAsync(&ss, size_t(mc) * 8, g_stream));
     CK(cudaMallocAsync(&es_, size_t(mc) * 4, g_stream));
-    CK(cudaMallocAsync(&Za, size_t(m) * mc * P * es, g_stream));
+    CK(cudaMallocAsync(&Za, size_t(L) * P * es, g_stream));
     CK(cudaMallocAsync(&sa, size_t(mc) * P * 8, g_stream));
     CK(cudaMallocAsync(&ea, size_t(mc) * P * 4, g_stream));
     CK(cudaMallocAsync(&perm_d, size_t(m) * 8, g_stream));
+    CK(cudaMallocAsync(&meta, size_t(m) * 3 * 8, g_stream));
+    T *Sb = nullptr;
+    CK(cudaMallocAsync(&Sb, size_t(std::max<int64_t>(L, 1)) * es, g_stream));
     int rc = ncols > 0 ? trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb) : 0;
     if (rc < 0) rc = 1;
     if (!rc) {
-        // 3. gather every shard (vectors, scales, exponents)
+        std::vector<int64_t> perm(m);
+        for (int q = 0; q < P; q++)
+            for (size_t i = 0; i < rc_cols[q].size(); i++) perm[rc_cols[q][i]] = int64_t(q) * mc + int64_t(i);
+        std::vector<int64_t> metah(size_t(m) * 3);
+        std::copy(hh.begin(), hh.end(), metah.begin());
+        std::copy(oo.begin(), oo.end(), metah.begin() + m);
+        std::copy(dd.begin(), dd.end(), metah.begin() + 2 * m);
+        CK(cudaMemcpyAsync(perm_d, perm.data(), size_t(m) * 8, cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemcpyAsync(meta, metah.data(), size_t(m) * 3 * 8, cudaMemcpyHostToDevice, g_stream));
+        // this rank's columns are entries [first_r, first_r + ncols) of the all-rank arrays
+        int64_t first_r = 0;
+        for (int q = 0; q < r; q++) first_r += int64_t(rc_cols[q].size());
+        std::vector<int64_t> off_local(size_t(std::max<int64_t>(ncols, 1)));
+        for (int64_t i = 0; i < ncols; i++) off_local[i] = oo[first_r + i] - int64_t(r) * L;
+        int64_t *offl = nullptr;
+        CK(cudaMallocAsync(&offl, size_t(std::max<int64_t>(ncols, 1)) * 8, g_stream));
+        CK(cudaMemcpyAsync(offl, off_local.data(), size_t(std::max<int64_t>(ncols, 1)) * 8, cudaMemcpyHostToDevice,
+                           g_stream));
+        if (ncols > 0) {
+            const int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
+            pack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(Zs, m, ncols, nullptr, meta + first_r, offl, Sb);
+            CK_LAUNCH("pack_cols_kernel");
+        }
+        // 3. gather every shard (packed vectors, scales, exponents)
         NCK(ncclGroupStart());
-        NCK(ncclAllGather(Zs, Za, size_t(m) * mc * ndbl, ncclDouble, g_comm, g_stream));
+        NCK(ncclAllGather(Sb, Za, size_t(L) * ndbl, ncclDouble, g_comm, g_stream));
         NCK(ncclAllGather(ss, sa, size_t(mc), ncclDouble, g_comm, g_stream));
         NCK(ncclAllGather(es_, ea, size_t(mc), ncclInt32, g_comm, g_stream));
         NCK(ncclGroupEnd());
-        // 4. natural order: eigenvector k is row-block slot q of rank owner(k)
-        std::vector<int64_t> perm(m);
-        for (int q = 0; q < P; q++) {
-            const int64_t nq = shard_of(m, P, q, kShardGroup, cols.data());
-            for (int64_t i = 0; i < nq; i++) perm[cols[i]] = int64_t(q) * mc + i;
-        }
-        CK(cudaMemcpyAsync(perm_d, perm.data(), size_t(m) * 8, cudaMemcpyHostToDevice, g_stream));
-        CK(cudaStreamSynchronize(g_stream));       // perm's host buffer goes out of scope below
+        // 4. natural order: vectors by the triangular layout, scales / exponents by perm
         const int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
-        gather_dist_kernel<T><<<blocks, 256, 0, g_stream>>>(Za, m, perm_d, m, Z, ldz, sa, ea, scales,
+        unpack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(Za, m, meta, meta + m, meta + 2 * m, m, Z, ldz);
+        CK_LAUNCH("unpack_cols_kernel");
+        gather_dist_kernel<T><<<blocks, 256, 0, g_stream>>>(nullptr, m, perm_d, m, Z, ldz, sa, ea, scales,
                                                             reinterpret_cast<int *>(scale_exp));
         CK_LAUNCH("gather_dist_kernel");
+        CK(cudaStreamSynchronize(g_stream));       // host index arrays go out of scope
+        cudaFreeAsync(offl, g_stream);
     }
+    cudaFreeAsync(meta, g_stream);
+    cudaFreeAsync(Sb, g_stream);
     for (void *p : {(void *)pack, (void *)Tw, (void *)Zs, (void *)ss, (void *)es_, (void *)Za, (void *)sa,
                     (void *)ea, (void *)perm_d})
         if (p) cudaFreeAsync(p, g_stream);
