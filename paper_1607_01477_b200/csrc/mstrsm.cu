@@ -159,7 +159,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
                   const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w,
                   const double *Usum = nullptr, double *Xsum = nullptr, int64_t ldus = 0, int ldxs = 0) {
     if constexpr (SAFE) {
-        if (op == 0 && lookahead_enabled())
+        if (op == 0 && m >= 1024 && lookahead_enabled())      // (small solves: stream/event overhead)
             return blocked_solve_la<T>(U, ldu, m, shifts, sstride, B, ldb, n, rowend_dev, rowend_sorted_host, nb, w,
                                        Usum, Xsum, ldus, ldxs);
     }
