@@ -28,7 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--only", default="c1,c2,c3,c4,c4d,g1,f2,f4,trsm")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c4d,g1,f2,f4,trsm,c5s8")
     a = ap.parse_args()
     import torch
     import paper_1607_01477_b200 as ms
@@ -63,6 +63,14 @@ def main():
                        15 * 2 * 4.0 * 1024 ** 2 * z.shape[0], z.shape[0], "points/s",
                        "c4d: c4 with SpectralCloud deflation (tol 1e-10, at most 15 steps; SURVEY §8f f3); "
                        "gflops counts the fixed 15-step work, so it is an effective rate")
+    if "c5s8" in a.only:
+        # one rank's shard of the 8-GPU c5 step (2048 eigenvectors, serpentine block-cyclic), the
+        # solve part of what each rank does at N = 8 (the collectives are the driver's to measure)
+        from paper_1607_01477_b200 import dist as pdist
+        T5 = dev(inputs.c5_grcar_like())
+        cols8 = pdist.shard_cols(16384, 8, 0, 16)
+        work["c5s8"] = (lambda: ms.trevc(T5, nb=128, cols=cols8), eig_flops(16384, True) / 8, len(cols8),
+                        "eigvecs/s", "c5s8: rank 0's shard of the 8-GPU c5 step (2048 eigenvectors), solve only")
     if "trsm" in a.only:
         # SURVEY §8d.5 paper analogue (context only): the multi-shift solve at zero shift against
         # cuBLAS trsm (torch.linalg.solve_triangular) on the same upper-triangular system
