@@ -55,6 +55,17 @@ static bool encode_2d(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The 3-product kernel's second consumer group starts MSTRSM_3P_PHASE/4 of a tile late (default
+// 2: half a tile), so the two groups' epilogues do not coincide (0: both start together)
+static int gemm_3p_phase() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_3P_PHASE");
+        v = (e && e[0] >= '0' && e[0] <= '3' && !e[1]) ? e[0] - '0' : 2;
+    }
+    return v;
+}
+
 // MSTRSM_3M_GROUPS=3: three consumer warpgroups (gemm_ws3q.cuh) instead of two
 static int gemm_3m_groups() {
     static int v = -1;
@@ -131,7 +142,8 @@ int launch_gemm(const GemmArgs<T> &g) {
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
             const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
             ProfScope ps(PK_GEMM, flops);
-            kern<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs);
+            kern<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs,
+                                                                gemm_3p_phase());
             CK_LAUNCH("gemm_ws3p_kernel");
             return 0;
         }

@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
                                                                   const __grid_constant__ CUtensorMap tmX,
                                                                   const __grid_constant__ CUtensorMap tmXs,
                                                                   const __grid_constant__ CUtensorMap tmA,
-                                                                  const __grid_constant__ CUtensorMap tmAs) {
+                                                                  const __grid_constant__ CUtensorMap tmAs,
+                                                                  int phase) {
     constexpr int kPC = k3p_pc<OPC>();
     constexpr int BM = k3mBM, BN = k3mBN, BK = k3mBK, RS = k3pRing;
     constexpr int MI = k3mMI, NI = 4;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
     unsigned char *smem_raw = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
     __shared__ uint64_t full_bar[2][RS], empty_bar[2][RS];
     __shared__ int s_d[2][BN];
+    __shared__ int s_go;    // phase != 0: group 1 starts once group 0 is phase/4 through its first tile
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nk = (g.K + BK - 1) / BK;
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
                 mbar_init(&full_bar[q][s], 64);     // every producer lane arrives (with its bytes)
                 mbar_init(&empty_bar[q][s], 4);     // the 4 warps of the consuming group
             }
+        s_go = phase ? 0 : 1;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -198,6 +201,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, local++) {
         if ((local & 1) != grp) continue;
         const int64_t m0 = int64_t(tile % tiles_m) * BM, n0 = int64_t(tile / tiles_m) * BN;
+        if (local == 1)         // group 1's first tile: offset the two groups' epilogues (by half a tile: phase 2)
+            while (*reinterpret_cast<volatile int *>(&s_go) == 0) __nanosleep(64);
 
         double p1[MI][NI][2], p2[MI][NI][2], p3[MI][NI][2];
 #pragma unroll
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[grp][s]);
+            if (local == 0 && kt == (nk * phase) / 4 && cw == 0 && lane == 0) *reinterpret_cast<volatile int *>(&s_go) = 1;
         }
 
         // ---- epilogue (as gemm_ws3m_kernel): C = 2^d C - (P1 - P2, P3 - P1 - P2) ----
