@@ -361,8 +361,11 @@ def run_cuda(args, cfgname):
     traffic, _ = ncu_traffic()
     roofline = {"bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": (gemm_tf / peak_tf) if gemm_tf else None, "traffic": traffic,
-                "kernel": (("gemm_ws3p_kernel (persistent warp-specialised, complex as 3 real products with "
-                            "precomputed operand sums, TMA/bulk-copy producer, mma.sync m8n8k4 f64 -> DMMA)")
+                "kernel": ((("gemm_ws3p_kernel (two" if os.environ.get("MSTRSM_3M_GROUPS") == "2" else
+                             "gemm_ws3q_kernel (three") +
+                            " staggered consumer warpgroups; persistent warp-specialised, complex as 3 real "
+                            "products with precomputed operand sums, TMA/bulk-copy producer, mma.sync m8n8k4 "
+                            "f64 -> DMMA)")
                            if os.environ.get("MSTRSM_3M_PRESUM", "1") != "0" else
                            "gemm_ws3m_kernel<false> (persistent warp-specialised, complex as 3 real products, "
                            "mma.sync m8n8k4 f64 -> DMMA)") if (cplx and prods == 3) else

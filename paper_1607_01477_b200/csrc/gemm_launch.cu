@@ -66,12 +66,12 @@ static int gemm_3p_phase() {
     return v;
 }
 
-// MSTRSM_3M_GROUPS=3: three consumer warpgroups (gemm_ws3q.cuh) instead of two
+// Three consumer warpgroups (gemm_ws3q.cuh, default) or two (MSTRSM_3M_GROUPS=2, gemm_ws3p.cuh)
 static int gemm_3m_groups() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MSTRSM_3M_GROUPS");
-        v = (e && !strcmp(e, "3")) ? 3 : 2;
+        v = (e && !strcmp(e, "2")) ? 2 : 3;
     }
     return v;
 }
@@ -129,7 +129,8 @@ int launch_gemm(const GemmArgs<T> &g) {
                 const int64_t tm = cdiv(g.M, k3qBM), tn = cdiv(g.N, k3qBN), nt = tm * tn;
                 const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
                 ProfScope ps(PK_GEMM, flops);
-                kq<<<grid, k3qThreads, k3qSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs);
+                kq<<<grid, k3qThreads, k3qSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs,
+                                                              gemm_3p_phase());
                 CK_LAUNCH("gemm_ws3q_kernel");
                 return 0;
             }

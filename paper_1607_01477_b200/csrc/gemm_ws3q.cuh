@@ -31,13 +31,15 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
                                                                   const __grid_constant__ CUtensorMap tmX,
                                                                   const __grid_constant__ CUtensorMap tmXs,
                                                                   const __grid_constant__ CUtensorMap tmA,
-                                                                  const __grid_constant__ CUtensorMap tmAs) {
+                                                                  const __grid_constant__ CUtensorMap tmAs,
+                                                                  int phase) {
     constexpr int kPC = k3q_pc<OPC>();
     constexpr int BM = k3qBM, BN = k3qBN, BK = k3qBK, RS = k3qRing, MI = k3qMI, NI = 4, NG = 3;
     extern __shared__ __align__(1024) unsigned char smem_dyn[];
     unsigned char *smem_raw = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
     __shared__ uint64_t full_bar[NG][RS], empty_bar[NG][RS];
     __shared__ int s_d[NG][BN];
+    __shared__ int s_go;    // phase != 0: group q starts its first tile once group 0 is q/3 through its own
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nk = (g.K + BK - 1) / BK;
@@ -47,6 +49,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
                 mbar_init(&full_bar[q][s], 32);     // the group's producer warp, every lane
                 mbar_init(&empty_bar[q][s], 4);     // the 4 warps of the consuming group
             }
+        s_go = phase ? 0 : NG;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -146,6 +149,8 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, local++) {
         if (local % NG != grp) continue;
         const int64_t m0 = int64_t(tile % tiles_m) * BM, n0 = int64_t(tile / tiles_m) * BN;
+        if (local == grp && grp > 0)   // staggered start: the groups' epilogues do not coincide
+            while (*reinterpret_cast<volatile int *>(&s_go) < grp) __nanosleep(64);
 
         double p1[MI][NI][2], p2[MI][NI][2], p3[MI][NI][2];
 #pragma unroll
@@ -205,6 +210,10 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[grp][s]);
+            if (local == 0 && cw == 0 && lane == 0) {
+                if (kt == nk / 3) *reinterpret_cast<volatile int *>(&s_go) = 1;
+                if (kt == (2 * nk) / 3) *reinterpret_cast<volatile int *>(&s_go) = 2;
+            }
         }
 
         // ---- epilogue: C = 2^d C - (P1 - P2, P3 - P1 - P2); warp (wm, wn) reads half wn ----
