@@ -361,7 +361,7 @@ def run_cuda(args, cfgname):
     traffic, _ = ncu_traffic()
     roofline = {"bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": (gemm_tf / peak_tf) if gemm_tf else None, "traffic": traffic,
-                "kernel": ((("gemm_ws3p_kernel (two" if os.environ.get("MSTRSM_3M_GROUPS") == "2" else
+                "kernel": ((("gemm_ws3p_kernel (two" if os.environ.get("MSTRSM_3M_GROUPS") == "2" or nb < 96 else
                              "gemm_ws3q_kernel (three") +
                             " staggered consumer warpgroups; persistent warp-specialised, complex as 3 real "
                             "products with precomputed operand sums, TMA/bulk-copy producer, mma.sync m8n8k4 "
