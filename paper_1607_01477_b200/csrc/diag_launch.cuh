@@ -2,11 +2,21 @@
 // diag_{d,z}{N,C}_{plain,safe}.cu units, each of which instantiates one (scalar, op, variant).
 #pragma once
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "runtime.cuh"
 
 namespace mstrsm {
 namespace rt {
+inline bool diag_balance() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_DIAG_BALANCE");   // 0: fill CTAs, short last pass
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <typename T, int LPC, int RPL, bool SAFE, int OP, bool FB, bool GEN>
 int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
     auto kern = diag_kernel<T, LPC, RPL, SAFE, OP, FB, GEN>;
@@ -25,6 +35,10 @@ int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
     const int64_t sms = g_cta_cap > 0 ? g_cta_cap : g_num_sms;
     int64_t wpc = cdiv(groups, sms * std::max(occ1, 1));
     wpc = std::max<int64_t>(1, std::min<int64_t>(kMaxThreads / 32, wpc));
+    if (diag_balance()) {   // equal passes: as many warps per CTA as the pass count needs, no short last pass
+        const int64_t npass = cdiv(groups, sms * std::max(occ1, 1) * (kMaxThreads / 32));
+        wpc = std::max<int64_t>(1, std::min<int64_t>(kMaxThreads / 32, cdiv(groups, sms * std::max(occ1, 1) * npass)));
+    }
     const int threads = int(wpc * 32);
     int occ = occupancy(kern, threads, smem);
     int grid = int(std::min<int64_t>(cdiv(groups, wpc), int64_t(occ) * sms));
