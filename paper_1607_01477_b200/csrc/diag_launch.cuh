@@ -8,6 +8,19 @@
 
 namespace mstrsm {
 namespace rt {
+// Pass costs of the RPL = 16 (which = 0) and RPL = 4 (which = 1) layouts in tenths of an RPL = 8
+// pass (measured on the c5 launch list: 12 and 7); MSTRSM_DIAG_COST16 / MSTRSM_DIAG_COST4 override.
+inline int diag_cost(int which) {
+    static int v[2] = {-1, -1};
+    if (v[which] < 0) {
+        const char *e = getenv(which ? "MSTRSM_DIAG_COST4" : "MSTRSM_DIAG_COST16");
+        const int d = which ? 7 : 12;
+        v[which] = e ? atoi(e) : d;
+        if (v[which] <= 0) v[which] = d;
+    }
+    return v[which];
+}
+
 inline bool diag_balance() {
     static int v = -1;
     if (v < 0) {
@@ -78,18 +91,15 @@ int launch_diag(const DiagArgs<T> &a, int nb) {
         const int64_t per_pass = int64_t(g_num_sms) * (rpl >= 16 ? DiagThreads<T, 16>::value : DiagThreads<T, 8>::value) / 32 * (32 / lpc);   // (RPL 4 uses RPL 8's CTA size)
         return cdiv(a.ncols, per_pass);
     };
-    auto few = [&](int lpc16) { return 10 * passes(2 * lpc16, 8) < 12 * passes(lpc16, 16); };
+    const int c16 = diag_cost(0), c4 = diag_cost(1);
+    auto few = [&](int lpc16) { return 10 * passes(2 * lpc16, 8) < c16 * passes(lpc16, 16); };
     if (nb <= 16) return launch_diag_pair<T, 1, 16, SAFE, OP, false>(a);
     if (nb <= 32) return launch_diag_pair<T, 2, 16, SAFE, OP, false>(a);
     if (nb <= 64) return few(4) ? launch_diag_pair<T, 8, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 4, 16, SAFE, OP, false>(a);
     if (g_cta_cap > 0) return launch_diag_pair<T, 8, 16, SAFE, OP, false>(a);   // look-ahead: densest layout
-#ifndef MSTRSM_DIAG_RPL4_COST
-#define MSTRSM_DIAG_RPL4_COST 7      // pass cost of the RPL = 4 layout in tenths of an RPL = 8 pass
-#endif
     // very few columns (the first blocks of TriangEig, every block of a multi-GPU shard): a whole
     // warp per column, 4 rows per lane -- the shortest per-row chain
-    if (MSTRSM_DIAG_RPL4_COST * passes(32, 4) < 10 * passes(16, 8) &&
-        MSTRSM_DIAG_RPL4_COST * passes(32, 4) < 12 * passes(8, 16))
+    if (c4 * passes(32, 4) < 10 * passes(16, 8) && c4 * passes(32, 4) < c16 * passes(8, 16))
         return launch_diag_pair<T, 32, 4, SAFE, OP, false>(a);
     return few(8) ? launch_diag_pair<T, 16, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 8, 16, SAFE, OP, false>(a);
 }
