@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
                 mbar_init(&full_bar[q][s], 64);     // every producer lane arrives (with its bytes)
                 mbar_init(&empty_bar[q][s], 4);     // the 4 warps of the consuming group
             }
-        s_go = phase ? 0 : 1;
+        s_go = (phase && nk > 0) ? 0 : 1;     // (K = 0: no k-tile would release group 1)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
                 mbar_init(&full_bar[q][s], 32);     // the group's producer warp, every lane
                 mbar_init(&empty_bar[q][s], 4);     // the 4 warps of the consuming group
             }
-        s_go = phase ? 0 : NG;
+        s_go = (phase && nk > 0) ? 0 : NG;    // (K = 0: no k-tile would release the others)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
