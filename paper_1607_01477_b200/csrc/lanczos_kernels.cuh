@@ -20,15 +20,30 @@ struct LanczosState {
 };
 
 // copy src -> dst for active points (m x npts, column-major), one warp per point
-__global__ void copy_cols_kernel(const cplx *__restrict__ src, cplx *__restrict__ dst, int64_t m,
-                                 int64_t npts) {
+// dst(:, p) = src(:, p) and the safe solve's right-hand-side set-up in the same pass (what
+// init_rhs_kernel does with every row active): G_p = max_l |dst(l, p)|, e_p = 0, and the
+// non-finite shift flag -- one read of the Lanczos vector instead of two.
+__global__ void copy_init_rhs_kernel(const cplx *__restrict__ src, cplx *__restrict__ dst, int64_t m,
+                                     int64_t npts, const cplx *__restrict__ shifts, double *__restrict__ G,
+                                     int *__restrict__ e, int *__restrict__ nonfinite) {
     int lane = threadIdx.x & 31;
     int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t p = w; p < npts; p += nw) {
         const cplx *s = src + p * m;
         cplx *d = dst + p * m;
-        for (int64_t i = lane; i < m; i += 32) d[i] = s[i];
+        double g = 0.0;
+        for (int64_t i = lane; i < m; i += 32) {
+            const cplx v = s[i];
+            d[i] = v;
+            g = fmax(g, S<cplx>::mod(v));
+        }
+        g = warp_max(g);
+        if (lane == 0) {
+            G[p] = g;
+            e[p] = 0;
+            if (shifts && nonfinite && !(S<cplx>::mod(shifts[p]) <= 1.7976931348623157e308)) atomicExch(nonfinite, 1);
+        }
     }
 }
 

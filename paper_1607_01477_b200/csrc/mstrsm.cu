@@ -838,17 +838,13 @@ int spectral_cloud_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, in
     int rc = 0;
     for (int it = 0; it < iters && !rc && nact > 0; it++) {
         const int ab = int(std::min<int64_t>(cdiv(nact, 8), int64_t(g_num_sms) * 16));
-        copy_cols_kernel<<<ab, 256, 0, g_stream>>>(st.V, st.Y, m, nact);
-        CK_LAUNCH("copy_cols_kernel");
-        init_rhs_kernel<cplx><<<ab, 256, 0, g_stream>>>(st.Y, m, m, nact, nullptr, zc, 1, wN.G, wN.e, g_flag);
-        CK_LAUNCH("init_rhs_kernel");
+        copy_init_rhs_kernel<<<ab, 256, 0, g_stream>>>(st.V, st.Y, m, nact, zc, wN.G, wN.e, g_flag);
+        CK_LAUNCH("copy_init_rhs_kernel");
         rc = blocked_solve<cplx, true>(0, U, ldu, m, zc, 1, st.Y, m, nact, nullptr, nullptr, nb, wN, spN.U, spN.X, spN.ldu, spN.ldx);
         if (!rc) rc = finalize<cplx>(0, 1, st.Y, m, m, nact, nb, nullptr, nullptr, e1, nullptr, wN);
         if (rc) break;
-        copy_cols_kernel<<<ab, 256, 0, g_stream>>>(st.Y, st.W, m, nact);
-        CK_LAUNCH("copy_cols_kernel");
-        init_rhs_kernel<cplx><<<ab, 256, 0, g_stream>>>(st.W, m, m, nact, nullptr, nullptr, 0, wC.G, wC.e, nullptr);
-        CK_LAUNCH("init_rhs_kernel");
+        copy_init_rhs_kernel<<<ab, 256, 0, g_stream>>>(st.Y, st.W, m, nact, nullptr, wC.G, wC.e, nullptr);
+        CK_LAUNCH("copy_init_rhs_kernel");
         rc = blocked_solve<cplx, true>(1, U, ldu, m, zc, 1, st.W, m, nact, nullptr, nullptr, nb, wC, spC.U, spC.X, spC.ldu, spC.ldx);
         if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, nact, nb, nullptr, nullptr, e2, nullptr, wC);
         if (rc) break;
