@@ -392,6 +392,9 @@ def run_cuda(args, cfgname):
                        "l2": "inputs (4.3 GB T, 4.3 GB Z) >> 126 MB L2; no flush needed"},
             "eigvecs_per_s": eig_per_s,
             "pct_fp64_peak": 100.0 * value / 1e3 / (peak_tf * ws) if peak_tf else None,
+            "pct_fp64_peak_note": "algorithmic flops (R18: 8 real flops per complex MAC) / measured DMMA "
+                                  "peak x N; the 3M update executes 3/4 of those flops, so this is the "
+                                  "metric's figure, not hardware utilisation (roofline.frac is)",
             "gflops_nominal_m2n": nominal_flops(m, m, cplx) / (ms_per_step * 1e-3) / 1e9,
             "roofline": roofline, "clocks": clocks, "gpu_launches": launches,
             "wall_s_timed": t_wall, "output_finite": ok_finite,
