@@ -74,7 +74,8 @@ __global__ void lanczos_step_kernel(LanczosState st, int64_t m, int64_t nslots, 
     for (int64_t sl = w; sl < nslots; sl += nw) {
         const int64_t p = st.pid[sl];
         if (!st.active[p]) continue;
-        cplx *V = st.V + sl * m, *Vp = st.Vp + sl * m, *W = st.W + sl * m;
+        const cplx *V = st.V + sl * m, *Vp = st.Vp + sl * m;
+        cplx *W = st.W + sl * m;
         const cplx *Y = st.Y + sl * m;
         int e1 = st.e1[sl], e2 = st.e2[sl];
         if (e1 < 0 || e2 < 0) {
@@ -113,12 +114,11 @@ __global__ void lanczos_step_kernel(LanczosState st, int64_t m, int64_t nslots, 
         int k = st.kdone[p];
         double amax = fmax(st.amax[p], a);
         bool brk = b <= double(m) * 0x1p-52 * amax;                       // Krylov space exhausted
-        if (!brk && it + 1 < iters) {
-            double binv = 1.0 / b;
+        if (!brk && it + 1 < iters) {   // v_next = w / beta in W's buffer; the host then rotates
+            double binv = 1.0 / b;      // (V, V_prev, W) <- (W, V, V_prev) instead of copying
             for (int64_t i = lane; i < m; i += 32) {
                 cplx wi = W[i];
-                Vp[i] = V[i];
-                V[i] = make_double2(wi.x * binv, wi.y * binv);
+                W[i] = make_double2(wi.x * binv, wi.y * binv);
             }
         }
         if (lane == 0) {

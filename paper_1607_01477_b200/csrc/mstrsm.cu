@@ -850,6 +850,12 @@ int spectral_cloud_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, in
         if (rc) break;
         lanczos_step_kernel<<<ab, 256, 0, g_stream>>>(st, m, nact, it, iters);
         CK_LAUNCH("lanczos_step_kernel");
+        if (it + 1 < iters) {           // the step left v_next in W: rotate (V, V_prev, W) <- (W, V, V_prev)
+            cplx *t = st.Vp;
+            st.Vp = st.V;
+            st.V = st.W;
+            st.W = t;
+        }
         if (tol > 0.0 && it + 1 < iters) {
             converge_kernel<<<int(cdiv(nact, 128)), 128, 0, g_stream>>>(st, nact);
             CK_LAUNCH("converge_kernel");
