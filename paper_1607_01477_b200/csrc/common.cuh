@@ -143,3 +143,9 @@ __host__ __device__ __forceinline__ Blk block_rows(int op, int64_t m, int nb, in
 }
 
 }  // namespace mstrsm
+
+namespace mstrsm {
+// Programmatic dependent launch: wait for the preceding grid in the stream (a no-op when the
+// kernel was launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+}  // namespace mstrsm

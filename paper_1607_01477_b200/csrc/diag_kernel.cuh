@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
     double *cn = reinterpret_cast<double *>(dgV + nfull);
     double *cnV = cn + (GEN ? nfull : 0);
 
+    pdl_wait();
     // ---- stage U(I1,I1) (packed, solve coordinates), its diagonal and cnl ----
     const int tid = threadIdx.x, nth = blockDim.x;
     {

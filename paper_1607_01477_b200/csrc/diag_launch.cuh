@@ -58,7 +58,7 @@ int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
     if (grid < 1) grid = 1;
     double fl = FB ? 0.0 : double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
     ProfScope ps(PK_DIAG, fl);
-    kern<<<grid, threads, smem, g_stream>>>(a);
+    CK(launch_k(kern, dim3(grid), dim3(threads), smem, g_stream, a));
     CK_LAUNCH("diag_kernel");
     return 0;
 }

@@ -134,8 +134,8 @@ int launch_gemm(const GemmArgs<T> &g) {
                 const int64_t tm = cdiv(g.M, k3qBM), tn = cdiv(g.N, k3qBN), nt = tm * tn;
                 const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
                 ProfScope ps(PK_GEMM, flops);
-                kq<<<grid, k3qThreads, k3qSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs,
-                                                              gemm_3p_phase());
+                CK(launch_k(kq, dim3(grid), dim3(k3qThreads), k3qSmemBytes, g_stream, g, int(tm), int(nt), tmX, tmXs, tmA,
+                            tmAs, gemm_3p_phase()));
                 CK_LAUNCH("gemm_ws3q_kernel");
                 return 0;
             }
@@ -148,8 +148,8 @@ int launch_gemm(const GemmArgs<T> &g) {
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
             const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
             ProfScope ps(PK_GEMM, flops);
-            kern<<<grid, kWsThreads, k3pSmemBytes, g_stream>>>(g, int(tm), int(nt), tmX, tmXs, tmA, tmAs,
-                                                                gemm_3p_phase());
+            CK(launch_k(kern, dim3(grid), dim3(kWsThreads), k3pSmemBytes, g_stream, g, int(tm), int(nt), tmX, tmXs,
+                            tmA, tmAs, gemm_3p_phase()));
             CK_LAUNCH("gemm_ws3p_kernel");
             return 0;
         }

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();
 
     if (warp < 4) {
         // ------------------------------------------------------------------ producers
