@@ -401,6 +401,7 @@ __global__ void finalize_kernel(int op, T *__restrict__ B, int64_t ldb, int64_t 
                                 const int *__restrict__ e, const int *__restrict__ Etab,
                                 double *__restrict__ scales, int *__restrict__ scale_exp,
                                 const int64_t *__restrict__ diag_row) {
+    pdl_wait();
     int lane = threadIdx.x & 31;
     int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;

@@ -178,7 +178,7 @@ int launch_gemm(const GemmArgs<T> &g) {
     const int64_t ntiles = tiles_m * tiles_n;
     const int grid = int(std::min<int64_t>(ntiles, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
     ProfScope ps(PK_GEMM, flops);
-    kern<<<grid, kWsThreads, smem, g_stream>>>(g, int(tiles_m), int(ntiles));
+    CK(launch_k(kern, dim3(grid), dim3(kWsThreads), smem, g_stream, g, int(tiles_m), int(ntiles)));
     CK_LAUNCH("gemm_ws_kernel");
     return 0;
 }

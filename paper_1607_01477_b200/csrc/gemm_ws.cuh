@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             }
     }
     __syncthreads();
+    pdl_wait();
 
     if (warp < 4) {
         // ------------------------------------------------------------------ producers

@@ -26,6 +26,7 @@ struct LanczosState {
 __global__ void copy_init_rhs_kernel(const cplx *__restrict__ src, cplx *__restrict__ dst, int64_t m,
                                      int64_t npts, const cplx *__restrict__ shifts, double *__restrict__ G,
                                      int *__restrict__ e, int *__restrict__ nonfinite) {
+    pdl_wait();
     int lane = threadIdx.x & 31;
     int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -67,6 +68,7 @@ __global__ void lanczos_init_kernel(const cplx *__restrict__ v0, LanczosState st
 // One Lanczos step for every active point, after y = (U - zI)^{-1} v (in Y, exponent e1) and
 // w = (U - zI)^{-H} y (in W, exponent e2).
 __global__ void lanczos_step_kernel(LanczosState st, int64_t m, int64_t nslots, int it, int iters) {
+    pdl_wait();
     int lane = threadIdx.x & 31;
     int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;

@@ -354,9 +354,9 @@ int finalize(int op, int safe, T *B, int64_t ldb, int64_t m, int64_t n, int nb,
              Work &w) {
     int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
     if (blocks < 1) blocks = 1;
-    finalize_kernel<T><<<blocks, 256, 0, g_stream>>>(op, B, ldb, m, n, nb, cdiv(m, nb), rowend_dev,
-                                                      safe ? w.e : nullptr, safe ? w.Etab : nullptr,
-                                                      scales, scale_exp, diag_row);
+    CK(launch_k_lvl(2, finalize_kernel<T>, dim3(blocks), dim3(256), 0, g_stream, op, B, ldb, m, n, nb, cdiv(m, nb),
+                rowend_dev, safe ? (const int *)w.e : nullptr, safe ? (const int *)w.Etab : nullptr, scales,
+                scale_exp, diag_row));
     CK_LAUNCH("finalize_kernel");
     return 0;
 }
@@ -838,17 +838,19 @@ int spectral_cloud_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, in
     int rc = 0;
     for (int it = 0; it < iters && !rc && nact > 0; it++) {
         const int ab = int(std::min<int64_t>(cdiv(nact, 8), int64_t(g_num_sms) * 16));
-        copy_init_rhs_kernel<<<ab, 256, 0, g_stream>>>(st.V, st.Y, m, nact, zc, wN.G, wN.e, g_flag);
+        CK(launch_k_lvl(2, copy_init_rhs_kernel, dim3(ab), dim3(256), 0, g_stream, (const cplx *)st.V, st.Y, m, nact,
+                    (const cplx *)zc, wN.G, wN.e, g_flag));
         CK_LAUNCH("copy_init_rhs_kernel");
         rc = blocked_solve<cplx, true>(0, U, ldu, m, zc, 1, st.Y, m, nact, nullptr, nullptr, nb, wN, spN.U, spN.X, spN.ldu, spN.ldx);
         if (!rc) rc = finalize<cplx>(0, 1, st.Y, m, m, nact, nb, nullptr, nullptr, e1, nullptr, wN);
         if (rc) break;
-        copy_init_rhs_kernel<<<ab, 256, 0, g_stream>>>(st.Y, st.W, m, nact, nullptr, wC.G, wC.e, nullptr);
+        CK(launch_k_lvl(2, copy_init_rhs_kernel, dim3(ab), dim3(256), 0, g_stream, (const cplx *)st.Y, st.W, m, nact,
+                    (const cplx *)nullptr, wC.G, wC.e, (int *)nullptr));
         CK_LAUNCH("copy_init_rhs_kernel");
         rc = blocked_solve<cplx, true>(1, U, ldu, m, zc, 1, st.W, m, nact, nullptr, nullptr, nb, wC, spC.U, spC.X, spC.ldu, spC.ldx);
         if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, nact, nb, nullptr, nullptr, e2, nullptr, wC);
         if (rc) break;
-        lanczos_step_kernel<<<ab, 256, 0, g_stream>>>(st, m, nact, it, iters);
+        CK(launch_k_lvl(2, lanczos_step_kernel, dim3(ab), dim3(256), 0, g_stream, st, m, nact, it, iters));
         CK_LAUNCH("lanczos_step_kernel");
         if (it + 1 < iters) {           // the step left v_next in W: rotate (V, V_prev, W) <- (W, V, V_prev)
             cplx *t = st.Vp;

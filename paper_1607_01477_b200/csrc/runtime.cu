@@ -17,7 +17,7 @@ char g_errmsg[512] = "no error";
 int g_num_sms = 0;
 bool g_debug_sync = getenv("MSTRSM_DEBUG_SYNC") != nullptr;   // synchronise + log after each diag launch
 int g_diag_force_fb = getenv("MSTRSM_DIAG_FORCE_FALLBACK") != nullptr;   // testing: synchronous diag path
-int g_pdl = [] { const char *e = getenv("MSTRSM_PDL"); return (e && e[0] == '0') ? 0 : 1; }();   // default on
+int g_pdl = [] { const char *e = getenv("MSTRSM_PDL"); return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2; }();
 static std::mutex g_mu;
 bool g_prof = false;
 std::vector<ProfRec> g_prof_recs;

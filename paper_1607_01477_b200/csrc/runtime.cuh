@@ -28,11 +28,13 @@ extern bool g_debug_sync;
 extern int g_diag_force_fb;
 extern int g_pdl;            // MSTRSM_PDL: programmatic dependent launch of the diag / GEMM kernels
 
-// Launch with the programmatic-stream-serialization attribute when g_pdl is set: the grid may be
+// Launch with the programmatic-stream-serialization attribute when g_pdl >= lvl (1: the diagonal
+// and update-GEMM kernels, 2: also the solve's finalize and the Lanczos kernels): the grid may be
 // scheduled while the preceding kernel in the stream drains; the kernel calls pdl_wait() before
 // touching global memory, which returns once that kernel has completed and its writes are visible.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+cudaError_t launch_k_lvl(int lvl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                         Args &&...args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -40,11 +42,16 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl >= lvl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    return launch_k_lvl(1, kern, grid, block, smem, st, std::forward<Args>(args)...);
+}
+
 
 int set_cuda_error(cudaError_t e, const char *where);
 cudaError_t last_cuda_error();   // the error recorded by the last set_cuda_error on this thread
