@@ -208,25 +208,72 @@ def trevc_z_cols(T, ldt, m, cols_host, ncols, Z, ldz, scales, scale_exp, nb):
     _call("trevc_z_cols", _ptr(T), ldt, m, p, ncols, _ptr(Z), ldz, _ptr(scales), _ptr(scale_exp), nb)
 
 
+def _check_host_square(A, m: int, name: str) -> int:
+    """A host matrix the C ABI reads as column-major complex128 with leading dimension
+    A.shape[0] >= m and at least m columns; returns that leading dimension."""
+    if not isinstance(A, np.ndarray):
+        raise TypeError(f"{name} must be a numpy array")
+    if A.dtype != np.complex128:
+        raise TypeError(f"{name} must be complex128 (got {A.dtype})")
+    if A.ndim != 2 or not A.flags.f_contiguous:
+        raise ValueError(f"{name} must be a 2-D Fortran-ordered (column-major) array")
+    if A.shape[0] < max(1, m) or A.shape[1] < m:
+        raise ValueError(f"{name} has shape {A.shape}; need at least ({m}, {m})")
+    return int(A.shape[0])
+
+
+def _check_host_vec(v, m: int, dtype, name: str):
+    if v is None:
+        return
+    if not isinstance(v, np.ndarray) or v.dtype != dtype or v.ndim != 1 or not v.flags.c_contiguous:
+        raise TypeError(f"{name} must be a contiguous 1-D numpy {np.dtype(dtype).name} array")
+    if v.shape[0] < m:
+        raise ValueError(f"{name} has length {v.shape[0]}; need at least {m}")
+
+
 def trevc_z_host(T_host: np.ndarray, m: int, Z_host: np.ndarray, scales_host=None, exp_host=None, nb=0):
-    """Host-buffer end-to-end entry (numpy complex128 Fortran arrays, blocking)."""
+    """Host-buffer end-to-end entry (numpy complex128 Fortran arrays, blocking).  The arrays are
+    checked here (dtype, column-major order, shape, lengths) because the C ABI reads and writes
+    them through raw pointers."""
+    ldt = _check_host_square(T_host, m, "T_host")
+    ldz = _check_host_square(Z_host, m, "Z_host")
+    if not Z_host.flags.writeable:
+        raise ValueError("Z_host must be writeable")
+    _check_host_vec(scales_host, m, np.float64, "scales_host")
+    _check_host_vec(exp_host, m, np.int32, "exp_host")
     lib = load()
     _bind_stream(lib)
     ptr = lambda a: a.ctypes.data_as(c_vp) if a is not None else None
-    _check(lib.trevc_z_host(ptr(T_host), T_host.shape[0], m, ptr(Z_host), Z_host.shape[0],
-                            ptr(scales_host), ptr(exp_host), nb), "trevc_z_host")
+    _check(lib.trevc_z_host(ptr(T_host), ldt, m, ptr(Z_host), ldz, ptr(scales_host), ptr(exp_host), nb),
+           "trevc_z_host")
 
 
 def trevc_z_host_batch(T_hosts, m: int, Z_hosts, scales_hosts=None, exp_hosts=None, nb=0):
     """Batched host-buffer entry (lists of numpy complex128 Fortran arrays, blocking): problem
-    k's solve overlaps k+1's upload and k-1's download."""
+    k's solve overlaps k+1's upload and k-1's download.  Every problem must share one leading
+    dimension for T and one for Z (the C ABI takes one ldt and one ldz)."""
+    n = len(T_hosts)
+    if len(Z_hosts) != n:
+        raise ValueError("T_hosts and Z_hosts must have the same length")
+    for lst, nm in ((scales_hosts, "scales_hosts"), (exp_hosts, "exp_hosts")):
+        if lst is not None and len(lst) != n:
+            raise ValueError(f"{nm} must have one entry per problem")
+    ldt = ldz = 1
+    for k in range(n):
+        lt = _check_host_square(T_hosts[k], m, f"T_hosts[{k}]")
+        lz = _check_host_square(Z_hosts[k], m, f"Z_hosts[{k}]")
+        if not Z_hosts[k].flags.writeable:
+            raise ValueError(f"Z_hosts[{k}] must be writeable")
+        if k == 0:
+            ldt, ldz = lt, lz
+        elif lt != ldt or lz != ldz:
+            raise ValueError("every problem of a batch must have the same leading dimensions")
+        _check_host_vec(scales_hosts[k] if scales_hosts is not None else None, m, np.float64, f"scales_hosts[{k}]")
+        _check_host_vec(exp_hosts[k] if exp_hosts is not None else None, m, np.int32, f"exp_hosts[{k}]")
     lib = load()
     _bind_stream(lib)
-    n = len(T_hosts)
-    assert len(Z_hosts) == n
     arr = lambda lst: (c_vp * n)(*[a.ctypes.data if a is not None else None for a in lst]) if lst is not None else None
-    _check(lib.trevc_z_host_batch(arr(T_hosts), T_hosts[0].shape[0] if n else 1, m, arr(Z_hosts),
-                                  Z_hosts[0].shape[0] if n else 1, arr(scales_hosts), arr(exp_hosts), n, nb),
+    _check(lib.trevc_z_host_batch(arr(T_hosts), ldt, m, arr(Z_hosts), ldz, arr(scales_hosts), arr(exp_hosts), n, nb),
            "trevc_z_host_batch")
 
 

@@ -1,0 +1,452 @@
+// diag_fast.cuh -- a.3 diagonal-block multi-shift (safe) solve + a.4 column bound: the chunked,
+// warp-specialised kernel of the standard solve (op N and op C, real and complex).
+//
+// Same operation and outputs as diag_kernel (diag_kernel.cuh, which stays as the generalized
+// solve's kernel and as the synchronous fallback): for one block I1 and every active column j
+//   plain:  Alg. 1 on U(I1,I1) - s_j I
+//   safe :  Alg. 4 on U(I1,I1) - s_j I with block-local bounds (R5),
+//           then steps (ii) and (iii) of Alg. 5.
+// What differs is how the work is laid out:
+//
+//  * Chunks.  Lane r of an LPC-lane group owns the solve rows sc = r + LPC t (t < RPL).  Slot t
+//    of the group is a chunk of LPC consecutive rows.  Within a chunk the row step is
+//        x_l = y_l / d_l (owner's lane, shuffled to the group),  y(rows < l) -= U(rows, l) x_l
+//    and the chunk's own slot is updated by every lane with no select: the diagonal block is
+//    staged as a PADDED triangle whose column l is zero from row l to the end of l's chunk, so
+//    lanes whose row is already solved (or is l itself) subtract x_l * 0.  The owner's quotient is
+//    recomputed once at the end of the chunk from its (then final) y_l, bit-identical to the one
+//    shuffled.
+//  * Own frame.  The guarded loop of Alg. 4 only scales the whole vector by powers of two
+//    (P:287), so its values are the unscaled substitution's values times 2^-K exactly
+//    (K = exponents taken so far; barring subnormals, R27).  The registers hold the unscaled
+//    values times 2^-F for a frame F of this kernel's own choosing: when the largest |x| of a
+//    group passes 2^600 the group's registers are multiplied by 2^-s (s = that exponent) and
+//    F += s.  The frame never depends on the paper's decisions, so the substitution never waits
+//    for them.
+//  * Replay warps.  Alg. 4's decisions are a sequential scalar chain per column.
+//    The substitution warps record |x_l| (once per chunk, with the frame it was read in) in
+//    shared memory and arrive on the chunk's mbarrier; one replay warp per 32 columns of the CTA
+//    (one lane per column, instead of LPC lanes repeating the same chain) follows one chunk
+//    behind and evaluates, in the paper's frame |x_l| = ax 2^(F - K):
+//        |y_l| >= Omega |d_l|  <=>  |x_l| >= Omega (to rounding, R27)  ->  k1 = minpow2(|x_l|, Omega)
+//        M = 2^-k1 |x_l|,  g = 2^-k1 g + M cnl(l),  g >= Omega  ->  k2 = minpow2(g, Omega)
+//    and hands K back through the "done" mbarrier.  The substitution warps then take their
+//    registers to the paper's frame with one exact power-of-two product, 2^(F - K).  A group
+//    whose values stop being finite (growth of more than ~2^400 inside one chunk: tiny pivots)
+//    is handed to the synchronous fallback (diag_kernel<FB>).
+#pragma once
+#include "diag_kernel.cuh"
+
+namespace mstrsm {
+
+// Offset of column l of the padded triangle (column l holds LPC (floor(l/LPC) + 1) elements:
+// rows 0 .. l-1 of U and zeros to the end of l's chunk).
+__host__ __device__ __forceinline__ int64_t padtri_off(int l, int lpc) {
+    const int64_t t = l / lpc, r = l % lpc;
+    return int64_t(lpc) * lpc * t * (t + 1) / 2 + r * lpc * (t + 1);
+}
+
+// CTA shape of an instantiation: up to kSub substitution warps (G columns each) and, for the
+// safe variants, one replay warp per 32 of their columns.
+// The CTA holds kWarps warps (a multiple of 4, so the register budget per thread is
+// 65536 / (32 kWarps): 168 for the complex RPL = 16 layouts, 128 otherwise).
+template <typename T, int LPC, int RPL, bool SAFE> struct DiagW {
+    static constexpr int G = 32 / LPC;
+    static constexpr int kWarps = (S<T>::cplx_ && RPL >= 16) ? 12 : 16;
+    static constexpr int sub_fit(int s) { return (s + (SAFE ? (s * G + 31) / 32 : 0)) <= kWarps ? s : sub_fit(s - 1); }
+    static constexpr int kSub = sub_fit(kWarps);
+    static constexpr int kRep = SAFE ? (kSub * G + 31) / 32 : 0;
+    static constexpr int kThreads = kWarps * 32;
+};
+__host__ __device__ inline int diagw_nrep(int nsub, int lpc, bool safe) { return safe ? (nsub * (32 / lpc) + 31) / 32 : 0; }
+
+// Shared-memory carve-up (byte offsets, 16-aligned): padded triangle, diagonal, cnl, and for the
+// safe variants the replay records |x| (row-major: [sc][column slot]), the chunk frames, the
+// per-column g0 / live row count / K, and RPL + 1 mbarriers.
+struct DiagWSmem {
+    int64_t pk, dg, cn, rec, fp, g0, lrows, kout, bar, total;
+};
+__host__ __device__ inline DiagWSmem diagw_smem(int nfull, int lpc, int rpl, int esize, int ncol_cta, bool safe) {
+    auto al = [](int64_t v) { return (v + 15) & ~int64_t(15); };
+    DiagWSmem s{};
+    s.pk = 0;
+    s.dg = al(padtri_off(nfull, lpc) * esize);
+    s.cn = al(s.dg + int64_t(nfull) * esize);
+    s.rec = al(s.cn + int64_t(nfull) * 8);
+    if (!safe) { s.total = s.rec; return s; }
+    s.fp = al(s.rec + int64_t(lpc) * rpl * ncol_cta * 8);
+    s.g0 = al(s.fp + int64_t(rpl) * ncol_cta * 4);
+    s.lrows = al(s.g0 + int64_t(ncol_cta) * 8);
+    s.kout = al(s.lrows + int64_t(ncol_cta) * 4);
+    s.bar = al(s.kout + int64_t(ncol_cta) * 4);
+    s.total = s.bar + int64_t(rpl + 1) * 8;
+    return s;
+}
+
+// The exponent of a non-negative double (biased; 0 for zero / subnormal, 2047 for inf / NaN).
+__device__ __forceinline__ int bexp(double v) { return (__double2hiint(v) >> 20) & 0x7ff; }
+// v with its biased exponent replaced by be (1 <= be <= 2046; v normal, non-negative).
+__device__ __forceinline__ double with_bexp(double v, int be) {
+    return __hiloint2double((__double2hiint(v) & 0x800fffff) | (be << 20), __double2loint(v));
+}
+// y := 2^s y for any integer s (one product when the factor is a normal double).
+template <typename T, int N>
+__device__ __forceinline__ void scale_pow2(T (&y)[N], int s) {
+    if (s >= -1022 && s <= 1023) {
+        const double p = pow2i(s);
+#pragma unroll
+        for (int t = 0; t < N; t++) {
+            if constexpr (S<T>::cplx_) y[t] = make_double2(__dmul_rn(y[t].x, p), __dmul_rn(y[t].y, p));
+            else y[t] = __dmul_rn(y[t], p);
+        }
+    } else {
+        scale_all_any(y, s);
+    }
+}
+
+template <int LPC>
+__device__ __forceinline__ int group_imax(int v) {
+#pragma unroll
+    for (int o = 1; o < LPC; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o, LPC));
+    return v;
+}
+
+__device__ __forceinline__ void dw_mbar_init(uint64_t *b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void dw_mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void dw_mbar_wait(uint64_t *b, int parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    } while (!done);
+}
+
+// Chunked row loop of one column group.  REC = false: Alg. 1 (the plain solve and the unguarded
+// branch of Alg. 4), bit-identical to diag_subst.  REC = true: the guarded loop's substitution in
+// the kernel's own frame, recording |x| of every row (rec[sc * ldrec]) and the frame of every
+// chunk (fp[t * ldrec], lane 0) for the replay warps; returns false when the group's values
+// stopped being finite.  Every chunk's mbarrier is arrived on (safe variants), solved or skipped.
+template <typename T, int LPC, int RPL, bool SAFE, bool REC, bool CONJ, typename PivF>
+__device__ __forceinline__ bool diagw_rows(T (&y)[RPL], PivF pivot, const T *__restrict__ pk, int rl, int nmax,
+                                           bool guarded, double gub, double *rec, int *fp, int ldrec,
+                                           uint64_t *bars, int &Fout) {
+    typedef S<T> ST;
+    int F = 0;
+    bool nonfinite = false;
+    auto uget = [&](const T *p) -> T {
+        if constexpr (CONJ) return ST::conj(*p);   // op C: L = U^H staged unconjugated
+        else return *p;
+    };
+    if constexpr (REC) {                                                   // initial frame
+        const int e0 = bexp(gub);
+        const bool need = guarded && e0 > 1623 && e0 < 2047;
+        if (__any_sync(0xffffffffu, need)) {
+            const int s = need ? min(e0 - 1023, 1022) : 0;
+            scale_all<true>(y, s);
+            F = s;
+        }
+    }
+#pragma unroll
+    for (int t = RPL - 1; t >= 0; t--) {
+        if (t * LPC < nmax) {                                              // warp-uniform
+            Piv<T> pvt;                                                    // own row of slot t
+            pvt.make(pivot(t * LPC + rl));
+            const int rr_hi = min(LPC - 1, nmax - 1 - t * LPC);           // rows >= nmax skipped
+            const int kStride = LPC * (t + 1);                            // padded column length
+            const T *pc = pk + (LPC * LPC * t * (t + 1) / 2 + rl) + rr_hi * kStride;
+#pragma unroll 1
+            for (int rr = rr_hi; rr >= 0; rr--, pc -= kStride) {
+                const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);      // P:82 / P:297
+                y[t] = ST::fnms(y[t], xl, uget(pc + LPC * t));             // zero for rows >= l
+#pragma unroll
+                for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xl, uget(pc + LPC * t2));
+            }
+            const T xo = pvt.apply(y[t]);                                  // = the shuffled x_l
+            y[t] = xo;
+            if constexpr (REC) {
+                const double ax = modv(xo);
+                nonfinite |= !(ax <= 1.7976931348623157e308);
+                rec[(t * LPC + rl) * ldrec] = ax;
+                if (rl == 0) fp[t * ldrec] = F;
+                const int em = group_imax<LPC>(bexp(ax));
+                const bool need = guarded && em > 1623 && em < 2047;      // |x| >= 2^601: new frame
+                if (__any_sync(0xffffffffu, need)) {
+                    const int s = need ? min(em - 1023, 1022) : 0;
+                    scale_all<true>(y, s);
+                    F += s;
+                }
+            }
+        }
+        if constexpr (SAFE) dw_mbar_arrive(bars + t);
+    }
+    if constexpr (REC) {
+#pragma unroll
+        for (int o = 1; o < LPC; o <<= 1) nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o, LPC);
+    }
+    Fout = F;
+    return !(guarded && nonfinite);
+}
+
+// One launch = one diagonal block for the active columns [c0, c0 + ncols).  Warps 0 .. nsub-1
+// substitute (G columns each), the rest replay (safe variants).  The column loop runs in passes of
+// nsub G columns per CTA; every warp of the CTA takes part in every pass.
+template <typename T, int LPC, int RPL, bool SAFE, int OP>
+__global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_kernel(DiagArgs<T> a) {
+    typedef S<T> ST;
+    constexpr int G = 32 / LPC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nfull = int(a.hi - a.lo);
+    const int64_t ncols = a.ncols;
+    const int nsub = a.nsub, C = nsub * G;
+    const DiagWSmem L = diagw_smem(nfull, LPC, RPL, int(sizeof(T)), C, SAFE);
+    T *pk = reinterpret_cast<T *>(smem_raw + L.pk);
+    T *dg = reinterpret_cast<T *>(smem_raw + L.dg);
+    double *cn = reinterpret_cast<double *>(smem_raw + L.cn);
+    double *s_rec = reinterpret_cast<double *>(smem_raw + L.rec);
+    int *s_fp = reinterpret_cast<int *>(smem_raw + L.fp);
+    double *s_g0 = reinterpret_cast<double *>(smem_raw + L.g0);
+    int *s_lrows = reinterpret_cast<int *>(smem_raw + L.lrows);
+    int *s_k = reinterpret_cast<int *>(smem_raw + L.kout);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar);   // [0, RPL): chunks, [RPL]: done
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+
+    // ---- stage U(I1,I1) as the padded triangle (solve coordinates), its diagonal and cnl.  U and
+    //      cnl are never written during a solve, so a launch after the solve's first one stages
+    //      them before waiting for the preceding grid (a.early) ----
+    if (!a.early) pdl_wait();
+    for (int idx = tid; idx < nfull * 128; idx += nth) {
+        const int cq = idx >> 7, r = idx & 127;                            // U(lo + r, lo + cq)
+        if (r < cq) {
+            const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;
+            if (OP == 0) cp_async<sizeof(T)>(pk + padtri_off(cq, LPC) + r, src, true);
+            else cp_async<sizeof(T)>(pk + padtri_off(nfull - 1 - r, LPC) + (nfull - 1 - cq), src, true);
+        }
+    }
+    for (int idx = tid; idx < nfull * LPC; idx += nth) {                 // zeros from row l down
+        const int l = idx / LPC, r = (l / LPC) * LPC + idx % LPC;
+        if (r >= l) pk[padtri_off(l, LPC) + r] = ST::zero();
+    }
+    for (int c = tid; c < nfull; c += nth) {
+        const int64_t row = OP == 0 ? a.lo + c : a.hi - 1 - c;
+        const T u = a.U[row + row * a.ldu];
+        dg[c] = OP == 0 ? u : ST::conj(u);
+        cn[c] = SAFE ? a.cnl[row] : 0.0;
+    }
+    if (SAFE && tid == 0) {
+        for (int t = 0; t < RPL; t++) dw_mbar_init(bars + t, nsub * 32);
+        dw_mbar_init(bars + RPL, diagw_nrep(nsub, LPC, true) * 32);
+    }
+    cp_async_commit();
+    if (a.early) pdl_wait();
+    __syncthreads();                                                       // diagonal, cnl, barriers
+    bool staged = false;
+    auto stage_wait = [&]() { cp_async_wait<0>(); __syncthreads(); staged = true; };
+
+    const int64_t cstride = int64_t(gridDim.x) * C;
+    if (warp >= nsub) {
+        // =========================== replay warp: one lane per column slot ===========================
+        if constexpr (SAFE) {
+            stage_wait();
+            const int c = (warp - nsub) * 32 + lane;
+            int pass = 0;
+            for (int64_t cb = int64_t(blockIdx.x) * C; cb < ncols; cb += cstride, pass++) {
+                const int par = pass & 1;
+                int K = 0, lrows = 0;
+                double g = 0.0;
+#pragma unroll 1
+                for (int t = RPL - 1; t >= 0; t--) {
+                    dw_mbar_wait(bars + t, par);
+                    if (t == RPL - 1 && c < C) { g = s_g0[c]; lrows = s_lrows[c]; }
+                    if (!__any_sync(0xffffffffu, lrows > t * LPC)) continue;
+                    const int Fp = lrows > t * LPC ? s_fp[t * C + c] : 0;
+#pragma unroll 4
+                    for (int rr = LPC - 1; rr >= 0; rr--) {
+                        const int sc = t * LPC + rr;
+                        const bool live = sc < lrows;
+                        const double ax = live ? s_rec[sc * C + c] : 0.0;
+                        // paper frame |x_l| = ax 2^(Fp - K); a row that is not live leaves g and K
+                        // unchanged exactly (M = 0, k1 = k2 = 0: g * 1 + 0)
+                        const int ea = bexp(ax);
+                        const int dK = Fp - K;
+                        const int ep = ea + dK;                           // biased exponent, paper frame
+                        const bool t1 = live && ea != 0 && ep >= 1993;    // |x_l| >= 2^970
+                        const int k1 = t1 ? ep - 1992 : 0;
+                        double M, gs;
+                        if (unsigned(dK + 1022) <= 2045u && k1 <= 1022) {
+                            M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
+                            gs = __dmul_rn(g, pow2i(-k1));                // P:287 applied to g
+                        } else {                                          // extreme frames (rare)
+                            M = t1 ? with_bexp(ax, 1992) : mulp2_any(ax, dK);
+                            gs = mulp2n(g, k1);
+                        }
+                        M = live ? M : 0.0;
+                        double gn = __dadd_rn(gs, __dmul_rn(M, cn[sc < nfull ? sc : 0]));
+                        const bool t2 = live && gn >= kOmega;
+                        const int k2 = t2 ? bexp(gn) - 1992 : 0;
+                        g = __dmul_rn(gn, pow2i(-k2));
+                        K += k1 + k2;
+                    }
+                }
+                if (c < C) s_k[c] = K;
+                dw_mbar_arrive(bars + RPL);
+            }
+        }
+        if (!staged) stage_wait();
+        return;
+    }
+
+    // =============================== substitution warps ===============================
+    const int grp = lane / LPC, rl = lane % LPC;
+    const int c = warp * G + grp;                                         // column slot in the CTA
+    const double delta = SAFE ? a.delta[0] : 0.0;
+    const double Pb = SAFE ? a.P[a.b] : 0.0;
+    int pass = 0;
+    for (int64_t cb = int64_t(blockIdx.x) * C; cb < ncols; cb += cstride, pass++) {
+        const int64_t q = cb + c;
+        const bool valid = q < ncols;
+        const int64_t j = a.c0 + (valid ? q : 0);
+        const int64_t r = valid ? ((OP == 0 && a.rowend) ? a.rowend[j] : a.m) : 0;
+        const bool active = valid && r > a.lo;
+        if (SAFE && valid && !active && rl == 0) a.dblk[j] = 0;           // inactive column: no rescale
+        const int nrow = active ? (OP == 0 ? int((a.hi < r ? a.hi : r) - a.lo) : nfull) : 0;
+        int nmax = nrow;
+#pragma unroll
+        for (int o = LPC; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        T sh = active ? a.shifts[j * a.sstride] : ST::zero();
+        if (OP == 1) sh = ST::conj(sh);
+        T *x = a.B + j * a.ldb;
+        auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
+        auto pivot = [&](int sc) -> T {                                    // d_l = U(l,l) - s_j
+            T dd = sc < nrow ? ST::sub(dg[sc], sh) : ST::real(1.0);
+            if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
+            return dd;
+        };
+        T y[RPL];
+#pragma unroll
+        for (int t = 0; t < RPL; t++) {
+            const int sc = rl + LPC * t;
+            y[t] = sc < nrow ? x[rowof(sc)] : ST::zero();
+        }
+
+        bool guarded = false;
+        double g0 = 0.0, gub = 0.0;
+        if (SAFE) {
+            // ---- precheck, eqs. (4)-(5), as diag_kernel: upper bounds of |y| and
+            //      the suffix products, lower bounds of |d| (a column the exact test would pass
+            //      may take the guarded loop, never the reverse) ----
+#pragma unroll
+            for (int t = 0; t < RPL; t++)
+                if (rl + LPC * t < nrow) gub = fmax(gub, maxabs(y[t]));
+            gub = group_max<LPC>(gub);
+            if constexpr (ST::cplx_) gub = __dmul_ru(gub, 1.4142135623730951);
+            double carry = gub;
+            bool okM = true;
+#pragma unroll 1
+            for (int t = RPL - 1; t >= 0; t--) {
+                if (t * LPC >= nmax) continue;
+                const int sc = t * LPC + rl;
+                const bool in = sc < nrow;
+                const double ad = maxabs(pivot(sc));
+                const double tf = in ? __dadd_ru(1.0, __ddiv_ru(cn[sc < nfull ? sc : 0], ad)) : 1.0;
+                double suf = tf;
+#pragma unroll
+                for (int o = 1; o < LPC; o <<= 1) {
+                    const double v = __shfl_down_sync(0xffffffffu, suf, o, LPC);
+                    if (rl + o < LPC) suf = __dmul_ru(suf, v);
+                }
+                double exc = __shfl_down_sync(0xffffffffu, suf, 1, LPC);
+                if (rl == LPC - 1) exc = 1.0;
+                const double gl = __dmul_ru(carry, exc);
+                okM = okM && (!in || gl < __dmul_rn(kOmega, ad));
+                carry = __dmul_ru(carry, __shfl_sync(0xffffffffu, suf, 0, LPC));
+            }
+#pragma unroll
+            for (int o = 1; o < LPC; o <<= 1) {
+                const bool other = __shfl_xor_sync(0xffffffffu, okM, o, LPC);
+                okM = okM && other;
+            }
+            guarded = active && !(okM && carry < kOmega);
+            if (__any_sync(0xffffffffu, guarded)) {                        // g := ||y(I1)||_inf
+#pragma unroll
+                for (int t = 0; t < RPL; t++)
+                    if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
+                g0 = group_max<LPC>(g0);
+            }
+            if (rl == 0) {                                                 // the replay's inputs
+                s_g0[c] = g0;
+                s_lrows[c] = guarded ? nrow : 0;
+            }
+        }
+
+        if (!staged) stage_wait();
+        int F = 0;
+        bool handed = false;
+        if (SAFE && __any_sync(0xffffffffu, guarded)) {
+            const bool ok = diagw_rows<T, LPC, RPL, SAFE, true, OP == 1>(y, pivot, pk, rl, nmax, guarded, gub,
+                                                                         s_rec + c, s_fp + c, C, bars, F) &&
+                            !(a.force_fb && guarded);
+            if (!ok) {                                                     // hand the column over
+                handed = true;
+                if (rl == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = int(j);
+            }
+        } else {
+            diagw_rows<T, LPC, RPL, SAFE, false, OP == 1>(y, pivot, pk, rl, nmax, false, 0.0, s_rec + c, s_fp + c,
+                                                          C, bars, F);
+        }
+
+        if (SAFE) {
+            dw_mbar_wait(bars + RPL, pass & 1);                            // K from the replay warp
+            const int kt = s_k[c];
+            if (!handed && F != kt) scale_pow2(y, F - kt);                 // to the paper's frame
+            int ej = 0;
+            double Gj = 0.0;
+            if (active) { ej = a.e[j]; Gj = a.G[j]; }
+            if (kt > 0) {                                                  // P:376-386, step (ii)
+                ej -= kt;
+                Gj = mulp2n(Gj, kt);
+            }
+            double xm = 0.0;
+#pragma unroll
+            for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
+            xm = group_max<LPC>(xm);
+            Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
+            int k3 = 0;
+            if (Gj >= kOmega) {
+                k3 = minpow2_bits(Gj, kOmega);
+                scale_all<false>(y, k3);
+                ej -= k3;
+                Gj = mulp2n(Gj, k3);
+            }
+            if (active && rl == 0 && !handed) {
+                a.e[j] = ej;
+                a.G[j] = Gj;
+                a.dblk[j] = -(kt + k3);
+                a.Etab[a.b * a.n + j] = ej;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < RPL; t++) {
+            const int sc = rl + LPC * t;
+            if (sc < nrow && !handed) x[rowof(sc)] = y[t];
+        }
+        if constexpr (ST::cplx_) {  // operand sums for the 3M update GEMM
+            if (a.Xsum && valid && !handed) {
+                double *xs = a.Xsum + j * a.ldxs;
+#pragma unroll
+                for (int t = 0; t < RPL; t++) {
+                    const int sc = rl + LPC * t;
+                    if (sc < nfull) xs[rowof(sc) - a.lo] = __dadd_rn(y[t].x, y[t].y);
+                }
+            }
+        }
+    }
+    if (!staged) stage_wait();
+}
+
+}  // namespace mstrsm

@@ -45,6 +45,8 @@ struct DiagArgs {
     double *G; int *e; int *dblk; int *Etab;
     int *fb_list; int *fb_count;   // columns handed to the synchronous fallback (safe variants)
     int force_fb;                  // testing: hand every guarded column to the fallback
+    int early;                     // U / cnl may be staged before waiting for the preceding grid
+    int nsub;                      // diagw_kernel: substitution warps per CTA (set by the launcher)
     // generalized solve (Alg. 7/8, op N): V with its norms, and the output C = -lambda_j X(I1,j)
     // (n_b x n, column j at Cbuf + j * ldc) that the V product of the update reads
     const T *V; int64_t ldv;
@@ -464,6 +466,8 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
     static_assert(!GEN || OP == 0, "the generalized solve is op N only");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nfull = int(a.hi - a.lo);
+    pdl_wait();                    // before any global access, fb_count included (it is written
+                                   // by the main launch that precedes this one in the stream)
     const int64_t ncols = FB ? int64_t(*a.fb_count) : a.ncols;
     if (ncols == 0) return;
     const int64_t npk = int64_t(nfull) * (nfull - 1) / 2 + 128;
@@ -474,7 +478,6 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
     double *cn = reinterpret_cast<double *>(dgV + nfull);
     double *cnV = cn + (GEN ? nfull : 0);
 
-    pdl_wait();
     // ---- stage U(I1,I1) (packed, solve coordinates), its diagonal and cnl ----
     const int tid = threadIdx.x, nth = blockDim.x;
     {

@@ -5,6 +5,7 @@
 #include <stdlib.h>
 
 #include "runtime.cuh"
+#include "diag_fast.cuh"
 
 namespace mstrsm {
 namespace rt {
@@ -84,7 +85,7 @@ int launch_diag_pair(const DiagArgs<T> &a) {
 }
 
 template <typename T, bool SAFE, int OP>
-int launch_diag(const DiagArgs<T> &a, int nb) {
+int launch_diag_old(const DiagArgs<T> &a, int nb) {
     // Whole passes of the grid over the columns: a pass of the RPL = 16 layout takes about 1.2x
     // one of the RPL = 8 layout (c5 launch list, profiles/r01), so pick the cheaper pass count.
     auto passes = [&](int lpc, int rpl) {
@@ -102,6 +103,110 @@ int launch_diag(const DiagArgs<T> &a, int nb) {
     if (c4 * passes(32, 4) < 10 * passes(16, 8) && c4 * passes(32, 4) < c16 * passes(8, 16))
         return launch_diag_pair<T, 32, 4, SAFE, OP, false>(a);
     return few(8) ? launch_diag_pair<T, 16, 8, SAFE, OP, false>(a) : launch_diag_pair<T, 8, 16, SAFE, OP, false>(a);
+}
+
+// MSTRSM_DIAG_OLD=1: the round-1 row loop (diag_kernel) for the standard solve as well.
+inline bool diag_old() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_DIAG_OLD");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+// MSTRSM_DIAG_LPC=k forces the lanes per column of the chunked kernel (testing / tuning).
+inline int diag_force_lpc() {
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("MSTRSM_DIAG_LPC");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <typename T, int LPC, int RPL, bool SAFE, int OP>
+int launch_diagf_k(const DiagArgs<T> &a0) {
+    auto kern = diagw_kernel<T, LPC, RPL, SAFE, OP>;
+    typedef DiagW<T, LPC, RPL, SAFE> W;
+    constexpr int G = W::G;
+    const int nfull = int(a0.hi - a0.lo);
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    const int64_t groups = cdiv(a0.ncols, G);
+    const int64_t sms = g_cta_cap > 0 ? g_cta_cap : g_num_sms;
+    // one CTA per SM; equal passes: as many substitution warps per CTA as the pass count needs
+    const int64_t npass = cdiv(groups, sms * W::kSub);
+    const int nsub = int(std::max<int64_t>(1, std::min<int64_t>(W::kSub, cdiv(groups, sms * npass))));
+    const int threads = (nsub + diagw_nrep(nsub, LPC, SAFE)) * 32;
+    const size_t smem = size_t(diagw_smem(nfull, LPC, RPL, sizeof(T), nsub * G, SAFE).total);
+    int grid = int(std::min<int64_t>(cdiv(groups, nsub), sms));
+    if (grid < 1) grid = 1;
+    DiagArgs<T> a = a0;
+    a.nsub = nsub;
+    const double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
+    ProfScope ps(PK_DIAG, fl);
+    CK(launch_k(kern, dim3(grid), dim3(threads), smem, g_stream, a));
+    CK_LAUNCH("diagw_kernel");
+    return 0;
+}
+
+// The chunked kernel, then (safe) the synchronous fallback launch of diag_kernel, which exits at
+// once unless columns were handed over (device-side count, no host synchronisation).
+template <typename T, int LPC, int RPL, bool SAFE, int OP>
+int launch_diagf_pair(const DiagArgs<T> &a, int nb) {
+    if (int rc = launch_diagf_k<T, LPC, RPL, SAFE, OP>(a)) return rc;
+    if (g_debug_sync) {
+        cudaError_t e = cudaStreamSynchronize(g_stream);
+        int cnt = -1;
+        if (SAFE) cudaMemcpy(&cnt, a.fb_count, 4, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[mstrsm debug] diagf<%d,%d> block %lld main done (%s), ncols %lld, handed %d\n", LPC, RPL,
+                (long long)a.b, cudaGetErrorString(e), (long long)a.ncols, cnt);
+    }
+    if constexpr (SAFE) {
+        const int64_t cap = std::min<int64_t>(a.ncols, int64_t(g_num_sms) * 32);
+        if (nb <= 16) return launch_diag_k<T, 1, 16, SAFE, OP, true, false>(a, cap);
+        if (nb <= 32) return launch_diag_k<T, 2, 16, SAFE, OP, true, false>(a, cap);
+        if (nb <= 64) return launch_diag_k<T, 4, 16, SAFE, OP, true, false>(a, cap);
+        return launch_diag_k<T, 8, 16, SAFE, OP, true, false>(a, cap);
+    }
+    return 0;
+}
+
+// Layout of the chunked kernel: LPC lanes per column, RPL rows per lane (LPC RPL >= n_b).  Fewer
+// lanes per column pack more columns into a warp (the per-row chain -- quotient, shuffle,
+// replay -- is shared by more columns) but give each lane more rows (a longer update per row)
+// and need more registers (fewer warps per SM).  Among the layouts that cover the active columns
+// in the fewest passes of the grid, the one with the most lanes per column (the shortest row
+// step) is taken.
+template <typename T, bool SAFE, int OP>
+int launch_diag(const DiagArgs<T> &a, int nb) {
+    if (diag_old()) return launch_diag_old<T, SAFE, OP>(a, nb);
+    auto passes = [&](int lpc, int nsub) {
+        const int64_t per_pass = int64_t(g_cta_cap > 0 ? g_cta_cap : g_num_sms) * nsub * (32 / lpc);
+        return cdiv(a.ncols, per_pass);
+    };
+    const int f = diag_force_lpc();
+    if (nb <= 16) return launch_diagf_pair<T, 1, 16, SAFE, OP>(a, nb);
+    if (nb <= 32) {
+        if (f == 4 || (f == 0 && passes(4, DiagW<T, 4, 8, SAFE>::kSub) <= passes(2, DiagW<T, 2, 16, SAFE>::kSub)))
+            return launch_diagf_pair<T, 4, 8, SAFE, OP>(a, nb);
+        return launch_diagf_pair<T, 2, 16, SAFE, OP>(a, nb);
+    }
+    if (nb <= 64) {
+        const int64_t p4 = passes(4, DiagW<T, 4, 16, SAFE>::kSub), p8 = passes(8, DiagW<T, 8, 8, SAFE>::kSub),
+                      p16 = passes(16, DiagW<T, 16, 4, SAFE>::kSub);
+        if (f == 16 || (f == 0 && p16 <= std::min(p8, p4))) return launch_diagf_pair<T, 16, 4, SAFE, OP>(a, nb);
+        if (f == 8 || (f == 0 && p8 <= p4)) return launch_diagf_pair<T, 8, 8, SAFE, OP>(a, nb);
+        return launch_diagf_pair<T, 4, 16, SAFE, OP>(a, nb);
+    }
+    const int64_t p8 = passes(8, DiagW<T, 8, 16, SAFE>::kSub), p16 = passes(16, DiagW<T, 16, 8, SAFE>::kSub),
+                  p32 = passes(32, DiagW<T, 32, 4, SAFE>::kSub);
+    if (f == 32 || (f == 0 && p32 <= std::min(p16, p8))) return launch_diagf_pair<T, 32, 4, SAFE, OP>(a, nb);
+    if (f == 16 || (f == 0 && p16 <= p8)) return launch_diagf_pair<T, 16, 8, SAFE, OP>(a, nb);
+    return launch_diagf_pair<T, 8, 16, SAFE, OP>(a, nb);
 }
 
 // Generalized solve (Alg. 7/8, op N): U' = U - lambda V on the fly; n_b <= 64 (two packed

@@ -165,6 +165,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
     }
     int64_t nblk = cdiv(m, nb);
     if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));   // diag fallback counts
+    int early = 0;                             // U / cnl ready: later launches stage before the wait
     for (int64_t b = 0; b < nblk; b++) {
         Blk bl = block_rows(op, m, nb, b);
         int64_t c0 = 0;
@@ -183,10 +184,12 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         a.G = w.G; a.e = w.e; a.dblk = w.dblk; a.Etab = w.Etab;
         a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
         a.force_fb = g_diag_force_fb;
+        a.early = early;
         a.Xsum = Xsum; a.ldxs = ldxs;
         if (Xsum && rowend_dev && !rowend_sorted_host)        // inactive columns in range: zero rows
             CK(cudaMemsetAsync(Xsum + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
         int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
+        early = 1;
         if (rc) return rc;
         if (g_debug_sync) {
             cudaError_t e = cudaStreamSynchronize(g_stream);
@@ -238,6 +241,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
     const int cap_max = g_num_sms / 3;
     bool rest_pending = false;
     int diag_cap = 0;                          // CTAs the next diagonal step may use (0: all)
+    int early = 0;
     int rc = 0;
     for (int64_t b = 0; b < nblk && !rc; b++) {
         const Blk bl = block_rows(0, m, nb, b);
@@ -255,12 +259,14 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         a.G = w.G; a.e = w.e; a.dblk = dblk; a.Etab = w.Etab;
         a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
         a.force_fb = g_diag_force_fb;
+        a.early = early;
         a.Xsum = xs; a.ldxs = ldxs;
         if (xs && rowend_dev && !rowend_sorted_host)          // inactive columns in range: zero rows
             CK(cudaMemsetAsync(xs + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
         g_cta_cap = diag_cap;
         rc = launch_diag<T, true, 0>(a, nb);
         g_cta_cap = 0;
+        early = 1;
         if (rc) break;
         diag_cap = 0;
         const int64_t M = bl.lo;
