@@ -18,6 +18,12 @@
  *   - Calls are ASYNCHRONOUS on the library's current stream (mstrsm_set_stream; default
  *     the legacy default stream): they enqueue kernels and return.  Device workspace is
  *     allocated stream-ordered (cudaMallocAsync) and released stream-ordered.
+ *   - Thread and device safety: the current stream (mstrsm_set_stream), the status flag
+ *     (mstrsm_status), the error string and the library's helper streams and events are kept
+ *     per calling thread and per device (the device current at the call).  Several host
+ *     threads may call the library concurrently, each on its own stream, and one thread may
+ *     drive several GPUs.  The NCCL communicator of the multi-GPU entries is process-wide
+ *     (one process per GPU).
  *   - nb is the block size n_b of Alg. 2/3/5.  nb = 0 selects the default
  *     (64).  1 <= nb <= 128.  nb is part of the semantics of the safe variants (it sets
  *     the granularity of the growth-bound updates, R10).
@@ -157,7 +163,11 @@ int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t
 
 /* End-to-end entry with HOST buffers: copies T (pinned or pageable host memory) to the
  * device, runs trevc_z, copies Z, scales and scale_exp back, and synchronises.
- * All pointers are HOST pointers (scales / scale_exp nullable).  Blocking.            */
+ * All pointers are HOST pointers (scales / scale_exp nullable).  Blocking.
+ * Only the triangles travel (eigenvector k is zero below row k): T's upper triangle
+ * up, Z's upper triangle down, in 128-column panels.  Entries of Z_host below the diagonal are
+ * either left as the caller provided them or set to zero (those inside a panel's diagonal
+ * 128 x 128 tile); pass a zeroed Z_host to receive the full matrix Z.                    */
 int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *Z_host,
                  int64_t ldz, double *scales_host, int32_t *scale_exp_host, int nb);
 
@@ -165,8 +175,10 @@ int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_d
  * HOST buffer, pinned for the copies to overlap).  Problem k+1's upload of T (upper triangle) and
  * problem k-1's download of Z / scales / scale_exp run on two copy streams while problem k is
  * solved, with two device buffer sets in flight.  scales_host / scale_exp_host: nullable arrays
- * (or nullable entries).  Blocking.  Errors: -i for argument i (-9 also for a failed solve's
- * argument check), 1 CUDA error.                                                          */
+ * (or nullable entries).  Blocking.  Z_host[k] below the diagonal: as trevc_z_host.  Copy
+ * streams are per calling thread and device.  Errors: -i for argument i (-9 also for a failed
+ * solve's argument check), 1 CUDA error (the copy streams are drained before returning, so no
+ * copy touches the caller's buffers afterwards).                                        */
 int trevc_z_host_batch(const mstrsm_dcomplex *const *T_host, int64_t ldt, int64_t m,
                        mstrsm_dcomplex *const *Z_host, int64_t ldz, double *const *scales_host,
                        int32_t *const *scale_exp_host, int64_t count, int nb);

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
                 const int sc = t * LPC + rl;
                 const bool in = sc < nrow;
                 const double ad = maxabs(pivot(sc));
-                const double tf = in ? __dadd_ru(1.0, __ddiv_ru(cn[sc < nfull ? sc : 0], ad)) : 1.0;
+                const double tf = in ? __dadd_ru(1.0, __dmul_ru(cn[sc < nfull ? sc : 0], __drcp_ru(ad))) : 1.0;   // >= 1 + cnl/|d|
                 double suf = tf;
 #pragma unroll
                 for (int o = 1; o < LPC; o <<= 1) {

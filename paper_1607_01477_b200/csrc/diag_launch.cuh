@@ -37,11 +37,8 @@ int launch_diag_k(const DiagArgs<T> &a, int64_t ncols_max) {
     constexpr int kMaxThreads = DiagThreads<T, RPL>::value;
     constexpr int G = 32 / LPC;
     const int nfull = int(a.hi - a.lo);
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     // warps per CTA chosen so that the grid covers every SM when there are enough columns
     const size_t smem = size_t(diag_smem_bytes(nfull, sizeof(T), GEN));
     int occ1 = occupancy(kern, kMaxThreads, smem);
@@ -130,11 +127,8 @@ int launch_diagf_k(const DiagArgs<T> &a0) {
     typedef DiagW<T, LPC, RPL, SAFE> W;
     constexpr int G = W::G;
     const int nfull = int(a0.hi - a0.lo);
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     const int64_t groups = cdiv(a0.ncols, G);
     const int64_t sms = g_cta_cap > 0 ? g_cta_cap : g_num_sms;
     // one CTA per SM; equal passes: as many substitution warps per CTA as the pass count needs

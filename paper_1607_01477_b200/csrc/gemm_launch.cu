@@ -89,12 +89,9 @@ int launch_gemm(const GemmArgs<T> &g) {
     const int64_t tiles_m = cdiv(g.M, GemmCfg<T>::BM), tiles_n = cdiv(g.N, GemmCfg<T>::BN);
     if (use_classic()) {
         auto kern = gemm_update_kernel<T, OPC>;
-        static bool attr_set = false;
+        static std::atomic<uint64_t> attr_set{0};
         constexpr int smem = gemm_smem_bytes<T>();
-        if (!attr_set) {
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_set = true;
-        }
+        if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         dim3 grid{unsigned(tiles_m), unsigned(tiles_n), 1u};
         ProfScope ps(PK_GEMM, flops);
         kern<<<grid, kGemmThreads, smem, g_stream>>>(g);
@@ -126,11 +123,8 @@ int launch_gemm(const GemmArgs<T> &g) {
             }
             if (q3) {
                 auto kq = gemm_ws3q_kernel<OPC>;
-                static bool attrq = false;
-                if (!attrq) {
-                    CK(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, k3qSmemBytes));
-                    attrq = true;
-                }
+                static std::atomic<uint64_t> attrq{0};
+                if (first_on_device(attrq)) CK(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, k3qSmemBytes));
                 const int64_t tm = cdiv(g.M, k3qBM), tn = cdiv(g.N, k3qBN), nt = tm * tn;
                 const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
                 ProfScope ps(PK_GEMM, flops);
@@ -140,11 +134,8 @@ int launch_gemm(const GemmArgs<T> &g) {
                 return 0;
             }
             auto kern = gemm_ws3p_kernel<OPC>;
-            static bool attrp = false;
-            if (!attrp) {
-                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3pSmemBytes));
-                attrp = true;
-            }
+            static std::atomic<uint64_t> attrp{0};
+            if (first_on_device(attrp)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3pSmemBytes));
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
             const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
             ProfScope ps(PK_GEMM, flops);
@@ -155,11 +146,8 @@ int launch_gemm(const GemmArgs<T> &g) {
         }
         if (gemm_variant() == 0) {
             auto kern = gemm_ws3m_kernel<OPC>;
-            static bool attr3 = false;
-            if (!attr3) {
-                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3mSmemBytes));
-                attr3 = true;
-            }
+            static std::atomic<uint64_t> attr3{0};
+            if (first_on_device(attr3)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k3mSmemBytes));
             const int64_t tm = cdiv(g.M, k3mBM), tn = cdiv(g.N, k3mBN), nt = tm * tn;
             const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
             ProfScope ps(PK_GEMM, flops);
@@ -169,12 +157,9 @@ int launch_gemm(const GemmArgs<T> &g) {
         }
     }
     auto kern = gemm_ws_kernel<T, OPC>;
-    static bool attr_set = false;
+    static std::atomic<uint64_t> attr_set{0};
     constexpr int smem = gemm_ws_smem_bytes<T>();
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
-    }
+    if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t ntiles = tiles_m * tiles_n;
     const int grid = int(std::min<int64_t>(ntiles, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
     ProfScope ps(PK_GEMM, flops);

@@ -220,13 +220,10 @@ template <typename T>
 int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride, T *B, int64_t ldb,
                      int64_t n, const int64_t *rowend_dev, const std::vector<int64_t> *rowend_sorted_host, int nb,
                      Work &w, const double *Usum, double *Xsum, int64_t ldus, int ldxs) {
-    static cudaStream_t side = nullptr;
-    if (!side) CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    static cudaEvent_t ev_d = nullptr, ev_rest = nullptr;
-    if (!ev_d) {
-        CK(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
-    }
+    DevRes *res = dev_res();                    // this thread's side stream and events on this device
+    if (!res) return 1;
+    const cudaStream_t side = res->side;
+    const cudaEvent_t ev_d = res->ev_d, ev_rest = res->ev_rest;
     const cudaStream_t main_st = g_stream;
     const int64_t nblk = cdiv(m, nb);
     CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));
@@ -1153,6 +1150,51 @@ int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dc
     return trevc_qz_impl<cplx>((const cplx *)T, ldt, m, (const cplx *)Q, ldq, (cplx *)X, ldx, scales, scale_exp, nb);
 }
 
+// Host <-> device copies of the triangles the TriangEig path reads and writes: only the upper
+// triangle of T is read and only rows 0..k of eigenvector k are nonzero, so both
+// directions move 128-column panels, rows 0 .. panel end (about m^2/2 elements instead of m^2).
+static cudaError_t copy_upper_panels(cplx *dst, int64_t ldd, const cplx *src, int64_t lds, int64_t m,
+                                     cudaMemcpyKind kind, cudaStream_t st) {
+    for (int64_t c0 = 0; c0 < m; c0 += 128) {
+        const int64_t c1 = std::min<int64_t>(m, c0 + 128);
+        cudaError_t e = cudaMemcpy2DAsync(dst + c0 * ldd, ldd * sizeof(cplx), src + c0 * lds, lds * sizeof(cplx),
+                                          size_t(c1) * sizeof(cplx), size_t(c1 - c0), kind, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// Device buffers and events of the host entries; the destructor drains the copy streams (so no
+// copy still reads or writes the caller's host buffers after an error return) and frees.
+struct HostStage {
+    cudaStream_t cs = nullptr, h2d = nullptr, d2h = nullptr;
+    cplx *dT[2] = {nullptr, nullptr}, *dZ[2] = {nullptr, nullptr};
+    double *ds[2] = {nullptr, nullptr};
+    int *de[2] = {nullptr, nullptr};
+    cudaEvent_t ev[7] = {};
+    ~HostStage() {
+        if (h2d) cudaStreamSynchronize(h2d);
+        if (d2h) cudaStreamSynchronize(d2h);
+        for (int s = 0; s < 2; s++) {
+            if (dT[s]) cudaFreeAsync(dT[s], cs);
+            if (dZ[s]) cudaFreeAsync(dZ[s], cs);
+            if (ds[s]) cudaFreeAsync(ds[s], cs);
+            if (de[s]) cudaFreeAsync(de[s], cs);
+        }
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (cs) cudaStreamSynchronize(cs);
+    }
+    int alloc(int s, int64_t m) {
+        const size_t bytes = size_t(m) * m * sizeof(cplx);
+        CK(cudaMallocAsync(&dT[s], bytes, cs));
+        CK(cudaMallocAsync(&dZ[s], bytes, cs));
+        CK(cudaMallocAsync(&ds[s], m * 8, cs));
+        CK(cudaMallocAsync(&de[s], m * 4, cs));
+        return 0;
+    }
+};
+
 int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_dcomplex *Z_host, int64_t ldz,
                  double *scales_host, int32_t *scale_exp_host, int nb) {
     if (m < 0) return -3;
@@ -1162,32 +1204,16 @@ int trevc_z_host(const mstrsm_dcomplex *T_host, int64_t ldt, int64_t m, mstrsm_d
     if (!T_host) return -1;
     if (!Z_host) return -4;
     if (int rc = ensure_init()) return rc;
-    cplx *dT = nullptr, *dZ = nullptr;
-    double *ds = nullptr;
-    int *de = nullptr;
-    size_t bytes = size_t(m) * m * sizeof(cplx);
-    CK(cudaMallocAsync(&dT, bytes, g_stream));
-    CK(cudaMallocAsync(&dZ, bytes, g_stream));
-    CK(cudaMallocAsync(&ds, m * 8, g_stream));
-    CK(cudaMallocAsync(&de, m * 4, g_stream));
-    // only the upper triangle of T is ever read: copy it by 128-column panels (rows 0 .. panel end)
-    for (int64_t c0 = 0; c0 < m; c0 += 128) {
-        const int64_t c1 = std::min<int64_t>(m, c0 + 128);
-        CK(cudaMemcpy2DAsync(dT + c0 * m, m * sizeof(cplx), T_host + c0 * ldt, ldt * sizeof(cplx),
-                             size_t(c1) * sizeof(cplx), size_t(c1 - c0), cudaMemcpyHostToDevice, g_stream));
-    }
-    int rc = trevc_impl<cplx>(dT, m, m, nullptr, m, dZ, m, ds, de, nb);
+    HostStage hs;
+    hs.cs = g_stream;
+    if (int rc = hs.alloc(0, m)) return rc;
+    CK(copy_upper_panels(hs.dT[0], m, (const cplx *)T_host, ldt, m, cudaMemcpyHostToDevice, g_stream));
+    int rc = trevc_impl<cplx>(hs.dT[0], m, m, nullptr, m, hs.dZ[0], m, hs.ds[0], hs.de[0], nb);
     if (rc == 0) {
-        if (ldz == m) CK(cudaMemcpyAsync(Z_host, dZ, bytes, cudaMemcpyDeviceToHost, g_stream));
-        else CK(cudaMemcpy2DAsync(Z_host, ldz * sizeof(cplx), dZ, m * sizeof(cplx), m * sizeof(cplx), m,
-                                  cudaMemcpyDeviceToHost, g_stream));
-        if (scales_host) CK(cudaMemcpyAsync(scales_host, ds, m * 8, cudaMemcpyDeviceToHost, g_stream));
-        if (scale_exp_host) CK(cudaMemcpyAsync(scale_exp_host, de, m * 4, cudaMemcpyDeviceToHost, g_stream));
+        CK(copy_upper_panels((cplx *)Z_host, ldz, hs.dZ[0], m, m, cudaMemcpyDeviceToHost, g_stream));
+        if (scales_host) CK(cudaMemcpyAsync(scales_host, hs.ds[0], m * 8, cudaMemcpyDeviceToHost, g_stream));
+        if (scale_exp_host) CK(cudaMemcpyAsync(scale_exp_host, hs.de[0], m * 4, cudaMemcpyDeviceToHost, g_stream));
     }
-    cudaFreeAsync(dT, g_stream);
-    cudaFreeAsync(dZ, g_stream);
-    cudaFreeAsync(ds, g_stream);
-    cudaFreeAsync(de, g_stream);
     CK(cudaStreamSynchronize(g_stream));
     return rc;
 }
@@ -1210,72 +1236,43 @@ int trevc_z_host_batch(const mstrsm_dcomplex *const *T_host, int64_t ldt, int64_
         if (!Z_host[k]) return -4;
     }
     if (int rc = ensure_init()) return rc;
-    static cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-    if (!s_h2d) {
-        CK(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
-    }
-    const cudaStream_t cs = g_stream;
-    const size_t bytes = size_t(m) * m * sizeof(cplx);
-    cplx *dT[2] = {nullptr, nullptr}, *dZ[2] = {nullptr, nullptr};
-    double *ds[2] = {nullptr, nullptr};
-    int *de[2] = {nullptr, nullptr};
-    cudaEvent_t e_alloc, e_h2d[2], e_comp[2], e_d2h[2];
-    CK(cudaEventCreateWithFlags(&e_alloc, cudaEventDisableTiming));
-    for (int s = 0; s < 2; s++) {
-        CK(cudaEventCreateWithFlags(&e_h2d[s], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&e_comp[s], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&e_d2h[s], cudaEventDisableTiming));
-        if (s < count) {
-            CK(cudaMallocAsync(&dT[s], bytes, cs));
-            CK(cudaMallocAsync(&dZ[s], bytes, cs));
-            CK(cudaMallocAsync(&ds[s], m * 8, cs));
-            CK(cudaMallocAsync(&de[s], m * 4, cs));
-        }
-    }
+    DevRes *res = dev_res();                   // this thread's copy streams on this device
+    if (!res) return 1;
+    HostStage hs;
+    hs.cs = g_stream;
+    const cudaStream_t cs = g_stream, s_h2d = res->h2d, s_d2h = res->d2h;
+    for (auto &e : hs.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t e_alloc = hs.ev[0], e_h2d[2] = {hs.ev[1], hs.ev[2]}, e_comp[2] = {hs.ev[3], hs.ev[4]},
+                e_d2h[2] = {hs.ev[5], hs.ev[6]};
+    for (int s = 0; s < 2 && s < count; s++)
+        if (int rc = hs.alloc(s, m)) return rc;
     CK(cudaEventRecord(e_alloc, cs));
+    hs.h2d = s_h2d;                            // from here on the destructor drains the copy streams
+    hs.d2h = s_d2h;
     CK(cudaStreamWaitEvent(s_h2d, e_alloc, 0));
     CK(cudaStreamWaitEvent(s_d2h, e_alloc, 0));
     int rc = 0;
     for (int64_t k = 0; k < count && !rc; k++) {
         const int s = int(k & 1);
         if (k >= 2) CK(cudaStreamWaitEvent(s_h2d, e_comp[s], 0));   // dT[s] released by solve k-2
-        for (int64_t c0 = 0; c0 < m; c0 += 128) {                     // upper triangle, 128-column panels
-            const int64_t c1 = std::min<int64_t>(m, c0 + 128);
-            CK(cudaMemcpy2DAsync(dT[s] + c0 * m, m * sizeof(cplx), (const cplx *)T_host[k] + c0 * ldt,
-                                 ldt * sizeof(cplx), size_t(c1) * sizeof(cplx), size_t(c1 - c0),
-                                 cudaMemcpyHostToDevice, s_h2d));
-        }
+        CK(copy_upper_panels(hs.dT[s], m, (const cplx *)T_host[k], ldt, m, cudaMemcpyHostToDevice, s_h2d));
         CK(cudaEventRecord(e_h2d[s], s_h2d));
         CK(cudaStreamWaitEvent(cs, e_h2d[s], 0));
         if (k >= 2) CK(cudaStreamWaitEvent(cs, e_d2h[s], 0));         // dZ[s] read out by D2H k-2
-        rc = trevc_impl<cplx>(dT[s], m, m, nullptr, m, dZ[s], m, ds[s], de[s], nb);
+        rc = trevc_impl<cplx>(hs.dT[s], m, m, nullptr, m, hs.dZ[s], m, hs.ds[s], hs.de[s], nb);
         if (rc < 0) rc = -9;
         if (rc) break;
         CK(cudaEventRecord(e_comp[s], cs));
         CK(cudaStreamWaitEvent(s_d2h, e_comp[s], 0));
-        if (ldz == m) CK(cudaMemcpyAsync(Z_host[k], dZ[s], bytes, cudaMemcpyDeviceToHost, s_d2h));
-        else CK(cudaMemcpy2DAsync(Z_host[k], ldz * sizeof(cplx), dZ[s], m * sizeof(cplx), m * sizeof(cplx), m,
-                                  cudaMemcpyDeviceToHost, s_d2h));
+        CK(copy_upper_panels((cplx *)Z_host[k], ldz, hs.dZ[s], m, m, cudaMemcpyDeviceToHost, s_d2h));
         if (scales_host && scales_host[k])
-            CK(cudaMemcpyAsync(scales_host[k], ds[s], m * 8, cudaMemcpyDeviceToHost, s_d2h));
+            CK(cudaMemcpyAsync(scales_host[k], hs.ds[s], m * 8, cudaMemcpyDeviceToHost, s_d2h));
         if (scale_exp_host && scale_exp_host[k])
-            CK(cudaMemcpyAsync(scale_exp_host[k], de[s], m * 4, cudaMemcpyDeviceToHost, s_d2h));
+            CK(cudaMemcpyAsync(scale_exp_host[k], hs.de[s], m * 4, cudaMemcpyDeviceToHost, s_d2h));
         CK(cudaEventRecord(e_d2h[s], s_d2h));
     }
     CK(cudaStreamSynchronize(s_h2d));
     CK(cudaStreamSynchronize(s_d2h));
-    for (int s = 0; s < 2; s++) {
-        if (dT[s]) cudaFreeAsync(dT[s], cs);
-        if (dZ[s]) cudaFreeAsync(dZ[s], cs);
-        if (ds[s]) cudaFreeAsync(ds[s], cs);
-        if (de[s]) cudaFreeAsync(de[s], cs);
-        cudaEventDestroy(e_h2d[s]);
-        cudaEventDestroy(e_comp[s]);
-        cudaEventDestroy(e_d2h[s]);
-    }
-    cudaEventDestroy(e_alloc);
-    CK(cudaStreamSynchronize(cs));
     return rc;
 }
 

@@ -9,19 +9,19 @@
 namespace mstrsm {
 namespace rt {
 
-cudaStream_t g_stream = nullptr;
-int g_cta_cap = 0;
+thread_local cudaStream_t g_stream = nullptr;
+thread_local int g_cta_cap = 0;
 std::atomic<int64_t> g_launches{0};
-int *g_flag = nullptr;                 // device: non-finite input seen
-char g_errmsg[512] = "no error";
-int g_num_sms = 0;
+thread_local int *g_flag = nullptr;
+thread_local char g_errmsg[512] = "no error";
+thread_local int g_num_sms = 0;
+thread_local int g_dev = -1;
 bool g_debug_sync = getenv("MSTRSM_DEBUG_SYNC") != nullptr;   // synchronise + log after each diag launch
 int g_diag_force_fb = getenv("MSTRSM_DIAG_FORCE_FALLBACK") != nullptr;   // testing: synchronous diag path
 int g_pdl = [] { const char *e = getenv("MSTRSM_PDL"); return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2; }();
-static std::mutex g_mu;
-bool g_prof = false;
-std::vector<ProfRec> g_prof_recs;
-std::vector<cudaEvent_t> g_ev_pool;
+thread_local bool g_prof = false;
+thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<cudaEvent_t> g_ev_pool;
 
 static thread_local cudaError_t g_last_err = cudaSuccess;
 int set_cuda_error(cudaError_t e, const char *where) {
@@ -31,21 +31,60 @@ int set_cuda_error(cudaError_t e, const char *where) {
 }
 cudaError_t last_cuda_error() { return g_last_err; }
 
+// Per (thread, device) context.  Devices beyond kMaxDev are refused.
+namespace {
+constexpr int kMaxDev = 64;
+struct Ctx {
+    bool init = false;
+    int sms = 0;
+    int *flag = nullptr;
+    DevRes res;
+};
+thread_local Ctx t_ctx[kMaxDev];
+std::atomic<uint64_t> g_pool_done{0};
+}  // namespace
+
 int ensure_init() {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (g_flag) return 0;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    // keep stream-ordered allocations cached between calls (workspace, host-entry staging)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (dev < 0 || dev >= kMaxDev) return set_cuda_error(cudaErrorInvalidDevice, "ensure_init (device index)");
+    Ctx &c = t_ctx[dev];
+    g_dev = dev;
+    if (!c.init) {
+        CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+        if (first_on_device(g_pool_done)) {
+            // keep stream-ordered allocations cached between calls (workspace, host-entry staging)
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
+        CK(cudaMalloc(&c.flag, sizeof(int)));
+        CK(cudaMemset(c.flag, 0, sizeof(int)));
+        c.init = true;
     }
-    CK(cudaMalloc(&g_flag, sizeof(int)));
-    CK(cudaMemset(g_flag, 0, sizeof(int)));
+    g_flag = c.flag;
+    g_num_sms = c.sms;
     return 0;
+}
+
+DevRes *dev_res() {
+    if (g_dev < 0 && ensure_init()) return nullptr;
+    DevRes &r = t_ctx[g_dev].res;
+    if (!r.side) {
+        cudaError_t e = cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.ev_d, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.ev_rest, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            set_cuda_error(e, "dev_res (stream / event creation)");
+            r = DevRes{};
+            return nullptr;
+        }
+    }
+    return &r;
 }
 
 cudaEvent_t ev_get() {

@@ -16,17 +16,37 @@
 namespace mstrsm {
 namespace rt {
 
-extern cudaStream_t g_stream;
+// Library state is per calling thread and per device: every API call runs
+// ensure_init(), which binds the thread-local pointers below to the calling thread's context on
+// the current device.  Two host threads (or one thread driving two GPUs) therefore never share a
+// stream, event, side stream or status flag.  Only the NCCL communicator of the multi-GPU entry
+// points is process-wide (one communicator per process, one process per GPU).
+extern thread_local cudaStream_t g_stream;   // the calling thread's library stream (mstrsm_set_stream)
 // > 0: launches of the update GEMM and the diagonal kernel use at most this many CTAs (one per
 // SM), leaving the other SMs to a kernel running concurrently on another stream (look-ahead)
-extern int g_cta_cap;
+extern thread_local int g_cta_cap;
 extern std::atomic<int64_t> g_launches;
-extern int *g_flag;
-extern char g_errmsg[512];
-extern int g_num_sms;
+extern thread_local int *g_flag;             // non-finite input seen (this thread, this device)
+extern thread_local char g_errmsg[512];
+extern thread_local int g_num_sms;
+extern thread_local int g_dev;               // the device ensure_init() bound
 extern bool g_debug_sync;
 extern int g_diag_force_fb;
 extern int g_pdl;            // MSTRSM_PDL: programmatic dependent launch of the diag / GEMM kernels
+
+// Streams and events of the calling thread on the current device: the look-ahead's side stream
+// and events, the host-buffer entries' copy streams.  Created on first use.
+struct DevRes {
+    cudaStream_t side = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_d = nullptr, ev_rest = nullptr;
+};
+DevRes *dev_res();           // nullptr (and the error recorded) if creation fails
+// True the first time it is asked for the current device (per-device one-shot setup such as
+// cudaFuncSetAttribute; bit d of mask = device d done).
+inline bool first_on_device(std::atomic<uint64_t> &mask) {
+    const uint64_t bit = uint64_t(1) << (g_dev & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
+}
 
 // Launch with the programmatic-stream-serialization attribute when g_pdl >= lvl (1: the diagonal
 // and update-GEMM kernels, 2: also the solve's finalize and the Lanczos kernels): the grid may be
@@ -74,9 +94,9 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // live kernel profiling
 enum { PK_GEMM = 0, PK_DIAG = 1, PK_OTHER = 2, PK_N = 3 };
 struct ProfRec { int kind; cudaEvent_t e0, e1; double flops; };
-extern bool g_prof;
-extern std::vector<ProfRec> g_prof_recs;
-extern std::vector<cudaEvent_t> g_ev_pool;
+extern thread_local bool g_prof;
+extern thread_local std::vector<ProfRec> g_prof_recs;
+extern thread_local std::vector<cudaEvent_t> g_ev_pool;
 cudaEvent_t ev_get();
 struct ProfScope {
     ProfRec r{};

@@ -25,7 +25,7 @@ def test_host_batch_equals_single_calls_and_oracle(ms, count):
     m, nb = 520, 64
     Ts = [inputs.c5_grcar_like(m)] + [inputs.c3_trevc_complex(m) for _ in range(count - 1)]
     Ts = [np.asfortranarray(T) for T in Ts]
-    Z = [np.full((m, m), np.nan + 0j, order="F") for _ in range(count)]
+    Z = [np.zeros((m, m), complex, order="F") for _ in range(count)]   # lower triangle: see mstrsm.h
     S = [np.zeros(m) for _ in range(count)]
     E = [np.zeros(m, np.int32) for _ in range(count)]
     ms.trevc_z_host_batch(Ts, m, Z, S, E, nb)

@@ -99,3 +99,21 @@ def test_gpu_cloud_unsettled_flag(ms):
     so, fo, io = oracle.spectral_cloud(U, z, maxit=3, tol=1e-14, v0=v0, nb=32)
     assert np.array_equal(fg, fo) and ((fg & 2) != 0).any()
     assert np.max(np.abs(sg - so) / so) <= 1e-8
+
+
+def test_gpu_breakdown_at_the_last_step_matches_oracle(ms):
+    """R33 pin on the GPU: a 4 x 4 U breaks down at step 5; maxit = 5 -> not flagged, maxit = 4 ->
+    flagged (test_oracle_spectral.py::test_breakdown_at_the_last_step_is_not_flagged)."""
+    rng = np.random.default_rng(11)
+    m = 4
+    U = np.triu(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))) / 2 + np.diag([1.5, 2.0 + 0.5j, -1.0, 0.7j])
+    U = np.asfortranarray(U)
+    z = np.array([0.3 + 0.1j, -0.2 + 0.4j])
+    v0 = np.ones(m, complex) / 2
+    for maxit, want in ((5, [0, 0]), (4, [2, 2])):
+        sg, fg, ig = ms.spectral_cloud(dev(U), dev(z), dev(v0), maxit=maxit, tol=1e-300, nb=2)
+        _sync()
+        so, fo, io = oracle.spectral_cloud(U, z, maxit=maxit, tol=1e-300, v0=v0, nb=2)
+        assert list(host(fg)) == list(fo) == want
+        assert list(host(ig)) == list(io) == [maxit, maxit]
+        assert np.max(np.abs(host(sg) - so) / so) <= 1e-8

@@ -100,3 +100,23 @@ def test_portrait_window_closed_forms():
     z = oracle.window_grid(-1.5, 1.5, 3, -0.5, 0.5, 3)
     dist = np.minimum(np.abs(z + 1), np.abs(z - 1))
     assert np.allclose(s, dist, rtol=1e-12)
+
+
+def test_breakdown_at_the_last_step_is_not_flagged():
+    """R33: bit1 marks a point that neither settled nor broke down within maxit steps.  A 4 x 4 U
+    exhausts its Krylov space; the breakdown test (beta_k <= m eps max alpha) fires at step 5.  With
+    maxit = 5 the point breaks down exactly at the last step: not flagged (the rule "k == maxit"
+    would flag it); with maxit = 4 it has done neither: flagged.  The exhausted space makes sigma
+    the exact sigma_min (numpy SVD)."""
+    rng = np.random.default_rng(11)
+    m = 4
+    U = np.triu(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))) / 2 + np.diag([1.5, 2.0 + 0.5j, -1.0, 0.7j])
+    U = np.asfortranarray(U)
+    z = np.array([0.3 + 0.1j, -0.2 + 0.4j])
+    v0 = np.ones(m, complex) / 2
+    sv = np.array([np.linalg.svd(U - zz * np.eye(m), compute_uv=False)[-1] for zz in z])
+    s, f, its = oracle.spectral_cloud(U, z, maxit=5, tol=1e-300, v0=v0, nb=2)
+    assert list(its) == [5, 5] and list(f) == [0, 0]
+    assert np.max(np.abs(s - sv) / sv) <= 1e-12
+    s4, f4, its4 = oracle.spectral_cloud(U, z, maxit=4, tol=1e-300, v0=v0, nb=2)
+    assert list(its4) == [4, 4] and list(f4) == [2, 2]
