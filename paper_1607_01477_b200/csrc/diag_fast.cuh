@@ -33,7 +33,7 @@
 //    and hands K back through the "done" mbarrier.  The substitution warps then take their
 //    registers to the paper's frame with one exact power-of-two product, 2^(F - K).  A group
 //    whose values stop being finite (growth of more than ~2^400 inside one chunk: tiny pivots)
-//    is handed to the synchronous fallback (diag_kernel<FB>).
+//    is rerun in place by the synchronous guarded loop (diag_rows, Alg. 4 step by step).
 #pragma once
 #include "diag_kernel.cuh"
 
@@ -386,64 +386,90 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
 
         if (!staged) stage_wait();
         int F = 0;
-        bool handed = false;
+        bool failed = false;
         if (SAFE && __any_sync(0xffffffffu, guarded)) {
-            const bool ok = diagw_rows<T, LPC, RPL, SAFE, true, OP == 1>(y, pivot, pk, rl, nmax, guarded, gub,
-                                                                         s_rec + c, s_fp + c, C, bars, F) &&
-                            !(a.force_fb && guarded);
-            if (!ok) {                                                     // hand the column over
-                handed = true;
-                if (rl == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = int(j);
-            }
+            failed = !diagw_rows<T, LPC, RPL, SAFE, true, OP == 1>(y, pivot, pk, rl, nmax, guarded, gub, s_rec + c,
+                                                                   s_fp + c, C, bars, F) ||
+                     (a.force_fb && guarded);
         } else {
             diagw_rows<T, LPC, RPL, SAFE, false, OP == 1>(y, pivot, pk, rl, nmax, false, 0.0, s_rec + c, s_fp + c,
                                                           C, bars, F);
         }
-
-        if (SAFE) {
-            dw_mbar_wait(bars + RPL, pass & 1);                            // K from the replay warp
-            const int kt = s_k[c];
-            if (!handed && F != kt) scale_pow2(y, F - kt);                 // to the paper's frame
-            int ej = 0;
-            double Gj = 0.0;
-            if (active) { ej = a.e[j]; Gj = a.G[j]; }
-            if (kt > 0) {                                                  // P:376-386, step (ii)
-                ej -= kt;
-                Gj = mulp2n(Gj, kt);
-            }
-            double xm = 0.0;
+        // steps (ii) and (iii) of Alg. 5 and the stores, for the groups with `keep`
+        auto finish = [&](int kt, bool keep) {
+            if (SAFE) {
+                int ej = 0;
+                double Gj = 0.0;
+                if (active) { ej = a.e[j]; Gj = a.G[j]; }
+                if (kt > 0) {                                              // P:376-386, step (ii)
+                    ej -= kt;
+                    Gj = mulp2n(Gj, kt);
+                }
+                double xm = 0.0;
 #pragma unroll
-            for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
-            xm = group_max<LPC>(xm);
-            Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
-            int k3 = 0;
-            if (Gj >= kOmega) {
-                k3 = minpow2_bits(Gj, kOmega);
-                scale_all<false>(y, k3);
-                ej -= k3;
-                Gj = mulp2n(Gj, k3);
-            }
-            if (active && rl == 0 && !handed) {
-                a.e[j] = ej;
-                a.G[j] = Gj;
-                a.dblk[j] = -(kt + k3);
-                a.Etab[a.b * a.n + j] = ej;
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < RPL; t++) {
-            const int sc = rl + LPC * t;
-            if (sc < nrow && !handed) x[rowof(sc)] = y[t];
-        }
-        if constexpr (ST::cplx_) {  // operand sums for the 3M update GEMM
-            if (a.Xsum && valid && !handed) {
-                double *xs = a.Xsum + j * a.ldxs;
-#pragma unroll
-                for (int t = 0; t < RPL; t++) {
-                    const int sc = rl + LPC * t;
-                    if (sc < nfull) xs[rowof(sc) - a.lo] = __dadd_rn(y[t].x, y[t].y);
+                for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
+                xm = group_max<LPC>(xm);
+                Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
+                int k3 = 0;
+                if (Gj >= kOmega) {
+                    k3 = minpow2_bits(Gj, kOmega);
+                    scale_all<false>(y, k3);
+                    ej -= k3;
+                    Gj = mulp2n(Gj, k3);
+                }
+                if (active && rl == 0 && keep) {
+                    a.e[j] = ej;
+                    a.G[j] = Gj;
+                    a.dblk[j] = -(kt + k3);
+                    a.Etab[a.b * a.n + j] = ej;
                 }
             }
+#pragma unroll
+            for (int t = 0; t < RPL; t++) {
+                const int sc = rl + LPC * t;
+                if (sc < nrow && keep) x[rowof(sc)] = y[t];
+            }
+            if constexpr (ST::cplx_) {  // operand sums for the 3M update GEMM
+                if (a.Xsum && valid && keep) {
+                    double *xs = a.Xsum + j * a.ldxs;
+#pragma unroll
+                    for (int t = 0; t < RPL; t++) {
+                        const int sc = rl + LPC * t;
+                        if (sc < nfull) xs[rowof(sc) - a.lo] = __dadd_rn(y[t].x, y[t].y);
+                    }
+                }
+            }
+        };
+        int kt = 0;
+        if (SAFE) {
+            dw_mbar_wait(bars + RPL, pass & 1);                            // K from the replay warp
+            kt = s_k[c];
+            if (!failed && F != kt) scale_pow2(y, F - kt);                 // to the paper's frame
+        }
+        finish(kt, !failed);
+        if (SAFE && __any_sync(0xffffffffu, failed)) {
+            // a group whose values stopped being finite (tiny pivots: growth beyond the frame's
+            // headroom inside one chunk) is rerun from its inputs by the synchronous guarded loop,
+            // Alg. 4 step by step; the other groups of the warp idle through it
+            const int nrow_f = failed ? nrow : 0;
+            int nmax_f = nrow_f;
+#pragma unroll
+            for (int o = LPC; o < 32; o <<= 1) nmax_f = max(nmax_f, __shfl_xor_sync(0xffffffffu, nmax_f, o));
+#pragma unroll
+            for (int t = 0; t < RPL; t++) {
+                const int sc = rl + LPC * t;
+                y[t] = sc < nrow_f ? x[rowof(sc)] : ST::zero();
+            }
+            auto pivot_f = [&](int sc) -> T {
+                T dd = sc < nrow_f ? ST::sub(dg[sc], sh) : ST::real(1.0);
+                if (ST::is_zero(dd)) dd = ST::real(delta);
+                return dd;
+            };
+            const UAcc<T, false, OP == 1> ua{pk, nullptr, cn, nullptr, ST::zero(), 0.0};
+            double g = g0;
+            int kt2 = 0;
+            diag_rows<T, LPC, RPL, true, true>(y, pivot_f, ua, rl, nrow_f, nmax_f, failed, g, kt2);
+            finish(kt2, failed);
         }
     }
     if (!staged) stage_wait();

@@ -385,7 +385,9 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
 
 // The synchronous guarded loop (fallback when phase 1 overflows): Alg. 4 step by step
 // with the rescales applied lazily through pend.
-template <typename T, int LPC, int RPL, bool GUARD, typename PivF, typename Acc>
+// PADDED: the triangle is diag_fast.cuh's padded layout (column l at LPC^2 t(t+1)/2 + r LPC (t+1),
+// l = t LPC + r) instead of the packed one (column l at l(l-1)/2).
+template <typename T, int LPC, int RPL, bool GUARD, bool PADDED = false, typename PivF, typename Acc>
 __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot, const Acc &ua,
                                           int rl, int nrow, int nmax, bool guarded, double &g, int &kt) {
     typedef S<T> ST;
@@ -436,7 +438,7 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot, const Acc &ua
             }
             const T xr = in ? xv : ST::zero();
             // owner stores x_l; substitution within the block (P:315 / P:84): rows sc' < sc
-            const int col = (sc * (sc - 1)) / 2;
+            const int col = PADDED ? LPC * LPC * t * (t + 1) / 2 + rr * LPC * (t + 1) : (sc * (sc - 1)) / 2;
             {
                 const int i = rl + LPC * t;
                 if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + i));

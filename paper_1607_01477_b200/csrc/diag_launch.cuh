@@ -147,24 +147,16 @@ int launch_diagf_k(const DiagArgs<T> &a0) {
     return 0;
 }
 
-// The chunked kernel, then (safe) the synchronous fallback launch of diag_kernel, which exits at
-// once unless columns were handed over (device-side count, no host synchronisation).
+// The chunked kernel (it reruns the rare column whose values stop being finite with the
+// synchronous guarded loop itself: no second launch).
 template <typename T, int LPC, int RPL, bool SAFE, int OP>
 int launch_diagf_pair(const DiagArgs<T> &a, int nb) {
+    (void)nb;
     if (int rc = launch_diagf_k<T, LPC, RPL, SAFE, OP>(a)) return rc;
     if (g_debug_sync) {
         cudaError_t e = cudaStreamSynchronize(g_stream);
-        int cnt = -1;
-        if (SAFE) cudaMemcpy(&cnt, a.fb_count, 4, cudaMemcpyDeviceToHost);
-        fprintf(stderr, "[mstrsm debug] diagf<%d,%d> block %lld main done (%s), ncols %lld, handed %d\n", LPC, RPL,
-                (long long)a.b, cudaGetErrorString(e), (long long)a.ncols, cnt);
-    }
-    if constexpr (SAFE) {
-        const int64_t cap = std::min<int64_t>(a.ncols, int64_t(g_num_sms) * 32);
-        if (nb <= 16) return launch_diag_k<T, 1, 16, SAFE, OP, true, false>(a, cap);
-        if (nb <= 32) return launch_diag_k<T, 2, 16, SAFE, OP, true, false>(a, cap);
-        if (nb <= 64) return launch_diag_k<T, 4, 16, SAFE, OP, true, false>(a, cap);
-        return launch_diag_k<T, 8, 16, SAFE, OP, true, false>(a, cap);
+        fprintf(stderr, "[mstrsm debug] diagw<%d,%d> block %lld done (%s), ncols %lld\n", LPC, RPL, (long long)a.b,
+                cudaGetErrorString(e), (long long)a.ncols);
     }
     return 0;
 }
