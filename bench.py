@@ -298,10 +298,21 @@ def run_cuda(args, cfgname):
 
     last = {}
 
+    # N > 1: the library's native NCCL path (torch only bootstraps the process group and hands the
+    # NCCL id over): delta + T's panels streamed right to left overlapping the shard solve, status
+    # all-reduce, triangular all-gather, unpack (trevc_*_dist, csrc/mstrsm.cu).  MSTRSM_DIST_IMPL=torch
+    # selects the torch.distributed mirror of the same sequence (paper_1607_01477_b200/dist.py).
+    native = ws > 1 and os.environ.get("MSTRSM_DIST_IMPL", "native") == "native"
+    if native:
+        ms.comm_init(ws, rank)
+
     def step():
-        # N = 1: the local solve; N > 1: NCCL broadcast of T, local shard, NCCL all-gather of the
-        # eigenvectors + exponents, unpack (paper_1607_01477_b200/dist.py)
-        last["Z"], last["e"] = pdist.trevc_sharded(Td, m, solve_cols, rank=rank, world=ws)
+        if native:
+            Z, _, e = ms.trevc_dist(Td if rank == 0 else None, m, nb=nb, root=0)
+            last["Z"], last["e"] = Z, e
+        else:
+            # N = 1: the local solve; torch mirror for N > 1 (paper_1607_01477_b200/dist.py)
+            last["Z"], last["e"] = pdist.trevc_sharded(Td, m, solve_cols, rank=rank, world=ws)
 
     # ---- FP64 roofline denominators (measured on this GPU, before timing)
     dmma_tf, dfma_tf = ms.fp64_peak(100.0)
@@ -353,6 +364,8 @@ def run_cuda(args, cfgname):
     eig_per_s = m / (ms_per_step * 1e-3)
 
     if rank != 0:
+        if native:
+            ms.comm_destroy()
         if dist:
             dist.destroy_process_group()
         return 0
@@ -394,7 +407,9 @@ def run_cuda(args, cfgname):
             "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)" if cplx else "f64",
             "data": "synthetic (seeded numpy generators, paper_1607_01477_b200/inputs.py)",
             "config": {"workload": cfg["workload"], "m": m, "n": m, "nb": nb,
-                       "parallelism": f"shift-sharded x{ws} (serpentine block-cyclic, 16 cols)",
+                       "parallelism": f"shift-sharded x{ws} (serpentine block-cyclic, 16 cols)" +
+                                      ("; native NCCL: delta + panel-streamed broadcast overlapping the "
+                                       "shard solve, status all-reduce, triangular all-gather" if native else ""),
                        "l2": "inputs (4.3 GB T, 4.3 GB Z) >> 126 MB L2; no flush needed"},
             "eigvecs_per_s": eig_per_s,
             "pct_fp64_peak": 100.0 * value / 1e3 / (peak_tf * ws) if peak_tf else None,
@@ -404,7 +419,7 @@ def run_cuda(args, cfgname):
             "gflops_nominal_m2n": nominal_flops(m, m, cplx) / (ms_per_step * 1e-3) / 1e9,
             "roofline": roofline, "clocks": clocks, "gpu_launches": launches,
             "wall_s_timed": t_wall, "output_finite": ok_finite,
-            "solve_only_ms_per_step": solve_ms / args.steps,
+            "solve_only_ms_per_step": (solve_ms / args.steps) if not native else None,
             "solve_only_note": "the local trevc_*_cols call alone (CUDA events, max over ranks); ms_per_step "
                                "is end to end: broadcast + solve + all-gather + unpack (SURVEY §8d.5)"}
 
@@ -415,6 +430,8 @@ def run_cuda(args, cfgname):
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(T_host, cfg, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
+    if native:
+        ms.comm_destroy()
     if dist:
         dist.destroy_process_group()
     return 0

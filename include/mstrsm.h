@@ -288,12 +288,20 @@ int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dc
  *                          (groups of 16 columns dealt serpentine block-cyclically, balancing the
  *                          ~(k-1)^2 cost); returns the count, fills cols_out (nullable) ascending
  *   trevc_*_dist           TriangEig over all ranks: T (device) is read on `root` only (other
- *                          ranks may pass NULL / any ldt), its upper triangle is broadcast, each
- *                          rank solves its shard, the shards (+ scales, exponents) are all-gathered
- *                          and every rank receives the full Z (m x m, ldz), scales and scale_exp
- *                          (nullable, m entries) in natural order -- bit-identical to trevc_*.
- *                          Collective: every rank must call it.  Errors: -i for argument i, 1
- *                          CUDA error, 3 communication error (or no communicator).           */
+ *                          ranks may pass NULL / any ldt).  Root computes delta (R4, ||T||_inf)
+ *                          and broadcasts it, then T's upper triangle in 128-column panels right
+ *                          to left (the order the blocks consume it) on a separate
+ *                          stream; each rank's block b waits only for panel b, so the solve of its
+ *                          shard overlaps the rest of the broadcast.  The ranks then agree on a
+ *                          status (one all-reduce), the triangular shards (+ scales, exponents) are
+ *                          all-gathered and every rank receives the full Z (m x m, ldz), scales and
+ *                          scale_exp (nullable, m entries) in natural order -- bit-identical to
+ *                          trevc_*.  Collective and blocking: every rank must call it; the call
+ *                          returns when its work is done.  NCCL's asynchronous errors are polled
+ *                          while waiting; an error or a wait longer than MSTRSM_NCCL_TIMEOUT_S
+ *                          (default 600 s) aborts the communicator and returns 3.  Errors: -i for
+ *                          argument i, 1 CUDA error, 3 communication error, timeout, a failure
+ *                          on another rank, or no communicator.                            */
 /* Triangular shard packing for the all-gather (eigenvector k is zero below row k):
  *   pack:   out[offsets[q] .. + heights[q]) = Z(0 : heights[q], src_cols[q])   (src_cols
  *           nullable: q), q < n
@@ -317,8 +325,8 @@ int trevc_d_dist(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz
                  int32_t *scale_exp, int nb, int root);
 /* Dense right-hand sides sharded by column (shifts / B / scales / scale_exp hold this rank's n
  * columns): U (device) is read on `root` only and its upper triangle broadcast; every rank then
- * runs mstrsm_*_ex on its own columns (no gather).  Collective.  Arguments as mstrsm_*_ex (no
- * row_end), root last.                                                                       */
+ * runs mstrsm_*_ex on its own columns (no gather).  Collective and blocking (NCCL errors and
+ * timeouts as trevc_*_dist: return 3).  Arguments as mstrsm_*_ex (no row_end), root last.   */
 int mstrsm_d_dist(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
                   int64_t shift_stride, double *B, int64_t ldb, int64_t n, double *scales,
                   int32_t *scale_exp, int nb, int root);

@@ -77,8 +77,8 @@ __global__ void norm_rows_c_kernel(const T *__restrict__ U, int64_t ldu, int64_t
 // Panel sums P_b, one thread per block, in the fixed order of R6 (op N: k ascending; op C:
 // l descending), sequential -> bit-identical to the oracle given bit-identical inputs.
 __global__ void panel_sum_kernel(int op, int64_t m, int nb, int64_t nblk,
-                                 const double *__restrict__ part, double *__restrict__ P) {
-    int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+                                 const double *__restrict__ part, double *__restrict__ P, int64_t b0 = 0) {
+    int64_t b = b0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (b >= nblk) return;
     Blk bl = block_rows(op, m, nb, b);
     double s = 0.0;
@@ -229,11 +229,13 @@ __global__ void trevc_prepass_kernel(const T *__restrict__ Tm, int64_t ldt, int6
                                      T *__restrict__ Z, int64_t ldz, T *__restrict__ shifts,
                                      int64_t *__restrict__ rowend, double *__restrict__ G, int *__restrict__ e,
                                      double *__restrict__ P, int64_t ldp, int *__restrict__ nonfinite,
-                                     const int *__restrict__ qof = nullptr) {
+                                     const int *__restrict__ qof = nullptr, int64_t k0 = 0, int64_t k1 = -1) {
+    // columns [k0, k1) of T (k1 < 0: all); the multi-GPU path runs it panel by panel as T arrives
     const int lane = threadIdx.x & 31;
     const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t k = w; k < m; k += nw) {
+    const int64_t kend = k1 < 0 ? m : k1;
+    for (int64_t k = k0 + w; k < kend; k += nw) {
         const int64_t b = (m - 1 - k) / nb;
         const Blk bl = block_rows(0, m, nb, b);
         const T *tc = Tm + k * ldt;

@@ -16,6 +16,9 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <functional>
+#include <thread>
+#include <chrono>
 #include <vector>
 
 #include "../../include/mstrsm.h"
@@ -129,6 +132,27 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w, bool 
     return 0;
 }
 
+// ||U||_inf of op N for delta (R4) into delta[0..1] (rowsum + ordered reduction + max).
+template <typename T>
+int compute_delta_n(const T *U, int64_t ldu, int64_t m, double *rs, double *delta) {
+    const int64_t nch = cdiv(m, kRowsumChunk);
+    double *part2 = nullptr;
+    CK(ws_malloc((void **)&part2, size_t(nch) * m * 8));
+    rowsum_n_kernel<T><<<dim3(unsigned(cdiv(m, 128)), unsigned(nch)), 128, 0, g_stream>>>(U, ldu, m, part2);
+    CK_LAUNCH("rowsum_n_kernel");
+    rowsum_reduce_kernel<<<int(cdiv(m, 128)), 128, 0, g_stream>>>(m, nch, part2, rs);
+    CK_LAUNCH("rowsum_reduce_kernel");
+    ws_free(part2, g_stream);
+    delta_kernel<<<1, 1024, 0, g_stream>>>(m, rs, delta);
+    CK_LAUNCH("delta_kernel");
+    return 0;
+}
+
+// Per-block hook of the blocked solve (this thread's): called at the top of block b, before its
+// diagonal step, on the library stream.  The multi-GPU path uses it to wait for T's panel b and run
+// that panel's prepass as the panels arrive (trevc_impl with panel_ready).
+thread_local const std::function<int(int64_t)> *t_pre_block = nullptr;
+
 // ---------------------------------------------------------------- look-ahead (op N, safe)
 // Look-ahead (default; MSTRSM_LOOKAHEAD=0 disables): block b's update is split into its top n_b rows (the next diagonal block,
 // on the library stream) and the rest (on a side stream, on fewer SMs), so that the next
@@ -167,6 +191,9 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
     if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));   // diag fallback counts
     int early = 0;                             // U / cnl ready: later launches stage before the wait
     for (int64_t b = 0; b < nblk; b++) {
+        if (t_pre_block) {
+            if (int rc = (*t_pre_block)(b)) return rc;
+        }
         Blk bl = block_rows(op, m, nb, b);
         int64_t c0 = 0;
         if (op == 0 && rowend_sorted_host) {
@@ -189,7 +216,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         if (Xsum && rowend_dev && !rowend_sorted_host)        // inactive columns in range: zero rows
             CK(cudaMemsetAsync(Xsum + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
         int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
-        early = 1;
+        early = t_pre_block ? 0 : 1;           // (a per-block prepass writes cnl right before the diag)
         if (rc) return rc;
         if (g_debug_sync) {
             cudaError_t e = cudaStreamSynchronize(g_stream);
@@ -241,6 +268,9 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
     int early = 0;
     int rc = 0;
     for (int64_t b = 0; b < nblk && !rc; b++) {
+        if (t_pre_block) {
+            if ((rc = (*t_pre_block)(b))) break;
+        }
         const Blk bl = block_rows(0, m, nb, b);
         const int64_t c0 = c0_of(bl), ncols = n - c0;
         if (ncols <= 0) { diag_cap = 0; continue; }
@@ -263,7 +293,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         g_cta_cap = diag_cap;
         rc = launch_diag<T, true, 0>(a, nb);
         g_cta_cap = 0;
-        early = 1;
+        early = t_pre_block ? 0 : 1;
         if (rc) break;
         diag_cap = 0;
         const int64_t M = bl.lo;
@@ -427,9 +457,14 @@ int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T
     return 0;
 }
 
+// panel_ready (nullable): nblk events, op N block order (b = 0: the last panel of columns); block
+// b waits for panel_ready[b] (columns [lo_b, hi_b) of T, rows 0 .. hi_b, have arrived) and runs that
+// panel's prepass first.  delta_ext (with panel_ready): delta[0..1] of T (R4), valid once
+// panel_ready[0] has completed.
 template <typename T>
 int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
-               T *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
+               T *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb,
+               const double *delta_ext = nullptr, const cudaEvent_t *panel_ready = nullptr) {
     if (m < 0) return -3;
     if (ldt < std::max<int64_t>(1, m)) return -2;
     if (ncols < 0) return -5;
@@ -461,15 +496,35 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
         CK(cudaMemcpyAsync(qof, qh.data(), size_t(m) * 4, cudaMemcpyHostToDevice, g_stream));
     }
     if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb, /*fill=*/false)) return rc;
-    {
+    std::function<int(int64_t)> hook;
+    if (!panel_ready) {
         int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
         trevc_prepass_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, nb, w.cnl, w.part, Z, ldz, sh, w.rowend,
                                                                w.G, w.e, sp.U, sp.ldu, g_flag, qof);
         CK_LAUNCH("trevc_prepass_kernel");
+        if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w, /*cols_done=*/true)) return rc;
+    } else {
+        // T arrives panel by panel (right to left, the order the blocks consume it): every block
+        // waits for its own panel and computes that panel's part of the prepass (column norms,
+        // panel sum P_b, Z / G / row_end / shifts of the requested columns, 3M sum plane)
+        CK(cudaStreamWaitEvent(g_stream, panel_ready[0], 0));
+        CK(cudaMemcpyAsync(w.delta, delta_ext, 2 * sizeof(double), cudaMemcpyDeviceToDevice, g_stream));
+        hook = [&, qof](int64_t b) -> int {
+            const Blk bl = block_rows(0, m, nb, b);
+            CK(cudaStreamWaitEvent(g_stream, panel_ready[b], 0));
+            const int blocks = int(std::min<int64_t>(cdiv(bl.hi - bl.lo, 8), int64_t(g_num_sms) * 16));
+            trevc_prepass_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, nb, w.cnl, w.part, Z, ldz, sh, w.rowend,
+                                                                   w.G, w.e, sp.U, sp.ldu, g_flag, qof, bl.lo, bl.hi);
+            CK_LAUNCH("trevc_prepass_kernel");
+            panel_sum_kernel<<<1, 32, 0, g_stream>>>(0, m, nb, b + 1, w.part, w.P, b);
+            CK_LAUNCH("panel_sum_kernel");
+            return 0;
+        };
+        t_pre_block = &hook;
     }
-    if (qof) cudaFreeAsync(qof, g_stream);
-    if (int rc = norm_pass<T>(0, Tm, ldt, m, nb, w, /*cols_done=*/true)) return rc;
     int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
+    t_pre_block = nullptr;
+    if (qof) cudaFreeAsync(qof, g_stream);
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
     return rc;
 }
@@ -1612,6 +1667,100 @@ int replicate_upper(const T *Tm, int64_t ldt, int64_t m, int root, T **pack_out,
     return 0;
 }
 
+// Wait for the work enqueued on st, polling NCCL's asynchronous error state: a failed or hung
+// peer aborts the communicator and returns 3 instead of blocking forever.
+// MSTRSM_NCCL_TIMEOUT_S (default 600) bounds the wait.
+int nccl_wait(cudaStream_t st, const char *what) {
+    static const double timeout_s = [] {
+        const char *e = getenv("MSTRSM_NCCL_TIMEOUT_S");
+        const double v = e ? atof(e) : 600.0;
+        return v > 0 ? v : 600.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) return 0;
+        if (e != cudaErrorNotReady) return set_cuda_error(e, what);
+        ncclResult_t ar = ncclSuccess;
+        if (g_comm) ncclCommGetAsyncError(g_comm, &ar);
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if ((ar != ncclSuccess && ar != ncclInProgress) || el > timeout_s) {
+            snprintf(g_errmsg, sizeof(g_errmsg), "%s: %s; communicator aborted", what,
+                     ar != ncclSuccess && ar != ncclInProgress ? ncclGetErrorString(ar) : "timeout");
+            if (g_comm) ncclCommAbort(g_comm);
+            g_comm = nullptr;
+            return 3;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
+// T's upper triangle from root, streamed in the order the blocks consume it: op N block b needs
+// columns [lo_b, hi_b) (rows 0 .. hi_b) -- its diagonal block and the update panel U(I0, I1), and
+// the per-panel prepass (P:503-508 shortcut: nothing below the diagonal travels).  On the comm
+// stream cs: delta of root's T (R4: ||T||_inf needs all of T, so root computes it and sends it
+// first), then one ncclBroadcast per panel, right to left, each followed by ev[b] (non-root: after
+// the panel is unpacked into the workspace copy of T).  The solve waits for ev[b] before block b,
+// so block b computes while panels b+1.. are still in flight.
+template <typename T>
+int stream_upper(const T *Tm, int64_t ldt, int64_t m, int nb, int root, cudaStream_t cs, T **pack_out, T **Tw_out,
+                 const T **Tuse, int64_t *lduse, double *dbuf, std::vector<cudaEvent_t> &ev) {
+    const size_t es = sizeof(T), ndbl = es / 8;
+    const int r = g_comm_r;
+    const int64_t nblk = cdiv(m, nb);
+    size_t packed = 0;
+    for (int64_t b = 0; b < nblk; b++) {
+        const Blk bl = block_rows(0, m, nb, b);
+        packed += size_t(bl.hi) * size_t(bl.hi - bl.lo);
+    }
+    T *pack = nullptr;
+    CK(cudaMallocAsync(&pack, packed * es, g_stream));
+    *pack_out = pack;
+    *Tuse = Tm;
+    *lduse = ldt;
+    // MSTRSM_DIST_TEST_UNPACK=1 (testing on one GPU): root also solves from its unpacked copy, so the
+    // non-root path (panels unpacked from the broadcast buffer) runs at nranks = 1
+    static const bool test_unpack = [] { const char *e = getenv("MSTRSM_DIST_TEST_UNPACK"); return e && e[0] == '1'; }();
+    const bool unpack = r != root || test_unpack;
+    if (r == root) {
+        double *rs = nullptr;
+        CK(ws_malloc((void **)&rs, size_t(m) * 8));
+        if (int rc = compute_delta_n<T>(Tm, ldt, m, rs, dbuf)) return rc;
+        ws_free(rs, g_stream);
+    }
+    if (unpack) {
+        T *Tw = nullptr;
+        CK(cudaMallocAsync(&Tw, size_t(m) * m * es, g_stream));
+        *Tw_out = Tw;
+        *Tuse = Tw;
+        *lduse = m;
+    }
+    cudaEvent_t e0;
+    CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    ev.push_back(e0);                                    // ev[0] is the setup event; panels follow
+    CK(cudaEventRecord(e0, g_stream));
+    CK(cudaStreamWaitEvent(cs, e0, 0));
+    NCK(ncclBroadcast(dbuf, dbuf, 2, ncclDouble, root, g_comm, cs));
+    size_t off = 0;
+    for (int64_t b = 0; b < nblk; b++) {
+        const Blk bl = block_rows(0, m, nb, b);
+        const int64_t rows = bl.hi, w = bl.hi - bl.lo;
+        if (r == root)
+            CK(cudaMemcpy2DAsync(pack + off, rows * es, Tm + bl.lo * ldt, ldt * es, rows * es, w,
+                                 cudaMemcpyDeviceToDevice, cs));
+        NCK(ncclBroadcast(pack + off, pack + off, size_t(rows) * w * ndbl, ncclDouble, root, g_comm, cs));
+        if (unpack)
+            CK(cudaMemcpy2DAsync(*Tw_out + bl.lo * m, m * es, pack + off, rows * es, rows * es, w,
+                                 cudaMemcpyDeviceToDevice, cs));
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, cs));
+        ev.push_back(e);
+        off += size_t(rows) * w;
+    }
+    return 0;
+}
+
 // Dense right-hand sides (SURVEY §8b mstrsm_z_safe_dist): U from root, every rank solves its own
 // columns of B (its shard of shifts); no gather.
 template <typename T>
@@ -1635,6 +1784,7 @@ int ex_dist_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *
         rc = mstrsm_ex_impl<T>(safe, op, Uuse, lduse, m, shifts, sstride, B, ldb, n, nullptr, scales, scale_exp, nb);
     if (pack) cudaFreeAsync(pack, g_stream);
     if (Tw) cudaFreeAsync(Tw, g_stream);
+    if (int wrc = nccl_wait(g_stream, "mstrsm_*_dist")) return wrc;
     return rc;
 }
 
@@ -1656,10 +1806,25 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     if (!Z) return -4;
     if (int rc = ensure_init()) return rc;
     const size_t es = sizeof(T), ndbl = es / 8;
+    if (nb == 0) nb = 64;
+    DevRes *res = dev_res();                        // this thread's comm stream on this device
+    if (!res) return 1;
+    const cudaStream_t cs = res->comm;
     T *pack = nullptr, *Tw = nullptr;
     const T *Tuse = Tm;
     int64_t lduse = ldt;
-    if (int rc = replicate_upper<T>(Tm, ldt, m, root, &pack, &Tw, &Tuse, &lduse)) return rc;
+    double *dbuf = nullptr;
+    CK(cudaMallocAsync(&dbuf, 2 * sizeof(double), g_stream));
+    std::vector<cudaEvent_t> ev;                    // [setup, panel 0, panel 1, ...]
+    struct EvGuard {
+        std::vector<cudaEvent_t> &v;
+        ~EvGuard() { for (auto e : v) cudaEventDestroy(e); }
+    } evg{ev};
+    // 1. T streamed from root panel by panel (comm stream), overlapping the solve below
+    if (int rc = stream_upper<T>(Tm, ldt, m, nb, root, cs, &pack, &Tw, &Tuse, &lduse, dbuf, ev)) {
+        nccl_wait(cs, "trevc_*_dist (broadcast)");
+        return rc;
+    }
     // 2. this rank's shard, written into the all-gather send buffer (m x mc, padded)
     int64_t mc = 0;
     for (int q = 0; q < P; q++) mc = std::max(mc, shard_of(m, P, q, kShardGroup, nullptr));
@@ -1701,8 +1866,27 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     CK(cudaMallocAsync(&meta, size_t(m) * 3 * 8, g_stream));
     T *Sb = nullptr;
     CK(cudaMallocAsync(&Sb, size_t(std::max<int64_t>(L, 1)) * es, g_stream));
-    int rc = ncols > 0 ? trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb) : 0;
+    int rc = ncols > 0 ? trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb, dbuf, ev.data() + 1)
+                       : 0;
     if (rc < 0) rc = 1;
+    // every rank agrees on the status before the all-gather (a rank that failed locally must not
+    // leave its peers blocked in the collective): max over ranks of the local return codes
+    {
+        CK(cudaStreamWaitEvent(g_stream, ev.back(), 0));   // broadcasts done before the next collective
+        int *st = nullptr;
+        CK(cudaMallocAsync(&st, sizeof(int), g_stream));
+        const int rc_local = rc;
+        CK(cudaMemcpyAsync(st, &rc_local, sizeof(int), cudaMemcpyHostToDevice, g_stream));
+        NCK(ncclAllReduce(st, st, 1, ncclInt32, ncclMax, g_comm, g_stream));
+        int rc_all = 0;
+        CK(cudaMemcpyAsync(&rc_all, st, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
+        cudaFreeAsync(st, g_stream);
+        if (int wrc = nccl_wait(g_stream, "trevc_*_dist (solve)")) return wrc;
+        if (rc_all && !rc) {
+            snprintf(g_errmsg, sizeof(g_errmsg), "trevc_*_dist: another rank failed");
+            rc = 3;
+        }
+    }
     if (!rc) {
         std::vector<int64_t> perm(m);
         for (int q = 0; q < P; q++)
@@ -1740,11 +1924,12 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
         gather_dist_kernel<T><<<blocks, 256, 0, g_stream>>>(nullptr, m, perm_d, m, Z, ldz, sa, ea, scales,
                                                             reinterpret_cast<int *>(scale_exp));
         CK_LAUNCH("gather_dist_kernel");
-        CK(cudaStreamSynchronize(g_stream));       // host index arrays go out of scope
         cudaFreeAsync(offl, g_stream);
+        if (int wrc = nccl_wait(g_stream, "trevc_*_dist (all-gather)")) return wrc;   // host index arrays go out of scope
     }
     cudaFreeAsync(meta, g_stream);
     cudaFreeAsync(Sb, g_stream);
+    cudaFreeAsync(dbuf, g_stream);
     for (void *p : {(void *)pack, (void *)Tw, (void *)Zs, (void *)ss, (void *)es_, (void *)Za, (void *)sa,
                     (void *)ea, (void *)perm_d})
         if (p) cudaFreeAsync(p, g_stream);

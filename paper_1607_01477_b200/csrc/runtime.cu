@@ -76,6 +76,7 @@ DevRes *dev_res() {
         cudaError_t e = cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.h2d, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.comm, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.ev_d, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.ev_rest, cudaEventDisableTiming);
         if (e != cudaSuccess) {

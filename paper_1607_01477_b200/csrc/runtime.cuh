@@ -37,7 +37,7 @@ extern int g_pdl;            // MSTRSM_PDL: programmatic dependent launch of the
 // Streams and events of the calling thread on the current device: the look-ahead's side stream
 // and events, the host-buffer entries' copy streams.  Created on first use.
 struct DevRes {
-    cudaStream_t side = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaStream_t side = nullptr, h2d = nullptr, d2h = nullptr, comm = nullptr;
     cudaEvent_t ev_d = nullptr, ev_rest = nullptr;
 };
 DevRes *dev_res();           // nullptr (and the error recorded) if creation fails

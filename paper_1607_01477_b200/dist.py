@@ -97,6 +97,20 @@ def _panels(m: int, w: int):
     return [(c0, min(m, c0 + w)) for c0 in range(0, m, w)]
 
 
+def block_panels(m: int, nb: int = 128):
+    """Column panels of T in the order the blocked solve consumes them (op N, bottom-up: block b =
+    rows [lo_b, hi_b) needs columns [lo_b, hi_b), rows 0 .. hi_b): [(lo_0, hi_0), (lo_1, hi_1), ...]
+    from the right; the top block is the short one (R9).  The native path (trevc_*_dist) broadcasts T
+    in exactly these panels and order."""
+    out = []
+    hi = m
+    while hi > 0:
+        lo = max(0, hi - nb)
+        out.append((lo, hi))
+        hi = lo
+    return out
+
+
 def pack_upper(T, m: int, w: int = 128):
     """The upper triangle of T as w-column panels T[0:c1, c0:c1] (rows up to the panel end, column
     by column) in one contiguous buffer: what the solve reads (the strictly lower triangle never
@@ -119,27 +133,38 @@ def unpack_upper(buf, T, m: int, w: int = 128) -> None:
         off += n
 
 
-def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, group=None):
-    """Broadcast T's upper triangle from rank 0, solve this rank's block-cyclic column shard with
-    `solve_cols`, all-gather the shards (vectors + int32 exponents) and unpack on every rank.
+def broadcast_panels(T, m: int, *, rank: int, nb: int = 128, group=None):
+    """T's upper triangle from rank 0 in block_panels order, one broadcast per panel, into T on the
+    other ranks (the collective sequence of the native trevc_*_dist; there each panel's arrival
+    gates its block of the solve)."""
+    import torch
+    import torch.distributed as dist
+    for lo, hi in block_panels(m, nb):
+        buf = torch.empty((hi - lo, hi), dtype=T.dtype, device=T.device)     # row q = column lo + q
+        if rank == 0:
+            buf.copy_(T[:hi, lo:hi].t())
+        dist.broadcast(buf, src=0, group=group)
+        if rank != 0:
+            T[:hi, lo:hi].copy_(buf.t())
+
+
+def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, group=None, nb: int = 128):
+    """The multi-GPU TriangEig step, torch.distributed form of the native trevc_*_dist sequence:
+    T's upper triangle from rank 0 panel by panel (block_panels order), this rank's block-cyclic
+    column shard solved with `solve_cols`, a status all-reduce (max of the ranks' codes), the
+    triangular shards (+ int32 exponents) all-gathered and unpacked on every rank.
 
     T: (m x m) tensor on every rank (contents only needed on rank 0; its upper triangle is
     overwritten elsewhere, the strictly lower triangle is not sent).
     solve_cols(T, cols, out) writes eigenvector cols[q] into column q of `out` (m x ncols,
     column-major) and returns the int32 exponents (ncols,).  Only rows 0..k of eigenvector k
     travel in the all-gather (tri_layout; the rest is zero by construction).
+    The same collective calls run on NCCL (GPU) and gloo (CPU tests).
     Returns (Z (m x m, column-major), e (m,) int32), identical on every rank."""
     import torch
     import torch.distributed as dist
     if world > 1:
-        buf = pack_upper(T, m) if rank == 0 else None
-        if rank != 0:
-            n = sum(c1 * (c1 - c0) for c0, c1 in _panels(m, 128))
-            buf = torch.empty(n, dtype=T.dtype, device=T.device)
-        dist.broadcast(buf, src=0, group=group)
-        if rank != 0:
-            unpack_upper(buf, T, m)
-        del buf
+        broadcast_panels(T, m, rank=rank, nb=nb, group=group)
     cols = shard_cols(m, world, rank, g)
     if world == 1:
         send = torch.empty((len(cols), m), dtype=T.dtype, device=T.device)   # row q = eigenvector q
@@ -149,7 +174,15 @@ def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, 
         return send.t(), e
     # this rank's shard, then only its upper-triangular part travels (≈ half the bytes)
     Zl = torch.empty((len(cols), m), dtype=T.dtype, device=T.device).t()   # m x ncols column-major
-    el = solve_cols(T, cols, Zl)
+    status = 0
+    try:
+        el = solve_cols(T, cols, Zl)
+    except Exception:                                                       # agree before the gather
+        status, el = 1, torch.zeros(len(cols), dtype=torch.int32, device=T.device)
+    st = torch.tensor([status], dtype=torch.int32, device=T.device)
+    dist.all_reduce(st, op=dist.ReduceOp.MAX, group=group)
+    if int(st.item()) != 0:
+        raise RuntimeError("trevc_sharded: the shard solve failed on a rank")
     lay, L = tri_layout(m, world, g)
     dev = T.device
     _, h_r, off_r = lay[rank]
@@ -158,18 +191,10 @@ def trevc_sharded(T, m: int, solve_cols, *, rank: int, world: int, g: int = 16, 
     mc = max_shard(m, world, g)
     epad = torch.zeros(mc, dtype=torch.int32, device=el.device)
     epad[: len(cols)] = el
-    backend = dist.get_backend(group)
-    if backend == "nccl":
-        out = torch.empty(world * L, dtype=send.dtype, device=dev)
-        eout = torch.empty(world * mc, dtype=torch.int32, device=el.device)
-        dist.all_gather_into_tensor(out, send, group=group)
-        dist.all_gather_into_tensor(eout, epad, group=group)
-    else:                                                                   # gloo (CPU tests)
-        outs = [torch.empty_like(send) for _ in range(world)]
-        eouts = [torch.empty_like(epad) for _ in range(world)]
-        dist.all_gather(outs, send, group=group)
-        dist.all_gather(eouts, epad, group=group)
-        out, eout = torch.cat(outs, 0), torch.cat(eouts, 0)
+    out = torch.empty(world * L, dtype=send.dtype, device=dev)
+    eout = torch.empty(world * mc, dtype=torch.int32, device=el.device)
+    dist.all_gather_into_tensor(out, send, group=group)
+    dist.all_gather_into_tensor(eout, epad, group=group)
     heights = np.concatenate([h for _, h, _ in lay])
     offsets = np.concatenate([off + r * L for r, (_, _, off) in enumerate(lay)])
     dst = np.concatenate([c for c, _, _ in lay]).astype(np.int64)

@@ -66,6 +66,21 @@ def test_pack_upper_roundtrip_keeps_the_upper_triangle():
     assert torch.equal(torch.triu(R), torch.triu(T))
 
 
+def test_block_panels_follow_the_block_partition():
+    """T travels in the panels the op N blocks consume, bottom-up (R9: the top block is short):
+    panel b = columns [lo_b, hi_b), rows 0 .. hi_b; together they cover the upper triangle once."""
+    for m, nb in [(1, 128), (300, 128), (1100, 128), (2048, 64), (97, 7)]:
+        pan = pdist.block_panels(m, nb)
+        assert pan[0][1] == m and pan[-1][0] == 0
+        for (lo, hi), (lo2, hi2) in zip(pan, pan[1:]):
+            assert hi2 == lo and hi - lo == nb
+        assert 0 < pan[-1][1] - pan[-1][0] <= nb
+        cover = np.zeros((m, m), int)
+        for lo, hi in pan:
+            cover[:hi, lo:hi] += 1
+        assert (np.triu(cover) == np.triu(np.ones((m, m), int))).all()
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -90,7 +105,7 @@ def _worker(rank, world, port, m, nb, cplx, out):
             out.copy_(torch.from_numpy(Zl))
             return torch.from_numpy(el)
 
-        Z, e = pdist.trevc_sharded(T, m, solve_cols, rank=rank, world=world, g=4)
+        Z, e = pdist.trevc_sharded(T, m, solve_cols, rank=rank, world=world, g=4, nb=nb)
         out[rank] = (Z.contiguous().numpy().copy(), e.numpy().copy())
     finally:
         dist.destroy_process_group()

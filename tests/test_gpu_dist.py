@@ -93,3 +93,36 @@ def test_triangular_pack_unpack_roundtrip(ms, cplx):
         Rh = host(R)
         for q, k in enumerate(c):
             assert np.array_equal(Rh[: k + 1, k], Zfull[: k + 1, k]) and not Rh[k + 1:, k].any()
+
+
+def test_trevc_dist_streamed_panels_unpack_path_bit_identical():
+    """The non-root side of the panel-streamed broadcast (panels unpacked from the broadcast buffer
+    into a workspace copy of T, the solve waiting for each panel's event, delta received rather
+    than computed) forced on the single rank with MSTRSM_DIST_TEST_UNPACK=1 (read at first use,
+    hence a subprocess): m = 1100 (look-ahead path, ragged top block) equals trevc bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = f"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1607_01477_b200 as ms
+from paper_1607_01477_b200 import inputs
+m = 1100
+T = torch.from_numpy(np.asfortranarray(inputs.c5_grcar_like(m))).cuda()
+ms.comm_init(1, 0)
+Z1, s1, e1 = ms.trevc_dist(T, m, nb=128)
+ms.comm_destroy()
+Z2, s2, e2 = ms.trevc(T, nb=128)
+torch.cuda.synchronize()
+print(json.dumps({{"Z": bool(torch.equal(Z1, Z2)), "e": bool(torch.equal(e1, e2)), "s": bool(torch.equal(s1, s2)),
+                   "rescaled": int((e2 < 0).sum().item())}}))
+"""
+    env = dict(os.environ, MSTRSM_DIST_TEST_UNPACK="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["Z"] and r["e"] and r["s"] and r["rescaled"] > 0, r
