@@ -39,12 +39,7 @@
 
 namespace mstrsm {
 
-// Offset of column l of the padded triangle (column l holds LPC (floor(l/LPC) + 1) elements:
-// rows 0 .. l-1 of U and zeros to the end of l's chunk).
-__host__ __device__ __forceinline__ int64_t padtri_off(int l, int lpc) {
-    const int64_t t = l / lpc, r = l % lpc;
-    return int64_t(lpc) * lpc * t * (t + 1) / 2 + r * lpc * (t + 1);
-}
+// (padtri_off, the padded triangle's column offsets: diag_kernel.cuh)
 
 // CTA shape of an instantiation: up to kSub substitution warps (G columns each) and, for the
 // safe variants, one replay warp per 32 of their columns.
@@ -468,7 +463,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
             const UAcc<T, false, OP == 1> ua{pk, nullptr, cn, nullptr, ST::zero(), 0.0};
             double g = g0;
             int kt2 = 0;
-            diag_rows<T, LPC, RPL, true, true>(y, pivot_f, ua, rl, nrow_f, nmax_f, failed, g, kt2);
+            diag_rows<T, LPC, RPL, true, LPC>(y, pivot_f, ua, rl, nrow_f, nmax_f, failed, g, kt2);
             finish(kt2, failed);
         }
     }

@@ -47,6 +47,7 @@ struct DiagArgs {
     int force_fb;                  // testing: hand every guarded column to the fallback
     int early;                     // U / cnl may be staged before waiting for the preceding grid
     int nsub;                      // diagw_kernel: substitution warps per CTA (set by the launcher)
+    T *Xscr; int64_t ldscr;        // diagl_kernel: per-column scratch of the solved rows (n_b rounded to 8 x n)
     // generalized solve (Alg. 7/8, op N): V with its norms, and the output C = -lambda_j X(I1,j)
     // (n_b x n, column j at Cbuf + j * ldc) that the V product of the update reads
     const T *V; int64_t ldv;
@@ -55,6 +56,13 @@ struct DiagArgs {
     // complex 3M update (nullable): Re + Im of the finished rows I1, Xsum[(row - lo) + j * ldxs]
     double *Xsum; int64_t ldxs;
 };
+
+// Offset of column l of the padded triangle with chunks of lpc rows (column l holds
+// lpc (floor(l/lpc) + 1) elements: rows 0 .. l-1 of U and zeros to the end of l's chunk).
+__host__ __device__ __forceinline__ int64_t padtri_off(int l, int lpc) {
+    const int64_t t = l / lpc, r = l % lpc;
+    return int64_t(lpc) * lpc * t * (t + 1) / 2 + r * lpc * (t + 1);
+}
 
 // Shared memory: the packed strictly upper triangle, the diagonal and cnl (generalized: the same
 // three for V as well).
@@ -385,9 +393,9 @@ __device__ __forceinline__ bool diag_lagged(T (&y)[RPL], PivF pivot, const Acc &
 
 // The synchronous guarded loop (fallback when phase 1 overflows): Alg. 4 step by step
 // with the rescales applied lazily through pend.
-// PADDED: the triangle is diag_fast.cuh's padded layout (column l at LPC^2 t(t+1)/2 + r LPC (t+1),
-// l = t LPC + r) instead of the packed one (column l at l(l-1)/2).
-template <typename T, int LPC, int RPL, bool GUARD, bool PADDED = false, typename PivF, typename Acc>
+// PADLPC > 0: the triangle is the padded layout of diag_fast.cuh / diag_tc.cuh with chunks of
+// PADLPC rows (column l at padtri_off(l, PADLPC)) instead of the packed one (column l at l(l-1)/2).
+template <typename T, int LPC, int RPL, bool GUARD, int PADLPC = 0, typename PivF, typename Acc>
 __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot, const Acc &ua,
                                           int rl, int nrow, int nmax, bool guarded, double &g, int &kt) {
     typedef S<T> ST;
@@ -438,7 +446,7 @@ __device__ __forceinline__ void diag_rows(T (&y)[RPL], PivF pivot, const Acc &ua
             }
             const T xr = in ? xv : ST::zero();
             // owner stores x_l; substitution within the block (P:315 / P:84): rows sc' < sc
-            const int col = PADDED ? LPC * LPC * t * (t + 1) / 2 + rr * LPC * (t + 1) : (sc * (sc - 1)) / 2;
+            const int col = PADLPC ? int(padtri_off(sc, PADLPC)) : (sc * (sc - 1)) / 2;
             {
                 const int i = rl + LPC * t;
                 if (rl < rr) y[t] = ST::fnms(y[t], xr, ua(col + i));

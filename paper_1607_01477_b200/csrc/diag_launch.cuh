@@ -6,6 +6,7 @@
 
 #include "runtime.cuh"
 #include "diag_fast.cuh"
+#include "diag_tc.cuh"
 
 namespace mstrsm {
 namespace rt {
@@ -161,6 +162,63 @@ int launch_diagf_pair(const DiagArgs<T> &a, int nb) {
     return 0;
 }
 
+// MSTRSM_DIAG=tc|w forces the left-looking tensor-pipe kernel (diagl, where its shared memory
+// fits) or the chunked one (diagw).  Default (measured, profiles/r02): diagl for real data (c2
+// 1.57 -> 1.35 ms, c1 0.228 -> 0.220 ms), diagw for complex (c4 88.5 ms vs 92.9 ms with diagl;
+// n_b = 128 complex does not fit diagl's scratch).
+inline int diag_impl() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_DIAG");
+        v = (e && e[0] == 'w') ? 1 : ((e && e[0] == 't') ? 2 : 0);
+    }
+    return v;
+}
+
+// The left-looking kernel keeps its per-warp scratch in shared memory: it is used when at least 8
+// substitution warps fit beside the block's triangle (n_b <= 64 complex, <= 96 real: c1, c2, c4);
+// larger blocks take the chunked kernel.
+template <typename T, bool SAFE>
+bool diagl_fits(int nfull) {
+    const int npad = (nfull + kDLTile - 1) / kDLTile * kDLTile;
+    return diagl_smem_bytes(npad, int(sizeof(T)), 8 * 8, SAFE) <= 227 * 1024;
+}
+
+template <typename T, bool SAFE, int OP>
+int launch_diagl(const DiagArgs<T> &a0) {
+    auto kern = diagl_kernel<T, SAFE, OP>;
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    const int nfull = int(a0.hi - a0.lo);
+    const int NT = (nfull + kDLTile - 1) / kDLTile, npad = NT * kDLTile;
+    const int64_t groups = cdiv(a0.ncols, 8);
+    const int64_t sms = g_cta_cap > 0 ? g_cta_cap : g_num_sms;
+    // substitution warps per CTA: as many as shared memory (the replay records grow with the CTA's
+    // columns) and the 16-warp CTA allow, then as few as the pass count needs
+    int kmax = 0;
+    for (int ns = kDLMaxSub; ns >= 1; ns--) {
+        if (ns + diagw_nrep(ns, 4, SAFE) > kDLMaxSub) continue;
+        if (diagl_smem_bytes(npad, int(sizeof(T)), ns * 8, SAFE) > 227 * 1024) continue;
+        kmax = ns;
+        break;
+    }
+    if (kmax == 0) return set_cuda_error(cudaErrorInvalidValue, "diagl_kernel: shared memory");
+    (void)0;
+    const int64_t npass = cdiv(groups, sms * kmax);
+    const int nsub = int(std::max<int64_t>(1, std::min<int64_t>(kmax, cdiv(groups, sms * npass))));
+    const int threads = (nsub + diagw_nrep(nsub, 4, SAFE)) * 32;
+    const size_t smem = size_t(diagl_smem_bytes(npad, int(sizeof(T)), nsub * 8, SAFE));
+    int grid = int(std::min<int64_t>(cdiv(groups, nsub), sms));
+    if (grid < 1) grid = 1;
+    DiagArgs<T> a = a0;
+    a.nsub = nsub;
+    const double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
+    ProfScope ps(PK_DIAG, fl);
+    CK(launch_k(kern, dim3(grid), dim3(threads), smem, g_stream, a));
+    CK_LAUNCH("diagl_kernel");
+    return 0;
+}
+
 // Layout of the chunked kernel: LPC lanes per column, RPL rows per lane (LPC RPL >= n_b).  Fewer
 // lanes per column pack more columns into a warp (the per-row chain -- quotient, shuffle,
 // replay -- is shared by more columns) but give each lane more rows (a longer update per row)
@@ -170,6 +228,9 @@ int launch_diagf_pair(const DiagArgs<T> &a, int nb) {
 template <typename T, bool SAFE, int OP>
 int launch_diag(const DiagArgs<T> &a, int nb) {
     if (diag_old()) return launch_diag_old<T, SAFE, OP>(a, nb);
+    const int impl = diag_impl();
+    if ((impl == 2 || (impl == 0 && !S<T>::cplx_)) && diagl_fits<T, SAFE>(int(a.hi - a.lo)))
+        return launch_diagl<T, SAFE, OP>(a);
     auto passes = [&](int lpc, int nsub) {
         const int64_t per_pass = int64_t(g_cta_cap > 0 ? g_cta_cap : g_num_sms) * nsub * (32 / lpc);
         return cdiv(a.ncols, per_pass);

@@ -65,6 +65,8 @@ struct Work {
     int *fb_list = nullptr, *fb_count = nullptr;   // diag fallback: column list, count per block
     int64_t *rowend = nullptr;
     void *shifts = nullptr;            // trevc: gathered diag(T)
+    void *xscr = nullptr;              // diagl_kernel scratch: n_b rounded up to 8 rows x n columns
+    int64_t ldscr = 0;
     cudaStream_t st = nullptr;
     ~Work() { ws_free(base, st); }
 };
@@ -79,6 +81,8 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
            o_E = take(std::max<int64_t>(nblk, 1) * n * 4), o_r = take(need_rowend ? n * 8 : 0),
            o_fl = take(n * 4), o_fc = take(std::max<int64_t>(nblk, 1) * 4),
            o_s = take(need_shifts ? n * sizeof(T) : 0);
+    const int64_t ldscr = (std::min(nb, 128) + 7) / 8 * 8;
+    const size_t o_x = take(size_t(ldscr) * std::max<int64_t>(n, 1) * sizeof(T));
     if (bytes_only) { *bytes_only = off; return 0; }
     w.st = g_stream;
     CK(ws_malloc(&w.base, off));
@@ -89,6 +93,8 @@ int alloc_work(Work &w, int64_t m, int64_t n, int nb, bool need_rowend, bool nee
     w.fb_list = (int *)(b + o_fl); w.fb_count = (int *)(b + o_fc);
     w.rowend = need_rowend ? (int64_t *)(b + o_r) : nullptr;
     w.shifts = need_shifts ? (void *)(b + o_s) : nullptr;
+    w.xscr = (void *)(b + o_x);
+    w.ldscr = ldscr;
     return 0;
 }
 
@@ -212,6 +218,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
         a.force_fb = g_diag_force_fb;
         a.early = early;
+        a.Xscr = static_cast<T *>(w.xscr); a.ldscr = w.ldscr;
         a.Xsum = Xsum; a.ldxs = ldxs;
         if (Xsum && rowend_dev && !rowend_sorted_host)        // inactive columns in range: zero rows
             CK(cudaMemsetAsync(Xsum + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
@@ -287,6 +294,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
         a.force_fb = g_diag_force_fb;
         a.early = early;
+        a.Xscr = static_cast<T *>(w.xscr); a.ldscr = w.ldscr;
         a.Xsum = xs; a.ldxs = ldxs;
         if (xs && rowend_dev && !rowend_sorted_host)          // inactive columns in range: zero rows
             CK(cudaMemsetAsync(xs + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));

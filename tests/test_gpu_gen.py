@@ -77,8 +77,10 @@ def test_gpu_generalized_hand_rescale_cases(ms):
 
 @pytest.mark.parametrize("cplx", [False, True])
 def test_gpu_V_identity_equals_the_standard_gpu_solve(ms, cplx):
-    """V = I: the generalized kernels reduce to the standard ones (U - s*1, U(i,l) - s*0, zero V
-    products are exact), so the two GPU paths agree bit for bit."""
+    """V = I: the generalized solve reduces to the standard one (U - s*1, U(i,l) - s*0, zero V
+    products are exact).  The standard path's diagonal step sums its in-block update on the tensor
+    pipe (diag_tc.cuh) and the generalized one row by row, so the two agree to rounding (R24):
+    same exponents, normwise 1e-12."""
     m, n = 300, 70
     U = _upper(m, cplx, 1)
     s = inputs.random_shifts(n, cplx, 3, radius=0.9)
@@ -87,7 +89,8 @@ def test_gpu_V_identity_equals_the_standard_gpu_solve(ms, cplx):
         Xg, _, eg = gpu_gen(ms, U, np.eye(m, dtype=U.dtype), s, B, safe=safe, nb=64)
         X, _, e = ms.solve(dev(U), dev(np.ascontiguousarray(s)), dev(B), safe=safe, nb=64)
         _sync()
-        assert np.array_equal(Xg, host(X)) and np.array_equal(eg, host(e))
+        rel, de = assert_parity(Xg, eg, host(X), host(e), tol=1e-12, what="V = I")
+        assert not de.any()
 
 
 SHAPES = [(1, 1, 8), (7, 3, 8), (100, 37, 32), (129, 64, 64), (333, 130, 64), (257, 129, 16)]
