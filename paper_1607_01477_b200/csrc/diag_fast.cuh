@@ -112,12 +112,34 @@ __device__ __forceinline__ void dw_mbar_init(uint64_t *b, int count) {
 __device__ __forceinline__ void dw_mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+// Device-side checks of the diagonal kernels' shared-memory indexing and barrier protocol
+// (compute-sanitizer is unavailable on the GPU pool): built with -DMSTRSM_DEVICE_CHECKS
+// (tools/build_checks.sh), a failed check prints its site and traps.
+#ifdef MSTRSM_DEVICE_CHECKS
+#define DW_CHECK(cond, what)                                                                   \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("mstrsm device check failed: %s (block %d thread %d)\n", what, int(blockIdx.x), \
+                   int(threadIdx.x));                                                          \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define DW_CHECK(cond, what) do { } while (0)
+#endif
+
 __device__ __forceinline__ void dw_mbar_wait(uint64_t *b, int parity) {
     uint32_t done = 0;
+#ifdef MSTRSM_DEVICE_CHECKS
+    long long spins = 0;
+#endif
     do {
         asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
                      " selp.u32 %0, 1, 0, p;\n}\n"
                      : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+#ifdef MSTRSM_DEVICE_CHECKS
+        DW_CHECK(++spins < (1ll << 26), "mbarrier wait does not complete (protocol deadlock)");
+#endif
     } while (!done);
 }
 
@@ -156,6 +178,7 @@ __device__ __forceinline__ bool diagw_rows(T (&y)[RPL], PivF pivot, const T *__r
             const T *pc = pk + (LPC * LPC * t * (t + 1) / 2 + rl) + rr_hi * kStride;
 #pragma unroll 1
             for (int rr = rr_hi; rr >= 0; rr--, pc -= kStride) {
+                DW_CHECK(pc >= pk && pc + LPC * t < pk + padtri_off(t * LPC + rr + 1, LPC), "diagw row pointer");
                 const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);      // P:82 / P:297
                 y[t] = ST::fnms(y[t], xl, uget(pc + LPC * t));             // zero for rows >= l
 #pragma unroll
@@ -166,6 +189,7 @@ __device__ __forceinline__ bool diagw_rows(T (&y)[RPL], PivF pivot, const T *__r
             if constexpr (REC) {
                 const double ax = modv(xo);
                 nonfinite |= !(ax <= 1.7976931348623157e308);
+                DW_CHECK(t * LPC + rl < LPC * RPL, "diagw record row");
                 rec[(t * LPC + rl) * ldrec] = ax;
                 if (rl == 0) fp[t * ldrec] = F;
                 const int em = group_imax<LPC>(bexp(ax));
@@ -219,6 +243,8 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
         const int cq = idx >> 7, r = idx & 127;                            // U(lo + r, lo + cq)
         if (r < cq) {
             const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;
+            DW_CHECK(padtri_off(cq, LPC) + r < padtri_off(nfull, LPC) &&
+                         padtri_off(nfull - 1 - r, LPC) + (nfull - 1 - cq) < padtri_off(nfull, LPC), "diagw staging index");
             if (OP == 0) cp_async<sizeof(T)>(pk + padtri_off(cq, LPC) + r, src, true);
             else cp_async<sizeof(T)>(pk + padtri_off(nfull - 1 - r, LPC) + (nfull - 1 - cq), src, true);
         }

@@ -124,6 +124,8 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         const int cq = idx >> 7, r = idx & 127;                            // U(lo + r, lo + cq)
         if (r < cq) {
             const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;
+            DW_CHECK(padtri_off(cq, TR) + r < padtri_off(npad, TR) &&
+                         padtri_off(nfull - 1 - r, TR) + (nfull - 1 - cq) < padtri_off(npad, TR), "diagl staging index");
             if (OP == 0) cp_async<sizeof(T)>(pk + padtri_off(cq, TR) + r, src, true);
             else cp_async<sizeof(T)>(pk + padtri_off(nfull - 1 - r, TR) + (nfull - 1 - cq), src, true);
         }
@@ -291,6 +293,9 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                     int stp_a = 64 * (u + 2) + 8 * tq, stp_b = stp_a + 32;
 #pragma unroll 2
                     for (int w = u + 1; w < NT; w++) {
+                        DW_CHECK(ua_p == pk + u * TR + gq + padtri_off(w * TR + tq, TR) &&
+                                 ub_p == pk + u * TR + gq + padtri_off(w * TR + 4 + tq, TR) &&
+                                 xa_p == xs + w * TR + tq && w * TR + 4 + tq < npad, "diagl k-step operands");
                         const T nxa = xa_p[0], nxb = xa_p[4];
                         const T ua = *ua_p, ub = *ub_p;
                         dl_kstep<T, CONJ>(y0, y1, nxa, ua);
@@ -322,6 +327,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                 T x0 = p0.apply(y0), x1 = p1.apply(y1);                    // = the shuffled values
                 const double ax0 = modv(x0), ax1 = modv(x1);
                 if (rec) {
+                    DW_CHECK(r0 + 1 < npad && c < C, "diagl record row");
                     nonfinite |= !(ax0 <= 1.7976931348623157e308) || !(ax1 <= 1.7976931348623157e308);
                     s_rec[r0 * C + c] = ax0;
                     s_rec[(r0 + 1) * C + c] = ax1;
