@@ -58,6 +58,7 @@ __global__ void norm_rows_c_kernel(const T *__restrict__ U, int64_t ldu, int64_t
     int64_t hi = l < m ? block_rows(1, m, nb, l / nb).hi : m;
     double c = 0.0, p = 0.0;
     bool bad = false;
+#pragma unroll 4
     for (int64_t i = l0; i < m; i++) {
         if (l < m && i >= l) {
             double a = S<T>::mod(U[l + i * ldu]);
@@ -90,7 +91,7 @@ __global__ void panel_sum_kernel(int op, int64_t m, int nb, int64_t nblk,
 // ||U||_inf for delta (R4).  op N: row sums sum_{k >= i} |U(i,k)|, ascending k, one thread per
 // row, warp walks columns in lockstep (coalesced).  op C: column sums sum_{l = i..0} |U(l,i)|
 // (= rows of U^H), descending l, one thread per column.
-constexpr int kRowsumChunk = 256;   // columns per partial sum
+constexpr int kRowsumChunk = 64;    // columns per partial sum (more chunks: more loads in flight)
 
 template <typename T>
 __global__ void rowsum_n_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
@@ -100,13 +101,12 @@ __global__ void rowsum_n_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
     // deterministic; differs from a single sequential sum only in rounding, which moves delta
     // by ulps).
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    int64_t i0 = int64_t(blockIdx.x) * blockDim.x;
     int64_t k0 = int64_t(blockIdx.y) * kRowsumChunk, k1 = k0 + kRowsumChunk < m ? k0 + kRowsumChunk : m;
     double s = 0.0;
-    if (k1 > i0) {
-        int64_t kb = k0 > i0 ? k0 : i0;
-        for (int64_t k = kb; k < k1; k++)
-            if (i < m && k >= i) s = __dadd_rn(s, S<T>::mod(U[i + k * ldu]));
+    if (i < m && k1 > i) {
+        const int64_t kb = k0 > i ? k0 : i;
+#pragma unroll 8
+        for (int64_t k = kb; k < k1; k++) s = __dadd_rn(s, S<T>::mod(U[i + k * ldu]));   // ascending k
     }
     if (i < m) part[int64_t(blockIdx.y) * m + i] = s;
 }
@@ -126,7 +126,8 @@ __global__ void colsum_c_kernel(const T *__restrict__ U, int64_t ldu, int64_t m,
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
     double s = 0.0;
-    for (int64_t l = i; l >= 0; l--) s = __dadd_rn(s, S<T>::mod(U[l + i * ldu]));
+#pragma unroll 8
+    for (int64_t l = i; l >= 0; l--) s = __dadd_rn(s, S<T>::mod(U[l + i * ldu]));   // descending l
     rs[i] = s;
 }
 

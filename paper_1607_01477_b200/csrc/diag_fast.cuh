@@ -239,10 +239,9 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
     //      cnl are never written during a solve, so a launch after the solve's first one stages
     //      them before waiting for the preceding grid (a.early) ----
     if (!a.early) pdl_wait();
-    for (int idx = tid; idx < nfull * 128; idx += nth) {
-        const int cq = idx >> 7, r = idx & 127;                            // U(lo + r, lo + cq)
-        if (r < cq) {
-            const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;
+    for (int cq = tid >> 5; cq < nfull; cq += nth >> 5) {                 // a warp per column of U,
+        for (int r = tid & 31; r < cq; r += 32) {                           // lanes down its rows
+            const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;         // U(lo + r, lo + cq)
             DW_CHECK(padtri_off(cq, LPC) + r < padtri_off(nfull, LPC) &&
                          padtri_off(nfull - 1 - r, LPC) + (nfull - 1 - cq) < padtri_off(nfull, LPC), "diagw staging index");
             if (OP == 0) cp_async<sizeof(T)>(pk + padtri_off(cq, LPC) + r, src, true);

@@ -120,10 +120,9 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
     //      nfull .. npad-1 all zero), its diagonal (1 past nfull) and cnl (0 past nfull).  U and
     //      cnl are never written during a solve: launches after the first stage before the wait ----
     if (!a.early) pdl_wait();
-    for (int idx = tid; idx < nfull * 128; idx += nth) {
-        const int cq = idx >> 7, r = idx & 127;                            // U(lo + r, lo + cq)
-        if (r < cq) {
-            const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;
+    for (int cq = tid >> 5; cq < nfull; cq += nth >> 5) {                 // a warp per column of U,
+        for (int r = tid & 31; r < cq; r += 32) {                           // lanes down its rows
+            const T *src = a.U + (a.lo + r) + (a.lo + cq) * a.ldu;         // U(lo + r, lo + cq)
             DW_CHECK(padtri_off(cq, TR) + r < padtri_off(npad, TR) &&
                          padtri_off(nfull - 1 - r, TR) + (nfull - 1 - cq) < padtri_off(npad, TR), "diagl staging index");
             if (OP == 0) cp_async<sizeof(T)>(pk + padtri_off(cq, TR) + r, src, true);
