@@ -170,7 +170,7 @@ inline int diag_impl() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MSTRSM_DIAG");
-        v = (e && e[0] == 'w') ? 1 : ((e && e[0] == 't') ? 2 : 0);
+        v = (e && e[0] == 'w') ? 1 : ((e && e[0] == 't') ? 2 : ((e && e[0] == 'g') ? 3 : 0));
     }
     return v;
 }
@@ -184,9 +184,9 @@ bool diagl_fits(int nfull) {
     return diagl_smem_bytes(npad, int(sizeof(T)), 8 * 8, SAFE) <= 227 * 1024;
 }
 
-template <typename T, bool SAFE, int OP>
+template <typename T, bool SAFE, int OP, bool GSCR = false>
 int launch_diagl(const DiagArgs<T> &a0) {
-    auto kern = diagl_kernel<T, SAFE, OP>;
+    auto kern = diagl_kernel<T, SAFE, OP, GSCR>;
     static std::atomic<uint64_t> attr_set{0};
     if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     const int nfull = int(a0.hi - a0.lo);
@@ -198,7 +198,7 @@ int launch_diagl(const DiagArgs<T> &a0) {
     int kmax = 0;
     for (int ns = kDLMaxSub; ns >= 1; ns--) {
         if (ns + diagw_nrep(ns, 4, SAFE) > kDLMaxSub) continue;
-        if (diagl_smem_bytes(npad, int(sizeof(T)), ns * 8, SAFE) > 227 * 1024) continue;
+        if (diagl_smem_bytes(npad, int(sizeof(T)), ns * 8, SAFE, GSCR) > 227 * 1024) continue;
         kmax = ns;
         break;
     }
@@ -207,7 +207,7 @@ int launch_diagl(const DiagArgs<T> &a0) {
     const int64_t npass = cdiv(groups, sms * kmax);
     const int nsub = int(std::max<int64_t>(1, std::min<int64_t>(kmax, cdiv(groups, sms * npass))));
     const int threads = (nsub + diagw_nrep(nsub, 4, SAFE)) * 32;
-    const size_t smem = size_t(diagl_smem_bytes(npad, int(sizeof(T)), nsub * 8, SAFE));
+    const size_t smem = size_t(diagl_smem_bytes(npad, int(sizeof(T)), nsub * 8, SAFE, GSCR));
     int grid = int(std::min<int64_t>(cdiv(groups, nsub), sms));
     if (grid < 1) grid = 1;
     DiagArgs<T> a = a0;
@@ -231,6 +231,7 @@ int launch_diag(const DiagArgs<T> &a, int nb) {
     const int impl = diag_impl();
     if ((impl == 2 || (impl == 0 && !S<T>::cplx_)) && diagl_fits<T, SAFE>(int(a.hi - a.lo)))
         return launch_diagl<T, SAFE, OP>(a);
+    if (impl == 3 && a.Xscr) return launch_diagl<T, SAFE, OP, true>(a);   // MSTRSM_DIAG=g: global scratch
     auto passes = [&](int lpc, int nsub) {
         const int64_t per_pass = int64_t(g_cta_cap > 0 ? g_cta_cap : g_num_sms) * nsub * (32 / lpc);
         return cdiv(a.ncols, per_pass);

@@ -89,11 +89,14 @@ __device__ __forceinline__ double dl_gprod_ru(double v) {
 __host__ __device__ inline int64_t diagl_scr_offset(int npad, int esize, int ncol, bool safe) {
     return (diagw_smem(npad, kDLTile, npad / kDLTile, esize, ncol, safe).total + 15) & ~int64_t(15);
 }
-__host__ __device__ inline int64_t diagl_smem_bytes(int npad, int esize, int ncol, bool safe) {
-    return diagl_scr_offset(npad, esize, ncol, safe) + int64_t(ncol) * (npad + 1) * esize;
+__host__ __device__ inline int64_t diagl_smem_bytes(int npad, int esize, int ncol, bool safe, bool gscr = false) {
+    return diagl_scr_offset(npad, esize, ncol, safe) + (gscr ? 0 : int64_t(ncol) * (npad + 1) * esize);
 }
 
-template <typename T, bool SAFE, int OP>
+// GSCR: the solved rows' scratch lives in global memory (a.Xscr, L2-resident; for blocks whose
+// triangle leaves no room for it in shared memory: n_b = 128 complex), read through a 4-deep
+// register prefetch ring; otherwise in shared memory.
+template <typename T, bool SAFE, int OP, bool GSCR = false>
 __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> a) {
     typedef S<T> ST;
     constexpr int G = 8, TR = kDLTile;
@@ -231,8 +234,9 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         T sh = active ? a.shifts[j * a.sstride] : ST::zero();
         if (OP == 1) sh = ST::conj(sh);
         T *x = a.B + j * a.ldb;
-        T *xs = reinterpret_cast<T *>(smem_raw + diagl_scr_offset(npad, int(sizeof(T)), C, SAFE)) +
-                c * (npad + 1);                                            // -x of the solved rows
+        T *xs = GSCR ? a.Xscr + j * a.ldscr
+                     : reinterpret_cast<T *>(smem_raw + diagl_scr_offset(npad, int(sizeof(T)), C, SAFE)) +
+                           c * (npad + 1);                                 // -x of the solved rows
         auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
         auto pivot = [&](int sc) -> T {                                    // d_l = U(l,l) - s_j
             T dd = sc < nrow ? ST::sub(dg[sc], sh) : ST::real(1.0);
@@ -270,12 +274,21 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         int F = 0;                                                         // this column's frame
         double axm = 0.0;                                                  // max |x|, frame F
         bool nonfinite = false;
+        T py0 = ST::zero(), py1 = ST::zero();                              // next tile's right-hand sides
+        {
+            const int r0 = (NT - 1) * TR + 2 * tq;
+            py0 = r0 < nrow ? x[rowof(r0)] : ST::zero();
+            py1 = r0 + 1 < nrow ? x[rowof(r0 + 1)] : ST::zero();
+        }
 #pragma unroll 1
         for (int u = NT - 1; u >= 0; u--) {
             const int r0 = u * TR + 2 * tq;                                // this lane's rows r0, r0 + 1
+            T y0 = py0, y1 = py1;                                          // (loaded one tile ahead)
+            if (u > 0) {                                                   // prefetch the next tile's rows
+                py0 = r0 - TR < nrow ? x[rowof(r0 - TR)] : ST::zero();
+                py1 = r0 - TR + 1 < nrow ? x[rowof(r0 - TR + 1)] : ST::zero();
+            }
             if (u * TR < nmax) {                                           // warp-uniform
-                T y0 = r0 < nrow ? x[rowof(r0)] : ST::zero();
-                T y1 = r0 + 1 < nrow ? x[rowof(r0 + 1)] : ST::zero();
                 if (F != 0) {                                              // into the column's frame
                     y0 = dl_scale1(y0, -F);
                     y1 = dl_scale1(y1, -F);
@@ -290,6 +303,37 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                     const T *ub_p = pk + u * TR + gq + padtri_off((u + 1) * TR + 4 + tq, TR);
                     const T *xa_p = xs + (u + 1) * TR + tq;
                     int stp_a = 64 * (u + 2) + 8 * tq, stp_b = stp_a + 32;
+                    if constexpr (GSCR) {
+                        // scratch in L2: loads run 4 k-step pairs ahead of their DMMAs
+                        constexpr int PD = 4;
+                        const int nw = NT - 1 - u;
+                        T ra[PD], rb[PD];
+#pragma unroll
+                        for (int i = 0; i < PD; i++) {
+                            ra[i] = i < nw ? xa_p[TR * i] : ST::zero();
+                            rb[i] = i < nw ? xa_p[TR * i + 4] : ST::zero();
+                        }
+#pragma unroll 1
+                        for (int w0 = 0; w0 < nw; w0 += PD) {
+#pragma unroll
+                            for (int i = 0; i < PD; i++) {
+                                if (w0 + i < nw) {
+                                    const T nxa = ra[i], nxb = rb[i];
+                                    if (w0 + i + PD < nw) {
+                                        ra[i] = xa_p[TR * (w0 + i + PD)];
+                                        rb[i] = xa_p[TR * (w0 + i + PD) + 4];
+                                    }
+                                    const T ua = *ua_p, ub = *ub_p;
+                                    dl_kstep<T, CONJ>(y0, y1, nxa, ua);
+                                    dl_kstep<T, CONJ>(b0, b1, nxb, ub);
+                                    ua_p += stp_a;
+                                    ub_p += stp_b;
+                                    stp_a += 64;
+                                    stp_b += 64;
+                                }
+                            }
+                        }
+                    } else
 #pragma unroll 2
                     for (int w = u + 1; w < NT; w++) {
                         DW_CHECK(ua_p == pk + u * TR + gq + padtri_off(w * TR + tq, TR) &&
