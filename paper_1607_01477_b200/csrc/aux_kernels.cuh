@@ -277,6 +277,69 @@ __global__ void trevc_prepass_kernel(const T *__restrict__ Tm, int64_t ldt, int6
     }
 }
 
+// trevc_prepass_kernel for the columns [k0, k1) of one panel of T (the multi-GPU path runs it as
+// each panel arrives): the same values, with every column split over gridDim.y row chunks so that
+// one panel fills the GPU.  The maxima are combined with atomicMax on the bit patterns
+// (non-negative doubles order like their bits; max is exact, so the result does not depend on
+// the order): cnl, pcol and G must be zero beforehand.  Chunk 0 writes the per-column scalars.
+__device__ __forceinline__ void atomic_max_nonneg(double *a, double v) {
+    atomicMax(reinterpret_cast<unsigned long long *>(a), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+template <typename T>
+__global__ void trevc_prepass_panel_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t m, int nb,
+                                           double *__restrict__ cnl, double *__restrict__ pcol,
+                                           T *__restrict__ Z, int64_t ldz, T *__restrict__ shifts,
+                                           int64_t *__restrict__ rowend, double *__restrict__ G, int *__restrict__ e,
+                                           double *__restrict__ P, int64_t ldp, int *__restrict__ nonfinite,
+                                           const int *__restrict__ qof, int64_t k0, int64_t k1, int64_t rchunk) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t r0 = int64_t(blockIdx.y) * rchunk, r1 = r0 + rchunk < m ? r0 + rchunk : m;
+    for (int64_t k = k0 + w; k < k1; k += nw) {
+        const int64_t b = (m - 1 - k) / nb;
+        const Blk bl = block_rows(0, m, nb, b);
+        const T *tc = Tm + k * ldt;
+        const int64_t q = qof ? int64_t(qof[k]) : k;
+        T *z = q >= 0 ? Z + q * ldz : nullptr;
+        double c = 0.0, p = 0.0;
+        bool bad = false;
+        for (int64_t l = r0 + lane; l < r1; l += 32) {
+            if (l < k) {
+                const T v = tc[l];
+                const double a = S<T>::mod(v);
+                bad |= !(a <= 1.7976931348623157e308);
+                if (l < bl.lo) p = fmax(p, a);
+                else c = fmax(c, a);
+                if (z) z[l] = S<T>::neg(v);
+                if constexpr (S<T>::cplx_) {
+                    if (P) P[l + k * ldp] = __dadd_rn(v.x, v.y);
+                }
+            } else if (z) {
+                z[l] = S<T>::zero();
+            }
+        }
+        c = warp_max(c);
+        p = warp_max(p);
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            if (c > 0.0) atomic_max_nonneg(cnl + k, c);
+            if (p > 0.0) atomic_max_nonneg(pcol + k, p);
+            if (q >= 0 && fmax(c, p) > 0.0) atomic_max_nonneg(G + q, fmax(c, p));
+            if (blockIdx.y == 0) {
+                const T d = tc[k];
+                if (q >= 0) {
+                    shifts[q] = d;
+                    rowend[q] = k;
+                    e[q] = 0;
+                }
+                if (!(S<T>::mod(d) <= 1.7976931348623157e308)) atomicExch(nonfinite, 1);
+            }
+            if (bad) atomicExch(nonfinite, 1);
+        }
+    }
+}
+
 // a.1 init for GeneralizedTriangEig (Alg. 9).  Column q holds eigenvector k = q:
 //   lambda_q = T(k,k) / S(k,k);  Z(l,q) = S(l,k) lambda_q - T(l,k) for l < k, 0 for l >= k;
 //   G_q = max_{l<k} |Z(l,q)|;  row_end_q = k.

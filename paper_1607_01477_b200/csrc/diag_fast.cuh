@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
     const int grp = lane / LPC, rl = lane % LPC;
     const int c = warp * G + grp;                                         // column slot in the CTA
     const double delta = SAFE ? a.delta[0] : 0.0;
-    const double Pb = SAFE ? a.P[a.b] : 0.0;
+    const double Pb = SAFE ? diag_panel_sum(a) : 0.0;
     int pass = 0;
     for (int64_t cb = int64_t(blockIdx.x) * C; cb < ncols; cb += cstride, pass++) {
         const int64_t q = cb + c;

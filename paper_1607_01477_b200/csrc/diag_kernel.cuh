@@ -48,6 +48,7 @@ struct DiagArgs {
     int early;                     // U / cnl may be staged before waiting for the preceding grid
     int nsub;                      // diagw_kernel: substitution warps per CTA (set by the launcher)
     T *Xscr; int64_t ldscr;        // diagl_kernel: per-column scratch of the solved rows (n_b rounded to 8 x n)
+    const double *Ppart;           // nullable: P_b = sum of Ppart[k], k in [lo, hi) ascending (else P[b])
     // generalized solve (Alg. 7/8, op N): V with its norms, and the output C = -lambda_j X(I1,j)
     // (n_b x n, column j at Cbuf + j * ldc) that the V product of the update reads
     const T *V; int64_t ldv;
@@ -56,6 +57,17 @@ struct DiagArgs {
     // complex 3M update (nullable): Re + Im of the finished rows I1, Xsum[(row - lo) + j * ldxs]
     double *Xsum; int64_t ldxs;
 };
+
+template <typename T> struct DiagArgs;
+// P_b of the block (R6): the precomputed panel sum, or -- when the multi-GPU path fed the
+// panels one by one -- the ascending sum of the panel's per-column maxima (as panel_sum_kernel)
+template <typename T>
+__device__ __forceinline__ double diag_panel_sum(const DiagArgs<T> &a) {
+    if (!a.Ppart) return a.P[a.b];
+    double s = 0.0;
+    for (int64_t k = a.lo; k < a.hi; k++) s = __dadd_rn(s, a.Ppart[k]);
+    return s;
+}
 
 // Offset of column l of the padded triangle with chunks of lpc rows (column l holds
 // lpc (floor(l/lpc) + 1) elements: rows 0 .. l-1 of U and zeros to the end of l's chunk).
@@ -535,7 +547,7 @@ __global__ void __launch_bounds__(DiagThreads<T, RPL>::value, 1) diag_kernel(Dia
     const int64_t wid = (int64_t(blockIdx.x) * nth + tid) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * nth) >> 5;
     const double delta = SAFE ? a.delta[0] : 0.0;
-    const double Pb = SAFE ? a.P[a.b] : 0.0;
+    const double Pb = SAFE ? diag_panel_sum(a) : 0.0;
     const double PbV = SAFE && GEN ? a.PV[a.b] : 0.0;
     const double rawU = SAFE && GEN ? a.delta[1] : 0.0, rawV = SAFE && GEN ? a.deltaV[1] : 0.0;
 

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
     const int gq = lane >> 2, tq = lane & 3;
     const int c = warp * G + gq;                                          // column slot in the CTA
     const double delta = SAFE ? a.delta[0] : 0.0;
-    const double Pb = SAFE ? a.P[a.b] : 0.0;
+    const double Pb = SAFE ? diag_panel_sum(a) : 0.0;
     int pass = 0;
     for (int64_t cb = int64_t(blockIdx.x) * C; cb < ncols; cb += cstride, pass++) {
         const int64_t q = cb + c;

@@ -158,6 +158,13 @@ int compute_delta_n(const T *U, int64_t ldu, int64_t m, double *rs, double *delt
 // diagonal step, on the library stream.  The multi-GPU path uses it to wait for T's panel b and run
 // that panel's prepass as the panels arrive (trevc_impl with panel_ready).
 thread_local const std::function<int(int64_t)> *t_pre_block = nullptr;
+// ... and may point block b at its own copy of the triangle's panel b (columns [lo_b, hi_b), rows
+// 0 .. hi_b): U(i, k) of block b is t_blk_U[i + k * t_blk_ld] (nullptr: the solve's U, ldu).
+thread_local const void *t_blk_U = nullptr;
+thread_local int64_t t_blk_ld = 0;
+// With the per-block hook: the panel sums P_b are formed by the diagonal kernel from these
+// per-column panel maxima (the same ascending sum panel_sum_kernel does) instead of a launch.
+thread_local const double *t_panel_part = nullptr;
 
 // ---------------------------------------------------------------- look-ahead (op N, safe)
 // Look-ahead (default; MSTRSM_LOOKAHEAD=0 disables): block b's update is split into its top n_b rows (the next diagonal block,
@@ -200,6 +207,8 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         if (t_pre_block) {
             if (int rc = (*t_pre_block)(b)) return rc;
         }
+        const T *Ub = t_blk_U ? static_cast<const T *>(t_blk_U) : U;   // this block's view of U
+        const int64_t ldub = t_blk_U ? t_blk_ld : ldu;
         Blk bl = block_rows(op, m, nb, b);
         int64_t c0 = 0;
         if (op == 0 && rowend_sorted_host) {
@@ -209,7 +218,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         int64_t ncols = n - c0;
         if (ncols <= 0) continue;
         DiagArgs<T> a{};
-        a.U = U; a.ldu = ldu; a.m = m; a.shifts = shifts; a.sstride = sstride;
+        a.U = Ub; a.ldu = ldub; a.m = m; a.shifts = shifts; a.sstride = sstride;
         a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
         a.rowend = op == 0 ? rowend_dev : nullptr;
         a.lo = bl.lo; a.hi = bl.hi; a.b = b;
@@ -219,6 +228,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         a.force_fb = g_diag_force_fb;
         a.early = early;
         a.Xscr = static_cast<T *>(w.xscr); a.ldscr = w.ldscr;
+        a.Ppart = t_panel_part;
         a.Xsum = Xsum; a.ldxs = ldxs;
         if (Xsum && rowend_dev && !rowend_sorted_host)        // inactive columns in range: zero rows
             CK(cudaMemsetAsync(Xsum + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
@@ -232,7 +242,7 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         int64_t M = op == 0 ? bl.lo : m - bl.hi;
         if (M <= 0) continue;
         GemmArgs<T> g{};
-        g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
+        g.U = Ub; g.ldu = ldub; g.B = B; g.ldb = ldb;
         g.M = M; g.N = ncols; g.K = int(bl.hi - bl.lo);
         if (op == 0) { g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0; }
         else { g.a_r0 = bl.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
@@ -278,6 +288,8 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         if (t_pre_block) {
             if ((rc = (*t_pre_block)(b))) break;
         }
+        const T *Ub = t_blk_U ? static_cast<const T *>(t_blk_U) : U;   // this block's view of U
+        const int64_t ldub = t_blk_U ? t_blk_ld : ldu;
         const Blk bl = block_rows(0, m, nb, b);
         const int64_t c0 = c0_of(bl), ncols = n - c0;
         if (ncols <= 0) { diag_cap = 0; continue; }
@@ -285,7 +297,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         int *dblk = par ? w.dblk2 : w.dblk;
         double *xs = Xsum ? (par ? Xsum2 : Xsum) : nullptr;
         DiagArgs<T> a{};
-        a.U = U; a.ldu = ldu; a.m = m; a.shifts = shifts; a.sstride = sstride;
+        a.U = Ub; a.ldu = ldub; a.m = m; a.shifts = shifts; a.sstride = sstride;
         a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
         a.rowend = rowend_dev;
         a.lo = bl.lo; a.hi = bl.hi; a.b = b;
@@ -295,6 +307,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         a.force_fb = g_diag_force_fb;
         a.early = early;
         a.Xscr = static_cast<T *>(w.xscr); a.ldscr = w.ldscr;
+        a.Ppart = t_panel_part;
         a.Xsum = xs; a.ldxs = ldxs;
         if (xs && rowend_dev && !rowend_sorted_host)          // inactive columns in range: zero rows
             CK(cudaMemsetAsync(xs + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
@@ -307,7 +320,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         const int64_t M = bl.lo;
         if (M <= 0) continue;
         GemmArgs<T> g{};
-        g.U = U; g.ldu = ldu; g.B = B; g.ldb = ldb;
+        g.U = Ub; g.ldu = ldub; g.B = B; g.ldb = ldb;
         g.N = ncols; g.K = int(bl.hi - bl.lo);
         g.a_c0 = bl.lo; g.x_r0 = bl.lo; g.col0 = c0;
         g.X = B; g.ldx = ldb;
@@ -465,14 +478,20 @@ int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T
     return 0;
 }
 
-// panel_ready (nullable): nblk events, op N block order (b = 0: the last panel of columns); block
-// b waits for panel_ready[b] (columns [lo_b, hi_b) of T, rows 0 .. hi_b, have arrived) and runs that
-// panel's prepass first.  delta_ext (with panel_ready): delta[0..1] of T (R4), valid once
-// panel_ready[0] has completed.
+// T fed panel by panel (the multi-GPU path): `enqueue(b)` puts the arrival of panel b -- columns
+// [lo_b, hi_b) of T, rows 0 .. hi_b, op N block order (b = 0: the last columns) -- on stream cs;
+// delta[0..1] (R4) is valid on cs before panel 0.  trevc_impl puts each panel's prepass on cs
+// right behind its arrival and makes block b wait only for that.
+struct PanelFeed {
+    cudaStream_t cs;
+    std::function<int(int64_t)> enqueue;
+    const double *delta;
+    std::function<void(int64_t, const void **, int64_t *)> view;   // nullable: block b's copy of panel b
+};
+
 template <typename T>
 int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
-               T *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb,
-               const double *delta_ext = nullptr, const cudaEvent_t *panel_ready = nullptr) {
+               T *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb, const PanelFeed *feed = nullptr) {
     if (m < 0) return -3;
     if (ldt < std::max<int64_t>(1, m)) return -2;
     if (ncols < 0) return -5;
@@ -505,7 +524,12 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
     }
     if (int rc = make_sum_planes<T>(sp, 0, Tm, ldt, m, ncols, nb, /*fill=*/false)) return rc;
     std::function<int(int64_t)> hook;
-    if (!panel_ready) {
+    std::vector<cudaEvent_t> pev;               // panel b's arrival + prepass done (feed mode)
+    struct PevGuard {
+        std::vector<cudaEvent_t> &v;
+        ~PevGuard() { for (auto e : v) cudaEventDestroy(e); }
+    } pevg{pev};
+    if (!feed) {
         int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
         trevc_prepass_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, nb, w.cnl, w.part, Z, ldz, sh, w.rowend,
                                                                w.G, w.e, sp.U, sp.ldu, g_flag, qof);
@@ -515,23 +539,46 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
         // T arrives panel by panel (right to left, the order the blocks consume it): every block
         // waits for its own panel and computes that panel's part of the prepass (column norms,
         // panel sum P_b, Z / G / row_end / shifts of the requested columns, 3M sum plane)
-        CK(cudaStreamWaitEvent(g_stream, panel_ready[0], 0));
-        CK(cudaMemcpyAsync(w.delta, delta_ext, 2 * sizeof(double), cudaMemcpyDeviceToDevice, g_stream));
-        hook = [&, qof](int64_t b) -> int {
+        CK(cudaMemsetAsync(w.cnl, 0, size_t(m) * 8, g_stream));        // (atomic maxima below)
+        CK(cudaMemsetAsync(w.part, 0, size_t(m) * 8, g_stream));
+        CK(cudaMemsetAsync(w.G, 0, size_t(ncols) * 8, g_stream));
+        const int64_t nblk = cdiv(m, nb);
+        pev.resize(size_t(nblk) + 1);
+        for (auto &e : pev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(pev[nblk], g_stream));                      // workspace ready
+        CK(cudaStreamWaitEvent(feed->cs, pev[nblk], 0));
+        for (int64_t b = 0; b < nblk; b++) {                           // everything on the comm stream
+            if (int rc = feed->enqueue(b)) return rc;
             const Blk bl = block_rows(0, m, nb, b);
-            CK(cudaStreamWaitEvent(g_stream, panel_ready[b], 0));
-            const int blocks = int(std::min<int64_t>(cdiv(bl.hi - bl.lo, 8), int64_t(g_num_sms) * 16));
-            trevc_prepass_kernel<T><<<blocks, 256, 0, g_stream>>>(Tm, ldt, m, nb, w.cnl, w.part, Z, ldz, sh, w.rowend,
-                                                                   w.G, w.e, sp.U, sp.ldu, g_flag, qof, bl.lo, bl.hi);
-            CK_LAUNCH("trevc_prepass_kernel");
-            panel_sum_kernel<<<1, 32, 0, g_stream>>>(0, m, nb, b + 1, w.part, w.P, b);
-            CK_LAUNCH("panel_sum_kernel");
+            const T *Tb = Tm;
+            int64_t ldtb = ldt;
+            if (feed->view) {
+                const void *pv = nullptr;
+                feed->view(b, &pv, &ldtb);
+                Tb = static_cast<const T *>(pv);
+            }
+            const int64_t rchunk = 1024;                               // one panel over the whole GPU
+            const dim3 grid(unsigned(cdiv(bl.hi - bl.lo, 8)), unsigned(cdiv(bl.hi, rchunk)));
+            trevc_prepass_panel_kernel<T><<<grid, 256, 0, feed->cs>>>(Tb, ldtb, m, nb, w.cnl, w.part, Z, ldz, sh,
+                                                                       w.rowend, w.G, w.e, sp.U, sp.ldu, g_flag, qof,
+                                                                       bl.lo, bl.hi, rchunk);
+            CK_LAUNCH("trevc_prepass_panel_kernel");
+            CK(cudaEventRecord(pev[b], feed->cs));
+        }
+        CK(cudaStreamWaitEvent(g_stream, pev[0], 0));
+        CK(cudaMemcpyAsync(w.delta, feed->delta, 2 * sizeof(double), cudaMemcpyDeviceToDevice, g_stream));
+        t_panel_part = w.part;                 // the diagonal kernel forms P_b from the panel's pcol
+        hook = [&](int64_t b) -> int {
+            CK(cudaStreamWaitEvent(g_stream, pev[b], 0));
+            if (feed->view) feed->view(b, &t_blk_U, &t_blk_ld);
             return 0;
         };
         t_pre_block = &hook;
     }
     int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
     t_pre_block = nullptr;
+    t_panel_part = nullptr;
+    t_blk_U = nullptr;
     if (qof) cudaFreeAsync(qof, g_stream);
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
     return rc;
@@ -1707,65 +1754,60 @@ int nccl_wait(cudaStream_t st, const char *what) {
 // columns [lo_b, hi_b) (rows 0 .. hi_b) -- its diagonal block and the update panel U(I0, I1), and
 // the per-panel prepass (P:503-508 shortcut: nothing below the diagonal travels).  On the comm
 // stream cs: delta of root's T (R4: ||T||_inf needs all of T, so root computes it and sends it
-// first), then one ncclBroadcast per panel, right to left, each followed by ev[b] (non-root: after
-// the panel is unpacked into the workspace copy of T).  The solve waits for ev[b] before block b,
-// so block b computes while panels b+1.. are still in flight.
+// first), then, through the returned feed, one ncclBroadcast per panel, right to left (non-root:
+// followed by the unpack into the workspace copy of T).  trevc_impl queues each panel's prepass
+// behind it and gates block b on it, so block b computes while panels b+1.. are in flight
+// (SURVEY §8e item 1).
 template <typename T>
-int stream_upper(const T *Tm, int64_t ldt, int64_t m, int nb, int root, cudaStream_t cs, T **pack_out, T **Tw_out,
-                 const T **Tuse, int64_t *lduse, double *dbuf, std::vector<cudaEvent_t> &ev) {
+int stream_upper(const T *Tm, int64_t ldt, int64_t m, int nb, int root, cudaStream_t cs, T **pack_out,
+                 double *dbuf, PanelFeed &feed) {
     const size_t es = sizeof(T), ndbl = es / 8;
     const int r = g_comm_r;
     const int64_t nblk = cdiv(m, nb);
-    size_t packed = 0;
+    std::vector<size_t> offs(size_t(nblk) + 1, 0);
     for (int64_t b = 0; b < nblk; b++) {
         const Blk bl = block_rows(0, m, nb, b);
-        packed += size_t(bl.hi) * size_t(bl.hi - bl.lo);
+        offs[b + 1] = offs[b] + size_t(bl.hi) * size_t(bl.hi - bl.lo);
     }
     T *pack = nullptr;
-    CK(cudaMallocAsync(&pack, packed * es, g_stream));
+    CK(cudaMallocAsync(&pack, offs[nblk] * es, g_stream));
     *pack_out = pack;
-    *Tuse = Tm;
-    *lduse = ldt;
-    // MSTRSM_DIST_TEST_UNPACK=1 (testing on one GPU): root also solves from its unpacked copy, so the
-    // non-root path (panels unpacked from the broadcast buffer) runs at nranks = 1
+    // MSTRSM_DIST_TEST_UNPACK=1 (testing on one GPU): root also solves from the broadcast buffer, so
+    // the non-root path runs at nranks = 1
     static const bool test_unpack = [] { const char *e = getenv("MSTRSM_DIST_TEST_UNPACK"); return e && e[0] == '1'; }();
-    const bool unpack = r != root || test_unpack;
+    const bool from_pack = r != root || test_unpack;
     if (r == root) {
         double *rs = nullptr;
         CK(ws_malloc((void **)&rs, size_t(m) * 8));
         if (int rc = compute_delta_n<T>(Tm, ldt, m, rs, dbuf)) return rc;
         ws_free(rs, g_stream);
     }
-    if (unpack) {
-        T *Tw = nullptr;
-        CK(cudaMallocAsync(&Tw, size_t(m) * m * es, g_stream));
-        *Tw_out = Tw;
-        *Tuse = Tw;
-        *lduse = m;
-    }
     cudaEvent_t e0;
     CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
-    ev.push_back(e0);                                    // ev[0] is the setup event; panels follow
     CK(cudaEventRecord(e0, g_stream));
     CK(cudaStreamWaitEvent(cs, e0, 0));
+    cudaEventDestroy(e0);
     NCK(ncclBroadcast(dbuf, dbuf, 2, ncclDouble, root, g_comm, cs));
-    size_t off = 0;
-    for (int64_t b = 0; b < nblk; b++) {
+    feed.cs = cs;
+    feed.delta = dbuf;
+    feed.enqueue = [=](int64_t b) -> int {
         const Blk bl = block_rows(0, m, nb, b);
         const int64_t rows = bl.hi, w = bl.hi - bl.lo;
         if (r == root)
-            CK(cudaMemcpy2DAsync(pack + off, rows * es, Tm + bl.lo * ldt, ldt * es, rows * es, w,
+            CK(cudaMemcpy2DAsync(pack + offs[b], rows * es, Tm + bl.lo * ldt, ldt * es, rows * es, w,
                                  cudaMemcpyDeviceToDevice, cs));
-        NCK(ncclBroadcast(pack + off, pack + off, size_t(rows) * w * ndbl, ncclDouble, root, g_comm, cs));
-        if (unpack)
-            CK(cudaMemcpy2DAsync(*Tw_out + bl.lo * m, m * es, pack + off, rows * es, rows * es, w,
-                                 cudaMemcpyDeviceToDevice, cs));
-        cudaEvent_t e;
-        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CK(cudaEventRecord(e, cs));
-        ev.push_back(e);
-        off += size_t(rows) * w;
-    }
+        NCK(ncclBroadcast(pack + offs[b], pack + offs[b], size_t(rows) * w * ndbl, ncclDouble, root, g_comm, cs));
+        return 0;
+    };
+    // every block reads only its own panel: a non-root rank solves straight from the broadcast
+    // buffer, panel b seen as a column-major matrix with leading dimension hi_b whose column lo_b
+    // is its first (no unpack, no second copy of T)
+    if (from_pack)
+        feed.view = [=](int64_t b, const void **ptr, int64_t *ld) {
+            const Blk bl = block_rows(0, m, nb, b);
+            *ptr = static_cast<const void *>(pack + offs[b] - bl.lo * bl.hi);
+            *ld = bl.hi;
+        };
     return 0;
 }
 
@@ -1806,8 +1848,13 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
         snprintf(g_errmsg, sizeof(g_errmsg), "trevc_*_dist: no communicator (mstrsm_comm_init)");
         return 3;
     }
-    const int P = g_comm_n, r = g_comm_r;
-    if (root < 0 || root >= P) return -9;
+    // MSTRSM_DIST_EMULATE_P=P (experiments, nranks = 1 only): run rank 0's step of a P-rank job on
+    // this GPU -- rank 0's shard, the P-rank all-gather layout, the other ranks' gathered bytes as a
+    // device-to-device copy of the same volume, the unpack of all m columns (tools/exp_dist_emul.py)
+    static const int emul_p = [] { const char *e = getenv("MSTRSM_DIST_EMULATE_P"); return e ? atoi(e) : 0; }();
+    const bool emul = g_comm_n == 1 && emul_p > 1;
+    const int P = emul ? emul_p : g_comm_n, r = emul ? 0 : g_comm_r;
+    if (root < 0 || root >= g_comm_n) return -9;
     if (r == root && ldt < std::max<int64_t>(1, m)) return -2;
     if (m == 0) return 0;
     if (r == root && !Tm) return -1;
@@ -1818,21 +1865,18 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     DevRes *res = dev_res();                        // this thread's comm stream on this device
     if (!res) return 1;
     const cudaStream_t cs = res->comm;
-    T *pack = nullptr, *Tw = nullptr;
-    const T *Tuse = Tm;
-    int64_t lduse = ldt;
+    T *pack = nullptr;
     double *dbuf = nullptr;
     CK(cudaMallocAsync(&dbuf, 2 * sizeof(double), g_stream));
-    std::vector<cudaEvent_t> ev;                    // [setup, panel 0, panel 1, ...]
-    struct EvGuard {
-        std::vector<cudaEvent_t> &v;
-        ~EvGuard() { for (auto e : v) cudaEventDestroy(e); }
-    } evg{ev};
     // 1. T streamed from root panel by panel (comm stream), overlapping the solve below
-    if (int rc = stream_upper<T>(Tm, ldt, m, nb, root, cs, &pack, &Tw, &Tuse, &lduse, dbuf, ev)) {
+    PanelFeed feed;
+    if (int rc = stream_upper<T>(Tm, ldt, m, nb, root, cs, &pack, dbuf, feed)) {
         nccl_wait(cs, "trevc_*_dist (broadcast)");
         return rc;
     }
+    // (non-root: T is never read outside the panels; the solve's U argument is only a placeholder)
+    const T *Tuse = Tm ? Tm : pack;
+    const int64_t lduse = Tm ? ldt : m;
     // 2. this rank's shard, written into the all-gather send buffer (m x mc, padded)
     int64_t mc = 0;
     for (int q = 0; q < P; q++) mc = std::max(mc, shard_of(m, P, q, kShardGroup, nullptr));
@@ -1874,13 +1918,23 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     CK(cudaMallocAsync(&meta, size_t(m) * 3 * 8, g_stream));
     T *Sb = nullptr;
     CK(cudaMallocAsync(&Sb, size_t(std::max<int64_t>(L, 1)) * es, g_stream));
-    int rc = ncols > 0 ? trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb, dbuf, ev.data() + 1)
-                       : 0;
+    int rc = 0;
+    if (ncols > 0) {
+        rc = trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb, &feed);
+    } else {                                        // no columns here: the broadcasts still run
+        for (int64_t b = 0; b < cdiv(m, nb) && !rc; b++) rc = feed.enqueue(b);
+    }
     if (rc < 0) rc = 1;
     // every rank agrees on the status before the all-gather (a rank that failed locally must not
     // leave its peers blocked in the collective): max over ranks of the local return codes
     {
-        CK(cudaStreamWaitEvent(g_stream, ev.back(), 0));   // broadcasts done before the next collective
+        {                                           // broadcasts done before the next collective
+            cudaEvent_t eb;
+            CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
+            CK(cudaEventRecord(eb, cs));
+            CK(cudaStreamWaitEvent(g_stream, eb, 0));
+            cudaEventDestroy(eb);
+        }
         int *st = nullptr;
         CK(cudaMallocAsync(&st, sizeof(int), g_stream));
         const int rc_local = rc;
@@ -1925,6 +1979,8 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
         NCK(ncclAllGather(ss, sa, size_t(mc), ncclDouble, g_comm, g_stream));
         NCK(ncclAllGather(es_, ea, size_t(mc), ncclInt32, g_comm, g_stream));
         NCK(ncclGroupEnd());
+        if (emul)   // stand-in for the other ranks' shards arriving (same byte volume, device-to-device)
+            CK(cudaMemcpyAsync(Za + L, pack, size_t(L) * (P - 1) * es, cudaMemcpyDeviceToDevice, g_stream));
         // 4. natural order: vectors by the triangular layout, scales / exponents by perm
         const int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
         unpack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(Za, m, meta, meta + m, meta + 2 * m, m, Z, ldz);
@@ -1938,7 +1994,7 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     cudaFreeAsync(meta, g_stream);
     cudaFreeAsync(Sb, g_stream);
     cudaFreeAsync(dbuf, g_stream);
-    for (void *p : {(void *)pack, (void *)Tw, (void *)Zs, (void *)ss, (void *)es_, (void *)Za, (void *)sa,
+    for (void *p : {(void *)pack, (void *)Zs, (void *)ss, (void *)es_, (void *)Za, (void *)sa,
                     (void *)ea, (void *)perm_d})
         if (p) cudaFreeAsync(p, g_stream);
     return rc;
