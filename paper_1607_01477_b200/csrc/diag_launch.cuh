@@ -205,7 +205,11 @@ int launch_diagl(const DiagArgs<T> &a0) {
     if (kmax == 0) return set_cuda_error(cudaErrorInvalidValue, "diagl_kernel: shared memory");
     (void)0;
     const int64_t npass = cdiv(groups, sms * kmax);
-    const int nsub = int(std::max<int64_t>(1, std::min<int64_t>(kmax, cdiv(groups, sms * npass))));
+    // at least 4 substitution warps per CTA: with fewer columns than SMs x 4 warps the launch is
+    // latency-bound anyway, and the triangle's staging is shared by more warps (a 1-warp CTA spent
+    // a quarter of its instructions staging, ncu c2)
+    const int nsub = int(std::max<int64_t>(std::min<int64_t>(4, kmax),
+                                           std::min<int64_t>(kmax, cdiv(groups, sms * npass))));
     const int threads = (nsub + diagw_nrep(nsub, 4, SAFE)) * 32;
     const size_t smem = size_t(diagl_smem_bytes(npad, int(sizeof(T)), nsub * 8, SAFE, GSCR));
     int grid = int(std::min<int64_t>(cdiv(groups, nsub), sms));
