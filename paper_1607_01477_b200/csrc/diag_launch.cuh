@@ -134,7 +134,9 @@ int launch_diagf_k(const DiagArgs<T> &a0) {
     const int64_t sms = g_cta_cap > 0 ? g_cta_cap : g_num_sms;
     // one CTA per SM; equal passes: as many substitution warps per CTA as the pass count needs
     const int64_t npass = cdiv(groups, sms * W::kSub);
-    const int nsub = int(std::max<int64_t>(1, std::min<int64_t>(W::kSub, cdiv(groups, sms * npass))));
+    // (at least 4 substitution warps per CTA, as diagl: the staging is shared by more warps)
+    const int nsub = int(std::max<int64_t>(std::min<int64_t>(4, W::kSub),
+                                           std::min<int64_t>(W::kSub, cdiv(groups, sms * npass))));
     const int threads = (nsub + diagw_nrep(nsub, LPC, SAFE)) * 32;
     const size_t smem = size_t(diagw_smem(nfull, LPC, RPL, sizeof(T), nsub * G, SAFE).total);
     int grid = int(std::min<int64_t>(cdiv(groups, nsub), sms));
