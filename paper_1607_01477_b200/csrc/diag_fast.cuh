@@ -357,40 +357,34 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
         bool guarded = false;
         double g0 = 0.0, gub = 0.0;
         if (SAFE) {
-            // ---- precheck, eqs. (4)-(5), as diag_kernel: upper bounds of |y| and
-            //      the suffix products, lower bounds of |d| (a column the exact test would pass
-            //      may take the guarded loop, never the reverse) ----
+            // ---- precheck, eqs. (4)-(5), with upper bounds (R36): ||y(I1)||_inf <=
+            //      G_j, every suffix product <= the whole block's product of (1 + cnl/|d|), every
+            //      1/|d| <= their max.  It only picks the unguarded loop when no rescale can
+            //      trigger; the guarded one returns the same values whenever none does ----
+            double prod = 1.0, minv = 0.0;
+#pragma unroll
+            for (int t = 0; t < RPL; t++) {
+                const int sc = rl + LPC * t;
+                if (sc < nrow) {
+                    const double inv = __drcp_ru(maxabs(pivot(sc)));       // >= 1/|d_l|
+                    prod = __dmul_ru(prod, __dadd_ru(1.0, __dmul_ru(cn[sc], inv)));
+                    minv = fmax(minv, inv);
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < LPC; o <<= 1) {
+                prod = __dmul_ru(prod, __shfl_xor_sync(0xffffffffu, prod, o, LPC));
+                minv = fmax(minv, __shfl_xor_sync(0xffffffffu, minv, o, LPC));
+            }
+            const double gtop = active ? __dmul_ru(a.G[j], 1.0 + 0x1p-40) : 0.0;   // >= ||y(I1)||_inf
+            const double carry = __dmul_ru(gtop, prod);
+            const bool okM = __dmul_ru(carry, minv) < kOmega;
+            // initial frame bound for the guarded loop: the registers' largest |y| (upper bound)
 #pragma unroll
             for (int t = 0; t < RPL; t++)
                 if (rl + LPC * t < nrow) gub = fmax(gub, maxabs(y[t]));
             gub = group_max<LPC>(gub);
             if constexpr (ST::cplx_) gub = __dmul_ru(gub, 1.4142135623730951);
-            double carry = gub;
-            bool okM = true;
-#pragma unroll 1
-            for (int t = RPL - 1; t >= 0; t--) {
-                if (t * LPC >= nmax) continue;
-                const int sc = t * LPC + rl;
-                const bool in = sc < nrow;
-                const double ad = maxabs(pivot(sc));
-                const double tf = in ? __dadd_ru(1.0, __dmul_ru(cn[sc < nfull ? sc : 0], __drcp_ru(ad))) : 1.0;   // >= 1 + cnl/|d|
-                double suf = tf;
-#pragma unroll
-                for (int o = 1; o < LPC; o <<= 1) {
-                    const double v = __shfl_down_sync(0xffffffffu, suf, o, LPC);
-                    if (rl + o < LPC) suf = __dmul_ru(suf, v);
-                }
-                double exc = __shfl_down_sync(0xffffffffu, suf, 1, LPC);
-                if (rl == LPC - 1) exc = 1.0;
-                const double gl = __dmul_ru(carry, exc);
-                okM = okM && (!in || gl < __dmul_rn(kOmega, ad));
-                carry = __dmul_ru(carry, __shfl_sync(0xffffffffu, suf, 0, LPC));
-            }
-#pragma unroll
-            for (int o = 1; o < LPC; o <<= 1) {
-                const bool other = __shfl_xor_sync(0xffffffffu, okM, o, LPC);
-                okM = okM && other;
-            }
             guarded = active && !(okM && carry < kOmega);
             if (__any_sync(0xffffffffu, guarded)) {                        // g := ||y(I1)||_inf
 #pragma unroll

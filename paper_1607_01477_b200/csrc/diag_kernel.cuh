@@ -215,6 +215,15 @@ template <> struct Piv<cplx> {
             r = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
             return;
         }
+        // Fast path: components 0 or in [2^-250, 2^250] keep every intermediate below normal --
+        // scaling by a power of two commutes with each rounded step, so this is bit for bit the
+        // prescaled computation below
+        const double ax = fabs(dd.x), ay = fabs(dd.y);
+        if ((ax == 0.0 || (ax >= 0x1p-250 && ax <= 0x1p+250)) && (ay == 0.0 || (ay >= 0x1p-250 && ay <= 0x1p+250))) {
+            const double inv = __drcp_rn(fma(dd.x, dd.x, __dmul_rn(dd.y, dd.y)));
+            r = make_double2(__dmul_rn(dd.x, inv), -__dmul_rn(dd.y, inv));
+            return;
+        }
         int e;
         long long mnt;
         exp_mant(big, e, mnt);
