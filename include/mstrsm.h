@@ -292,11 +292,11 @@ int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dc
  *                          and broadcasts it, then T's upper triangle in 128-column panels right
  *                          to left (the order the blocks consume it) on a separate
  *                          stream; each rank's block b waits only for panel b, so the solve of its
- *                          shard overlaps the rest of the broadcast.  The ranks then agree on a
- *                          status (one all-reduce), the triangular shards (+ scales, exponents) are
- *                          all-gathered and every rank receives the full Z (m x m, ldz), scales and
- *                          scale_exp (nullable, m entries) in natural order -- bit-identical to
- *                          trevc_*.  Collective and blocking: every rank must call it; the call
+ *                          shard overlaps the rest of the broadcast.  Each block's finished rows
+ *                          are all-gathered behind the compute front; the ranks then agree on a
+ *                          status (one all-reduce), gather the exponents, and every rank receives
+ *                          the full Z (m x m, ldz), scales and scale_exp (nullable, m entries) in
+ *                          natural order -- bit-identical to trevc_*.  Collective and blocking: every rank must call it; the call
  *                          returns when its work is done.  NCCL's asynchronous errors are polled
  *                          while waiting; an error or a wait longer than MSTRSM_NCCL_TIMEOUT_S
  *                          (default 600 s) aborts the communicator and returns 3.  Errors: -i for

@@ -162,6 +162,9 @@ thread_local const std::function<int(int64_t)> *t_pre_block = nullptr;
 // 0 .. hi_b): U(i, k) of block b is t_blk_U[i + k * t_blk_ld] (nullptr: the solve's U, ldu).
 thread_local const void *t_blk_U = nullptr;
 thread_local int64_t t_blk_ld = 0;
+// ... and may be told when block b's diagonal step has been launched (its rows are then final up to
+// the lazy exponent fix-up: the multi-GPU path gathers them behind the compute front)
+thread_local const std::function<int(int64_t)> *t_after_diag = nullptr;
 // With the per-block hook: the panel sums P_b are formed by the diagonal kernel from these
 // per-column panel maxima (the same ascending sum panel_sum_kernel does) instead of a launch.
 thread_local const double *t_panel_part = nullptr;
@@ -218,7 +221,12 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
             c0 = std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();   // first r > lo
         }
         int64_t ncols = n - c0;
-        if (ncols <= 0) continue;
+        if (ncols <= 0) {                      // (the after-diag hook's collectives run on every rank)
+            if (t_after_diag) {
+                if (int rc = (*t_after_diag)(b)) return rc;
+            }
+            continue;
+        }
         DiagArgs<T> a{};
         a.U = Ub; a.ldu = ldub; a.m = m; a.shifts = shifts; a.sstride = sstride;
         a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
@@ -237,6 +245,9 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
         int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
         early = t_pre_block ? 0 : 1;           // (a per-block prepass writes cnl right before the diag)
         if (rc) return rc;
+        if (t_after_diag) {
+            if ((rc = (*t_after_diag)(b))) return rc;
+        }
         if (g_debug_sync) {
             cudaError_t e = cudaStreamSynchronize(g_stream);
             fprintf(stderr, "[mstrsm debug] block %lld diag done (%s)\n", (long long)b, cudaGetErrorString(e));
@@ -294,7 +305,11 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         const int64_t ldub = t_blk_U ? t_blk_ld : ldu;
         const Blk bl = block_rows(0, m, nb, b);
         const int64_t c0 = c0_of(bl), ncols = n - c0;
-        if (ncols <= 0) { diag_cap = 0; continue; }
+        if (ncols <= 0) {
+            diag_cap = 0;
+            if (t_after_diag && (rc = (*t_after_diag)(b))) break;
+            continue;
+        }
         const int par = int(b & 1);
         int *dblk = par ? w.dblk2 : w.dblk;
         double *xs = Xsum ? (par ? Xsum2 : Xsum) : nullptr;
@@ -318,6 +333,7 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         g_cta_cap = 0;
         early = t_pre_block ? 0 : 1;
         if (rc) break;
+        if (t_after_diag && (rc = (*t_after_diag)(b))) break;
         diag_cap = 0;
         const int64_t M = bl.lo;
         if (M <= 0) continue;
@@ -489,6 +505,9 @@ struct PanelFeed {
     std::function<int(int64_t)> enqueue;
     const double *delta;
     std::function<void(int64_t, const void **, int64_t *)> view;   // nullable: block b's copy of panel b
+    std::function<int(int64_t)> after_diag;   // nullable: block b's diagonal step launched (library stream)
+    int *etab_out = nullptr;    // non-null: no lazy fix-up here; E (nblk x ncols) copied to etab_out,
+    int64_t ld_etab = 0;        //   row b at etab_out + b * ld_etab, for the receiver's fix-up
 };
 
 template <typename T>
@@ -575,13 +594,25 @@ int trevc_impl(const T *Tm, int64_t ldt, int64_t m, const int64_t *cols_host, in
             if (feed->view) feed->view(b, &t_blk_U, &t_blk_ld);
             return 0;
         };
+        if (feed->after_diag) t_after_diag = &feed->after_diag;
         t_pre_block = &hook;
     }
     int rc = blocked_solve<T, true>(0, Tm, ldt, m, sh, 1, Z, ldz, ncols, w.rowend, &cols, nb, w, sp.U, sp.X, sp.ldu, sp.ldx);
     t_pre_block = nullptr;
     t_panel_part = nullptr;
     t_blk_U = nullptr;
+    t_after_diag = nullptr;
     if (qof) cudaFreeAsync(qof, g_stream);
+    if (!rc && feed && feed->etab_out) {       // the receiver applies the fix-up (a.6) itself
+        const int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
+        CK(launch_k_lvl(2, finalize_kernel<T>, dim3(std::max(blocks, 1)), dim3(256), 0, g_stream, 0, Z, ldz, m,
+                        ncols, nb, cdiv(m, nb), (const int64_t *)w.rowend, (const int *)w.e, (const int *)nullptr,
+                        scales, scale_exp, (const int64_t *)nullptr));
+        CK_LAUNCH("finalize_kernel");
+        CK(cudaMemcpy2DAsync(feed->etab_out, size_t(feed->ld_etab) * 4, w.Etab, size_t(ncols) * 4, size_t(ncols) * 4,
+                             size_t(cdiv(m, nb)), cudaMemcpyDeviceToDevice, g_stream));
+        return 0;
+    }
     if (!rc) rc = finalize<T>(0, 1, Z, ldz, m, ncols, nb, w.rowend, scales, scale_exp, w.rowend, w);
     return rc;
 }
@@ -1840,6 +1871,47 @@ int ex_dist_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *
     return rc;
 }
 
+// Receiver side of the row-block gather (a.6 applied here, as finalize_kernel does on one GPU):
+// Z(l, k) = ldexp(slab value, e_k - E_b(k)) for l < k (block b of row l), Z(k, k) = c_k = 2^e_k,
+// Z(l, k) = 0 for l > k; scales / exponents in natural order.  One warp per eigenvector k.
+template <typename T>
+__global__ void unpack_slabs_kernel(T *__restrict__ Z, int64_t ldz, int64_t m, int nb, int64_t nblk, int P,
+                                    const T *__restrict__ recv, const int64_t *__restrict__ slab_off,
+                                    const int64_t *__restrict__ slab_cols, const int64_t *__restrict__ c0,
+                                    const int *__restrict__ owner, const int *__restrict__ qidx, int64_t mc,
+                                    const int *__restrict__ Eall, const int *__restrict__ eall,
+                                    double *__restrict__ scales, int *__restrict__ scale_exp) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t k = w; k < m; k += nw) {
+        const int r = owner[k];
+        const int64_t q = qidx[k];
+        const int ek = eall[int64_t(r) * mc + q];
+        T *z = Z + k * ldz;
+        for (int64_t l = lane; l < m; l += 32) {
+            T v = S<T>::zero();
+            if (l < k) {
+                const int64_t b = (m - 1 - l) / nb;
+                const Blk bl = block_rows(0, m, nb, b);
+                const int64_t nbr = bl.hi - bl.lo;
+                const int64_t col = q - c0[b * P + r];
+                v = recv[slab_off[b] + (int64_t(r) * slab_cols[b] + col) * nbr + (l - bl.lo)];
+                const int d = ek - Eall[(int64_t(r) * nblk + b) * mc + q];
+                if (d != 0) v = S<T>::ldx(v, d);
+            } else if (l == k) {
+                v = S<T>::real(ldexp(1.0, ek));
+            }
+            z[l] = v;
+        }
+        if (lane == 0) {
+            if (scales) scales[k] = ldexp(1.0, ek);
+            if (scale_exp) scale_exp[k] = ek;
+        }
+    }
+}
+
 template <typename T>
 int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, double *scales, int32_t *scale_exp,
                     int nb, int root) {
@@ -1850,9 +1922,9 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
         snprintf(g_errmsg, sizeof(g_errmsg), "trevc_*_dist: no communicator (mstrsm_comm_init)");
         return 3;
     }
-    // MSTRSM_DIST_EMULATE_P=P (experiments, nranks = 1 only): run rank 0's step of a P-rank job on
-    // this GPU -- rank 0's shard, the P-rank all-gather layout, the other ranks' gathered bytes as a
-    // device-to-device copy of the same volume, the unpack of all m columns (tools/exp_dist_emul.py)
+    // MSTRSM_DIST_EMULATE_P=P (experiments, nranks = 1 only): rank 0's step of a P-rank job on this
+    // GPU -- rank 0's shard, the P-rank gather layout with the other ranks' slabs as device-to-device
+    // copies of the same volume, the unpack of all m columns (tools/exp_dist_emul.py)
     static const int emul_p = [] { const char *e = getenv("MSTRSM_DIST_EMULATE_P"); return e ? atoi(e) : 0; }();
     const bool emul = g_comm_n == 1 && emul_p > 1;
     const int P = emul ? emul_p : g_comm_n, r = emul ? 0 : g_comm_r;
@@ -1866,139 +1938,170 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     if (nb == 0) nb = 64;
     DevRes *res = dev_res();                        // this thread's comm stream on this device
     if (!res) return 1;
-    const cudaStream_t cs = res->comm;
-    T *pack = nullptr;
-    double *dbuf = nullptr;
+    const cudaStream_t cs = res->comm;              // every collective of the call runs on cs, in call order
+    const int64_t nblk = cdiv(m, nb);
+
+    // shard maps of every rank; per block b: the first active local column c0[b][q] (eigenvectors
+    // k > lo_b are active), the slab width (most active columns over the ranks) and offsets
+    std::vector<std::vector<int64_t>> rc_cols(P);
+    int64_t mc = 1;
+    for (int q = 0; q < P; q++) {
+        rc_cols[q].resize(size_t(std::max<int64_t>(shard_of(m, P, q, kShardGroup, nullptr), 1)));
+        rc_cols[q].resize(size_t(shard_of(m, P, q, kShardGroup, rc_cols[q].data())));
+        mc = std::max<int64_t>(mc, int64_t(rc_cols[q].size()));
+    }
+    const std::vector<int64_t> &cols = rc_cols[r];
+    const int64_t ncols = int64_t(cols.size());
+    std::vector<int64_t> c0(size_t(nblk) * P), slab_cols(nblk), slab_off(nblk + 1, 0), send_off(nblk + 1, 0);
+    for (int64_t b = 0; b < nblk; b++) {
+        const Blk bl = block_rows(0, m, nb, b);
+        int64_t wmax = 0;
+        for (int q = 0; q < P; q++) {
+            const auto &cq = rc_cols[q];
+            const int64_t f = std::upper_bound(cq.begin(), cq.end(), bl.lo) - cq.begin();
+            c0[b * P + q] = f;
+            wmax = std::max<int64_t>(wmax, int64_t(cq.size()) - f);
+        }
+        slab_cols[b] = wmax;
+        const int64_t S = wmax * (bl.hi - bl.lo);
+        send_off[b + 1] = send_off[b] + S;
+        slab_off[b + 1] = slab_off[b] + S * P;
+    }
+    std::vector<int> owner(m), qidx(m);
+    for (int q = 0; q < P; q++)
+        for (size_t i = 0; i < rc_cols[q].size(); i++) {
+            owner[rc_cols[q][i]] = q;
+            qidx[rc_cols[q][i]] = int(i);
+        }
+
+    T *pack = nullptr, *Zs = nullptr, *sendb = nullptr, *recvb = nullptr;
+    double *dbuf = nullptr, *ss = nullptr;
+    int *es_ = nullptr, *ea = nullptr, *Eloc = nullptr, *Eall = nullptr, *owner_d = nullptr, *qidx_d = nullptr;
+    int64_t *meta = nullptr;                        // [slab_off | slab_cols | c0]
     CK(cudaMallocAsync(&dbuf, 2 * sizeof(double), g_stream));
+    CK(cudaMallocAsync(&Zs, size_t(m) * std::max<int64_t>(ncols, 1) * es, g_stream));
+    CK(cudaMallocAsync(&ss, size_t(mc) * 8, g_stream));
+    CK(cudaMallocAsync(&es_, size_t(mc) * 4, g_stream));
+    CK(cudaMallocAsync(&ea, size_t(mc) * P * 4, g_stream));
+    CK(cudaMallocAsync(&Eloc, size_t(nblk) * mc * 4, g_stream));
+    CK(cudaMallocAsync(&Eall, size_t(nblk) * mc * P * 4, g_stream));
+    CK(cudaMallocAsync(&sendb, size_t(std::max<int64_t>(send_off[nblk], 1)) * es, g_stream));
+    CK(cudaMallocAsync(&recvb, size_t(std::max<int64_t>(slab_off[nblk], 1)) * es, g_stream));
+    CK(cudaMallocAsync(&owner_d, size_t(m) * 4, g_stream));
+    CK(cudaMallocAsync(&qidx_d, size_t(m) * 4, g_stream));
+    CK(cudaMallocAsync(&meta, size_t(2 * nblk + nblk * P) * 8, g_stream));
+    CK(cudaMemsetAsync(es_, 0, size_t(mc) * 4, g_stream));
+    CK(cudaMemsetAsync(Eloc, 0, size_t(nblk) * mc * 4, g_stream));
+    {
+        std::vector<int64_t> mh(size_t(2 * nblk + nblk * P));
+        std::copy(slab_off.begin(), slab_off.begin() + nblk, mh.begin());
+        std::copy(slab_cols.begin(), slab_cols.end(), mh.begin() + nblk);
+        std::copy(c0.begin(), c0.end(), mh.begin() + 2 * nblk);
+        CK(cudaMemcpyAsync(meta, mh.data(), mh.size() * 8, cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemcpyAsync(owner_d, owner.data(), size_t(m) * 4, cudaMemcpyHostToDevice, g_stream));
+        CK(cudaMemcpyAsync(qidx_d, qidx.data(), size_t(m) * 4, cudaMemcpyHostToDevice, g_stream));
+        CK(cudaStreamSynchronize(g_stream));        // host arrays go out of scope
+    }
+    std::vector<cudaEvent_t> evs;
+    struct EvGuard {
+        std::vector<cudaEvent_t> &v;
+        ~EvGuard() { for (auto e : v) cudaEventDestroy(e); }
+    } evg{evs};
+    auto new_event = [&](cudaEvent_t *e) -> int {
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        evs.push_back(*e);
+        return 0;
+    };
+    auto free_all = [&]() {
+        for (void *p : {(void *)pack, (void *)Zs, (void *)sendb, (void *)recvb, (void *)dbuf, (void *)ss, (void *)es_,
+                        (void *)ea, (void *)Eloc, (void *)Eall, (void *)owner_d, (void *)qidx_d, (void *)meta})
+            if (p) cudaFreeAsync(p, g_stream);
+    };
+
     // 1. T streamed from root panel by panel (comm stream), overlapping the solve below
     PanelFeed feed;
     if (int rc = stream_upper<T>(Tm, ldt, m, nb, root, cs, &pack, dbuf, feed)) {
         nccl_wait(cs, "trevc_*_dist (broadcast)");
+        free_all();
         return rc;
     }
     // (non-root: T is never read outside the panels; the solve's U argument is only a placeholder)
     const T *Tuse = Tm ? Tm : pack;
     const int64_t lduse = Tm ? ldt : m;
-    // 2. this rank's shard, written into the all-gather send buffer (m x mc, padded)
-    int64_t mc = 0;
-    for (int q = 0; q < P; q++) mc = std::max(mc, shard_of(m, P, q, kShardGroup, nullptr));
-    std::vector<int64_t> cols(std::max<int64_t>(mc, 1));
-    const int64_t ncols = shard_of(m, P, r, kShardGroup, cols.data());
-    T *Zs = nullptr, *Za = nullptr;
-    double *ss = nullptr, *sa = nullptr;
-    int *es_ = nullptr, *ea = nullptr;
-    int64_t *perm_d = nullptr;
-    // triangular all-gather layout: rows 0 .. k of eigenvector k (zero below), packed per rank
-    std::vector<std::vector<int64_t>> rc_cols(P);
-    int64_t L = 0;
-    for (int q = 0; q < P; q++) {
-        rc_cols[q].resize(size_t(std::max<int64_t>(shard_of(m, P, q, kShardGroup, nullptr), 1)));
-        const int64_t nq = shard_of(m, P, q, kShardGroup, rc_cols[q].data());
-        rc_cols[q].resize(size_t(nq));
-        int64_t tot = 0;
-        for (int64_t i = 0; i < nq; i++) tot += rc_cols[q][i] + 1;
-        L = std::max(L, tot);
-    }
-    std::vector<int64_t> hh, oo, dd;                // all ranks: heights, offsets (in Za), columns
-    for (int q = 0; q < P; q++) {
-        int64_t off = int64_t(q) * L;
-        for (int64_t k : rc_cols[q]) {
-            hh.push_back(k + 1);
-            oo.push_back(off);
-            dd.push_back(k);
-            off += k + 1;
+    // 2. row blocks gathered behind the compute front: once block b's diagonal
+    //    step is done, rows I1_b of this rank's active columns are final up to the lazy exponent
+    //    fix-up; the slab is packed and all-gathered on cs while the solve goes on
+    feed.after_diag = [&](int64_t b) -> int {
+        const Blk bl = block_rows(0, m, nb, b);
+        const int64_t nbr = bl.hi - bl.lo, act = ncols - c0[b * P + r];
+        cudaEvent_t e;
+        if (int rc = new_event(&e)) return rc;
+        CK(cudaEventRecord(e, g_stream));
+        CK(cudaStreamWaitEvent(cs, e, 0));
+        if (act > 0)
+            CK(cudaMemcpy2DAsync(sendb + send_off[b], size_t(nbr) * es, Zs + bl.lo + c0[b * P + r] * m, size_t(m) * es,
+                                 size_t(nbr) * es, size_t(act), cudaMemcpyDeviceToDevice, cs));
+        const int64_t S = send_off[b + 1] - send_off[b];
+        if (S > 0) {
+            NCK(ncclAllGather(sendb + send_off[b], recvb + slab_off[b], size_t(S) * ndbl, ncclDouble, g_comm, cs));
+            if (emul)   // stand-in for the other ranks' slabs (same byte volume)
+                CK(cudaMemcpyAsync(recvb + slab_off[b] + S, pack, size_t(S) * (P - 1) * es,
+                                   cudaMemcpyDeviceToDevice, cs));
         }
-    }
-    int64_t *meta = nullptr;                        // [heights | offsets | cols] for all m eigenvectors
-    CK(cudaMallocAsync(&Zs, size_t(m) * mc * es, g_stream));
-    CK(cudaMallocAsync(&ss, size_t(mc) * 8, g_stream));
-    CK(cudaMallocAsync(&es_, size_t(mc) * 4, g_stream));
-    CK(cudaMallocAsync(&Za, size_t(L) * P * es, g_stream));
-    CK(cudaMallocAsync(&sa, size_t(mc) * P * 8, g_stream));
-    CK(cudaMallocAsync(&ea, size_t(mc) * P * 4, g_stream));
-    CK(cudaMallocAsync(&perm_d, size_t(m) * 8, g_stream));
-    CK(cudaMallocAsync(&meta, size_t(m) * 3 * 8, g_stream));
-    T *Sb = nullptr;
-    CK(cudaMallocAsync(&Sb, size_t(std::max<int64_t>(L, 1)) * es, g_stream));
+        return 0;
+    };
+    feed.etab_out = Eloc;
+    feed.ld_etab = mc;
     int rc = 0;
     if (ncols > 0) {
         rc = trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb, &feed);
-    } else {                                        // no columns here: the broadcasts still run
-        for (int64_t b = 0; b < cdiv(m, nb) && !rc; b++) rc = feed.enqueue(b);
+    } else {                                        // no columns here: the collectives still run
+        for (int64_t b = 0; b < nblk && !rc; b++) {
+            rc = feed.enqueue(b);
+            if (!rc) rc = feed.after_diag(b);
+        }
     }
     if (rc < 0) rc = 1;
-    // every rank agrees on the status before the all-gather (a rank that failed locally must not
-    // leave its peers blocked in the collective): max over ranks of the local return codes
+    // 3. status agreement (a rank that failed must not leave its peers in the final gathers), then
+    //    the exponents (final e_j, the E table) -- all on cs, after the solve
     {
-        {                                           // broadcasts done before the next collective
-            cudaEvent_t eb;
-            CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
-            CK(cudaEventRecord(eb, cs));
-            CK(cudaStreamWaitEvent(g_stream, eb, 0));
-            cudaEventDestroy(eb);
-        }
+        cudaEvent_t e;
+        if (int erc = new_event(&e)) return erc;
+        CK(cudaEventRecord(e, g_stream));
+        CK(cudaStreamWaitEvent(cs, e, 0));
         int *st = nullptr;
-        CK(cudaMallocAsync(&st, sizeof(int), g_stream));
+        CK(cudaMallocAsync(&st, sizeof(int), cs));
         const int rc_local = rc;
-        CK(cudaMemcpyAsync(st, &rc_local, sizeof(int), cudaMemcpyHostToDevice, g_stream));
-        NCK(ncclAllReduce(st, st, 1, ncclInt32, ncclMax, g_comm, g_stream));
+        CK(cudaMemcpyAsync(st, &rc_local, sizeof(int), cudaMemcpyHostToDevice, cs));
+        NCK(ncclAllReduce(st, st, 1, ncclInt32, ncclMax, g_comm, cs));
         int rc_all = 0;
-        CK(cudaMemcpyAsync(&rc_all, st, sizeof(int), cudaMemcpyDeviceToHost, g_stream));
-        cudaFreeAsync(st, g_stream);
-        if (int wrc = nccl_wait(g_stream, "trevc_*_dist (solve)")) return wrc;
+        CK(cudaMemcpyAsync(&rc_all, st, sizeof(int), cudaMemcpyDeviceToHost, cs));
+        cudaFreeAsync(st, cs);
+        if (int wrc = nccl_wait(cs, "trevc_*_dist (solve)")) return wrc;
         if (rc_all && !rc) {
             snprintf(g_errmsg, sizeof(g_errmsg), "trevc_*_dist: another rank failed");
             rc = 3;
         }
     }
     if (!rc) {
-        std::vector<int64_t> perm(m);
-        for (int q = 0; q < P; q++)
-            for (size_t i = 0; i < rc_cols[q].size(); i++) perm[rc_cols[q][i]] = int64_t(q) * mc + int64_t(i);
-        std::vector<int64_t> metah(size_t(m) * 3);
-        std::copy(hh.begin(), hh.end(), metah.begin());
-        std::copy(oo.begin(), oo.end(), metah.begin() + m);
-        std::copy(dd.begin(), dd.end(), metah.begin() + 2 * m);
-        CK(cudaMemcpyAsync(perm_d, perm.data(), size_t(m) * 8, cudaMemcpyHostToDevice, g_stream));
-        CK(cudaMemcpyAsync(meta, metah.data(), size_t(m) * 3 * 8, cudaMemcpyHostToDevice, g_stream));
-        // this rank's columns are entries [first_r, first_r + ncols) of the all-rank arrays
-        int64_t first_r = 0;
-        for (int q = 0; q < r; q++) first_r += int64_t(rc_cols[q].size());
-        std::vector<int64_t> off_local(size_t(std::max<int64_t>(ncols, 1)));
-        for (int64_t i = 0; i < ncols; i++) off_local[i] = oo[first_r + i] - int64_t(r) * L;
-        int64_t *offl = nullptr;
-        CK(cudaMallocAsync(&offl, size_t(std::max<int64_t>(ncols, 1)) * 8, g_stream));
-        CK(cudaMemcpyAsync(offl, off_local.data(), size_t(std::max<int64_t>(ncols, 1)) * 8, cudaMemcpyHostToDevice,
-                           g_stream));
-        if (ncols > 0) {
-            const int blocks = int(std::min<int64_t>(cdiv(ncols, 8), int64_t(g_num_sms) * 16));
-            pack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(Zs, m, ncols, nullptr, meta + first_r, offl, Sb);
-            CK_LAUNCH("pack_cols_kernel");
-        }
-        // 3. gather every shard (packed vectors, scales, exponents)
         NCK(ncclGroupStart());
-        NCK(ncclAllGather(Sb, Za, size_t(L) * ndbl, ncclDouble, g_comm, g_stream));
-        NCK(ncclAllGather(ss, sa, size_t(mc), ncclDouble, g_comm, g_stream));
-        NCK(ncclAllGather(es_, ea, size_t(mc), ncclInt32, g_comm, g_stream));
+        NCK(ncclAllGather(es_, ea, size_t(mc), ncclInt32, g_comm, cs));
+        NCK(ncclAllGather(Eloc, Eall, size_t(nblk) * mc, ncclInt32, g_comm, cs));
         NCK(ncclGroupEnd());
-        if (emul)   // stand-in for the other ranks' shards arriving (same byte volume, device-to-device)
-            CK(cudaMemcpyAsync(Za + L, pack, size_t(L) * (P - 1) * es, cudaMemcpyDeviceToDevice, g_stream));
-        // 4. natural order: vectors by the triangular layout, scales / exponents by perm
+        cudaEvent_t e;
+        if (int erc = new_event(&e)) return erc;
+        CK(cudaEventRecord(e, cs));
+        CK(cudaStreamWaitEvent(g_stream, e, 0));
+        // 4. natural order, lazy fix-up applied, zeros below the diagonal, c_k on it
         const int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
-        unpack_cols_kernel<T><<<blocks, 256, 0, g_stream>>>(Za, m, meta, meta + m, meta + 2 * m, m, Z, ldz);
-        CK_LAUNCH("unpack_cols_kernel");
-        gather_dist_kernel<T><<<blocks, 256, 0, g_stream>>>(nullptr, m, perm_d, m, Z, ldz, sa, ea, scales,
-                                                            reinterpret_cast<int *>(scale_exp));
-        CK_LAUNCH("gather_dist_kernel");
-        cudaFreeAsync(offl, g_stream);
-        if (int wrc = nccl_wait(g_stream, "trevc_*_dist (all-gather)")) return wrc;   // host index arrays go out of scope
+        CK(launch_k_lvl(2, unpack_slabs_kernel<T>, dim3(blocks), dim3(256), 0, g_stream, Z, ldz, m, nb, nblk, P,
+                        (const T *)recvb, (const int64_t *)meta, (const int64_t *)(meta + nblk),
+                        (const int64_t *)(meta + 2 * nblk), (const int *)owner_d, (const int *)qidx_d, mc,
+                        (const int *)Eall, (const int *)ea, scales, reinterpret_cast<int *>(scale_exp)));
+        CK_LAUNCH("unpack_slabs_kernel");
+        if (int wrc = nccl_wait(g_stream, "trevc_*_dist (gather)")) return wrc;
     }
-    cudaFreeAsync(meta, g_stream);
-    cudaFreeAsync(Sb, g_stream);
-    cudaFreeAsync(dbuf, g_stream);
-    for (void *p : {(void *)pack, (void *)Zs, (void *)ss, (void *)es_, (void *)Za, (void *)sa,
-                    (void *)ea, (void *)perm_d})
-        if (p) cudaFreeAsync(p, g_stream);
+    free_all();
     return rc;
 }
 }  // namespace
