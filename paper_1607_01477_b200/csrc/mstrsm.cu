@@ -2052,6 +2052,52 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     };
     feed.etab_out = Eloc;
     feed.ld_etab = mc;
+    // MSTRSM_DIST_EMULATE_FULL=1 (testing, with MSTRSM_DIST_EMULATE_P): every rank's shard is solved
+    // here in turn and its slabs, E table and exponents land where the P-rank gathers would put
+    // them, so the unpack must reproduce trevc_* bit for bit -- the P-rank layout tested on one GPU
+    static const bool emul_full = [] { const char *e = getenv("MSTRSM_DIST_EMULATE_FULL"); return e && e[0] == '1'; }();
+    if (emul && emul_full) {
+        int rc = 0;
+        std::vector<T *> zq(P, nullptr);
+        for (int q = 0; q < P && !rc; q++) {
+            const auto &cq = rc_cols[q];
+            const int64_t nq = int64_t(cq.size());
+            CK(cudaMallocAsync(&zq[q], size_t(m) * std::max<int64_t>(nq, 1) * es, g_stream));
+            PanelFeed fq = feed;
+            T *Zq = zq[q];
+            fq.after_diag = [&, q, Zq, nq](int64_t b) -> int {
+                const Blk bl = block_rows(0, m, nb, b);
+                const int64_t nbr = bl.hi - bl.lo, act = nq - c0[b * P + q], S = send_off[b + 1] - send_off[b];
+                cudaEvent_t e;
+                if (int erc = new_event(&e)) return erc;
+                CK(cudaEventRecord(e, g_stream));
+                CK(cudaStreamWaitEvent(cs, e, 0));
+                if (act > 0)
+                    CK(cudaMemcpy2DAsync(recvb + slab_off[b] + q * S, size_t(nbr) * es, Zq + bl.lo + c0[b * P + q] * m,
+                                         size_t(m) * es, size_t(nbr) * es, size_t(act), cudaMemcpyDeviceToDevice, cs));
+                return 0;
+            };
+            fq.etab_out = Eall + int64_t(q) * nblk * mc;
+            if (nq > 0) rc = trevc_impl<T>(Tuse, lduse, m, cq.data(), nq, Zq, m, ss, ea + int64_t(q) * mc, nb, &fq);
+        }
+        cudaEvent_t e;
+        if (int erc = new_event(&e)) return erc;
+        CK(cudaEventRecord(e, cs));
+        CK(cudaStreamWaitEvent(g_stream, e, 0));
+        if (!rc) {
+            const int blocks = int(std::min<int64_t>(cdiv(m, 8), int64_t(g_num_sms) * 16));
+            CK(launch_k_lvl(2, unpack_slabs_kernel<T>, dim3(blocks), dim3(256), 0, g_stream, Z, ldz, m, nb, nblk, P,
+                            (const T *)recvb, (const int64_t *)meta, (const int64_t *)(meta + nblk),
+                            (const int64_t *)(meta + 2 * nblk), (const int *)owner_d, (const int *)qidx_d, mc,
+                            (const int *)Eall, (const int *)ea, scales, reinterpret_cast<int *>(scale_exp)));
+            CK_LAUNCH("unpack_slabs_kernel");
+        }
+        CK(cudaStreamSynchronize(g_stream));
+        for (T *z : zq)
+            if (z) cudaFreeAsync(z, g_stream);
+        free_all();
+        return rc < 0 ? 1 : rc;
+    }
     int rc = 0;
     if (ncols > 0) {
         rc = trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb, &feed);

@@ -126,3 +126,39 @@ print(json.dumps({{"Z": bool(torch.equal(Z1, Z2)), "e": bool(torch.equal(e1, e2)
     assert out.returncode == 0, out.stderr[-2000:]
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["Z"] and r["e"] and r["s"] and r["rescaled"] > 0, r
+
+
+@pytest.mark.parametrize("P,case", [(4, "c5"), (8, "c5"), (3, "c2")])
+def test_trevc_dist_p_rank_layout_emulated_bit_identical(P, case):
+    """The P-rank row-block gather (slab widths, offsets, the receiver's a.6 fix-up with the
+    gathered E table) on one GPU: MSTRSM_DIST_EMULATE_P=P with MSTRSM_DIST_EMULATE_FULL=1 solves
+    every rank's shard in turn and places its slabs, E table and exponents where the gathers would,
+    so the unpack must reproduce trevc bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = f"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1607_01477_b200 as ms
+from paper_1607_01477_b200 import inputs
+case = {case!r}
+m, nb = (1100, 128) if case == "c5" else (700, 64)
+T = inputs.c5_grcar_like(m) if case == "c5" else inputs.c2_trevc_real(m)
+T = torch.from_numpy(np.asfortranarray(T)).cuda()
+ms.comm_init(1, 0)
+Z1, s1, e1 = ms.trevc_dist(T, m, nb=nb)
+ms.comm_destroy()
+Z2, s2, e2 = ms.trevc(T, nb=nb)
+torch.cuda.synchronize()
+print(json.dumps({{"Z": bool(torch.equal(Z1, Z2)), "e": bool(torch.equal(e1, e2)), "s": bool(torch.equal(s1, s2)),
+                   "rescaled": int((e2 < 0).sum().item())}}))
+"""
+    env = dict(os.environ, MSTRSM_DIST_EMULATE_P=str(P), MSTRSM_DIST_EMULATE_FULL="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["Z"] and r["e"] and r["s"], r
