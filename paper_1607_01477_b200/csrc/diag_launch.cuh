@@ -256,11 +256,13 @@ int launch_diag(const DiagArgs<T> &a, int nb) {
         if (f == 8 || (f == 0 && p8 <= p4)) return launch_diagf_pair<T, 8, 8, SAFE, OP>(a, nb);
         return launch_diagf_pair<T, 4, 16, SAFE, OP>(a, nb);
     }
-    const int64_t p8 = passes(8, DiagW<T, 8, 16, SAFE>::kSub), p16 = passes(16, DiagW<T, 16, 8, SAFE>::kSub),
-                  p32 = passes(32, DiagW<T, 32, 4, SAFE>::kSub);
-    if (f == 32 || (f == 0 && p32 <= std::min(p16, p8))) return launch_diagf_pair<T, 32, 4, SAFE, OP>(a, nb);
-    if (f == 16 || (f == 0 && p16 <= p8)) return launch_diagf_pair<T, 16, 8, SAFE, OP>(a, nb);
-    return launch_diagf_pair<T, 8, 16, SAFE, OP>(a, nb);
+    // n_b > 64: (8, 16) packs 4 columns per warp but its 16 register slots make a large,
+    // instruction-cache-hungry loop nest; two passes of (16, 8) beat one of (8, 16) (c5 diagonal
+    // step 12.9 -> 12.2 ms, profiles/r02/exp_c5lpc.txt), so (8, 16) is only taken when forced
+    const int64_t p16 = passes(16, DiagW<T, 16, 8, SAFE>::kSub), p32 = passes(32, DiagW<T, 32, 4, SAFE>::kSub);
+    if (f == 8) return launch_diagf_pair<T, 8, 16, SAFE, OP>(a, nb);
+    if (f == 32 || (f == 0 && p32 <= p16)) return launch_diagf_pair<T, 32, 4, SAFE, OP>(a, nb);
+    return launch_diagf_pair<T, 16, 8, SAFE, OP>(a, nb);
 }
 
 // Generalized solve (Alg. 7/8, op N): U' = U - lambda V on the fly; n_b <= 64 (two packed
