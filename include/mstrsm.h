@@ -33,7 +33,8 @@
  *    -i   argument i is invalid (1-based position in the C prototype)
  *     1   CUDA launch / runtime error (message: mstrsm_error_string(1))
  *     2   non-finite entry in U or the shifts (safe variants; reported by
- *         mstrsm_status(), which synchronises -- the solve itself stays asynchronous)
+ *         mstrsm_status(), which synchronises -- the solve itself stays asynchronous; after
+ *         mstrsm_set_sync_status(1) the call itself synchronises and returns it)
  *     3   communication error (multi-GPU helpers)
  *   m == 0 or n == 0 returns 0 immediately.  A zero right-hand-side column yields x = 0,
  *   c = 1 (R13).  The unsafe variants do not replace zero pivots: Inf/NaN propagate.
@@ -86,19 +87,23 @@ int mstrsm_z_safe(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm
  *   safe          0: Alg. 3, 1: Alg. 5
  *   op            MSTRSM_OP_N or MSTRSM_OP_C (C: (U - s I)^H, i.e. L = U^H - conj(s) I)
  *   shift_stride  stride between consecutive shifts (ldu + 1 reads diag(U) in place)
- *   row_end_host  HOST pointer (nullable, op N only): n values r_j in [0, m]; column j is
+ *   row_end       nullable, op N only: n values r_j (clamped to [0, m]); column j is
  *                 solved on rows [0, r_j) and rows [r_j, m) are set to 0 (R26; the eigen
- *                 shortcut of P:503-508 is r_k = k).  If the values are non-decreasing the
- *                 library skips inactive columns per block.  Copied before return.
+ *                 shortcut of P:503-508 is r_k = k).  Device memory or host
+ *                 memory, told apart with cudaPointerGetAttributes.  If the values are
+ *                 non-decreasing the library skips inactive columns per block; to know that it
+ *                 reads them on the host, so a DEVICE row_end costs one synchronisation of the
+ *                 caller's stream (the work already enqueued on it completes first).  Read
+ *                 before return; the caller may free or reuse it afterwards.
  *   scales        nullable for safe = 0; required for safe = 1
  *   scale_exp     nullable: n int32 receiving e_j (c_j = 2^{e_j}); 0 for safe = 0
  */
 int mstrsm_d_ex(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m,
                 const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
-                const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb);
+                const int64_t *row_end, double *scales, int32_t *scale_exp, int nb);
 int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
                 const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb,
-                int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
+                int64_t n, const int64_t *row_end, double *scales, int32_t *scale_exp,
                 int nb);
 
 /* Caller-managed workspace: as mstrsm_*_ex, with every device allocation of the
@@ -110,11 +115,11 @@ int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, i
 size_t mstrsm_workspace_size(int64_t m, int64_t n, int nb, int is_complex, int safe);
 int mstrsm_d_ex_ws(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m,
                    const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
-                   const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb,
+                   const int64_t *row_end, double *scales, int32_t *scale_exp, int nb,
                    void *workspace, size_t workspace_bytes);
 int mstrsm_z_ex_ws(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
                    const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
-                   int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales,
+                   int64_t ldb, int64_t n, const int64_t *row_end, double *scales,
                    int32_t *scale_exp, int nb, void *workspace, size_t workspace_bytes);
 
 /* ------------------------------------------------------------------------------------
@@ -235,13 +240,14 @@ int spectral_portrait_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, int64_
  * is B(I0) -= U(I0,I1) X(I1) and B(I0) += V(I0,I1) C, C = lambda X(I1).  Bounds: R30;
  * zero pivots of U' are replaced by delta_j = 2^-52 (||U|| + |lambda_j| ||V||) (R31); C is formed
  * after the column rescale (R32).  1 <= nb <= 64 (nb = 0: 64).  Other arguments as mstrsm_*_ex
- * (row_end_host a HOST pointer, nullable).  Errors: -i for argument i, 1 CUDA error.        */
+ * (row_end nullable, device or host memory, as there).  Errors: -i for argument i, 1 CUDA
+ * error.                                                                                   */
 int mstrsm_d_gen(int safe, const double *U, int64_t ldu, const double *V, int64_t ldv, int64_t m,
                  const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
-                 const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb);
+                 const int64_t *row_end, double *scales, int32_t *scale_exp, int nb);
 int mstrsm_z_gen(int safe, const mstrsm_dcomplex *U, int64_t ldu, const mstrsm_dcomplex *V, int64_t ldv,
                  int64_t m, const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
-                 int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
+                 int64_t ldb, int64_t n, const int64_t *row_end, double *scales, int32_t *scale_exp,
                  int nb);
 
 /* GeneralizedTriangEig, appendix Alg. 9 first function: lambda_k = T(k,k)/S(k,k)
@@ -344,6 +350,12 @@ const char *mstrsm_error_string(int code);
 /* Synchronises the current stream; returns 0, 1 (sticky CUDA error) or 2 (a safe call
  * since the last mstrsm_status saw a non-finite U entry or shift); clears the flag.   */
 int         mstrsm_status(void);
+/* on = 1: every safe solve / eigenvector entry (mstrsm_*_safe, _ex, _ex_ws, _side, _gen,
+ * trevc_*, trevc_*_cols, trevc_qz_*, tgevc_*) synchronises the current stream before it
+ * returns and returns 2 itself when the input held a non-finite value (clearing the flag as
+ * mstrsm_status does).  on = 0 (default): asynchronous, code 2 through mstrsm_status only.
+ * Per calling thread.  Returns 0.                                                         */
+int         mstrsm_set_sync_status(int on);
 /* Number of kernels libmstrsm.so has launched since the last reset (for bench/gpu_launches). */
 int64_t     mstrsm_launch_count(int reset);
 

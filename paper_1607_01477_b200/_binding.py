@@ -28,7 +28,7 @@ __all__ = [
     "spectral_cloud_z", "spectral_window_z", "spectral_portrait_z", "spectral_cloud", "spectral_window",
     "spectral_portrait", "comm_init", "comm_destroy", "dist_shard", "trevc_dist", "solve_dist", "pack_cols", "unpack_cols", "mstrsm_workspace_size", "mstrsm_d_ex_ws", "mstrsm_z_ex_ws", "mstrsm_d_side", "mstrsm_z_side", "solve_side",
     "eig_backtransform_d", "eig_backtransform_z", "trevc_qz_d", "trevc_qz_z", "eig_backtransform", "trevc_qz",
-    "mstrsm_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
+    "mstrsm_status", "mstrsm_set_sync_status", "mstrsm_launch_count", "mstrsm_fp64_peak", "mstrsm_error_string",
     "mstrsm_profile", "mstrsm_profile_read", "mstrsm_gemm_real_products",
     "solve", "trevc", "pseudospectra", "fp64_peak", "status", "launch_count", "gemm_real_products",
 ]
@@ -92,6 +92,7 @@ def load():
         "trevc_qz_z": [P, c_i64, c_i64, P, c_i64, P, c_i64, P, P, c_int],
         "mstrsm_set_stream": [P],
         "mstrsm_status": [],
+        "mstrsm_set_sync_status": [c_int],
         "mstrsm_launch_count": [c_int],
         "mstrsm_fp64_peak": [c_dbl, P, P],
         "mstrsm_error_string": [c_int],
@@ -155,6 +156,25 @@ def _host_i64(a):
     return arr, arr.ctypes.data_as(c_vp)
 
 
+def _row_end(a, n):
+    """row_end for the C call: a CUDA int64 tensor is passed as a device pointer (the ABI's form,
+    include/mstrsm.h), anything else is converted to a host int64 array."""
+    if a is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor) and a.is_cuda:
+            if a.dtype != torch.int64 or not a.is_contiguous() or a.numel() < n:
+                raise ValueError("row_end: a contiguous int64 CUDA tensor with at least n entries")
+            return a, c_vp(a.data_ptr())
+    except ImportError:
+        pass
+    arr, p = _host_i64(a)
+    if arr.size < n:
+        raise ValueError("row_end: at least n entries")
+    return arr, p
+
+
 # ------------------------------------------------------------------ C-named entry points
 def _call(name, *args):
     lib = load()
@@ -178,14 +198,14 @@ def mstrsm_z_safe(U, ldu, m, shifts, B, ldb, n, scales, nb):
     _call("mstrsm_z_safe", _ptr(U), ldu, m, _ptr(shifts), _ptr(B), ldb, n, _ptr(scales), nb)
 
 
-def mstrsm_d_ex(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
-    arr, p = _host_i64(row_end_host)
+def mstrsm_d_ex(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end, scales, scale_exp, nb):
+    arr, p = _row_end(row_end, n)
     _call("mstrsm_d_ex", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
           _ptr(scales), _ptr(scale_exp), nb)
 
 
-def mstrsm_z_ex(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
-    arr, p = _host_i64(row_end_host)
+def mstrsm_z_ex(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end, scales, scale_exp, nb):
+    arr, p = _row_end(row_end, n)
     _call("mstrsm_z_ex", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
           _ptr(scales), _ptr(scale_exp), nb)
 
@@ -277,14 +297,14 @@ def trevc_z_host_batch(T_hosts, m: int, Z_hosts, scales_hosts=None, exp_hosts=No
            "trevc_z_host_batch")
 
 
-def mstrsm_d_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
-    arr, p = _host_i64(row_end_host)
+def mstrsm_d_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end, scales, scale_exp, nb):
+    arr, p = _row_end(row_end, n)
     _call("mstrsm_d_gen", safe, _ptr(U), ldu, _ptr(V), ldv, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
           _ptr(scales), _ptr(scale_exp), nb)
 
 
-def mstrsm_z_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb):
-    arr, p = _host_i64(row_end_host)
+def mstrsm_z_gen(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end, scales, scale_exp, nb):
+    arr, p = _row_end(row_end, n)
     _call("mstrsm_z_gen", safe, _ptr(U), ldu, _ptr(V), ldv, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
           _ptr(scales), _ptr(scale_exp), nb)
 
@@ -382,16 +402,16 @@ def mstrsm_workspace_size(m: int, n: int, nb: int, is_complex: bool, safe: bool)
     return int(load().mstrsm_workspace_size(m, n, nb, int(is_complex), int(safe)))
 
 
-def mstrsm_d_ex_ws(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb,
+def mstrsm_d_ex_ws(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end, scales, scale_exp, nb,
                    workspace, workspace_bytes):
-    arr, p = _host_i64(row_end_host)
+    arr, p = _row_end(row_end, n)
     _call("mstrsm_d_ex_ws", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
           _ptr(scales), _ptr(scale_exp), nb, _ptr(workspace), workspace_bytes)
 
 
-def mstrsm_z_ex_ws(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales, scale_exp, nb,
+def mstrsm_z_ex_ws(safe, op, U, ldu, m, shifts, shift_stride, B, ldb, n, row_end, scales, scale_exp, nb,
                    workspace, workspace_bytes):
-    arr, p = _host_i64(row_end_host)
+    arr, p = _row_end(row_end, n)
     _call("mstrsm_z_ex_ws", safe, op, _ptr(U), ldu, m, _ptr(shifts), shift_stride, _ptr(B), ldb, n, p,
           _ptr(scales), _ptr(scale_exp), nb, _ptr(workspace), workspace_bytes)
 
@@ -442,6 +462,10 @@ def mstrsm_status() -> int:
     lib = load()
     _bind_stream(lib)
     return int(lib.mstrsm_status())
+
+
+def mstrsm_set_sync_status(on: int) -> int:
+    return int(load().mstrsm_set_sync_status(1 if on else 0))
 
 
 def mstrsm_launch_count(reset: int = 0) -> int:

@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
                     a.dblk[j] = -(kt + k3);
                     a.Etab[a.b * a.n + j] = ej;
                 }
+                if (active && keep) pair_fix(a, j, -(kt + k3), ej, rl, LPC);
             }
 #pragma unroll
             for (int t = 0; t < RPL; t++) {

@@ -56,6 +56,11 @@ struct DiagArgs {
     T *Cbuf; int64_t ldc;
     // complex 3M update (nullable): Re + Im of the finished rows I1, Xsum[(row - lo) + j * ldxs]
     double *Xsum; int64_t ldxs;
+    // paired blocks (the merged update; nullable): this block is the second of a pair
+    // whose first block p = rows [plo, phi), columns from c0prev, solved just before it, wrote its
+    // exponent deltas to dprev; xsprev = p's X+ rows (ld ldxs, complex 3M only)
+    const int *dprev; int64_t c0prev, plo, phi, bprev;
+    double *xsprev;
 };
 
 template <typename T> struct DiagArgs;
@@ -102,6 +107,30 @@ __device__ __forceinline__ double mulp2n(double v, int k) {
     return __dmul_rn(__dmul_rn(v, pow2i(-1022)), pow2i(-min(k - 1022, 1022)));
 }
 __device__ __forceinline__ cplx mulp2n(cplx v, int k) { return make_double2(mulp2n(v.x, k), mulp2n(v.y, k)); }
+
+// Paired blocks (merged update).  The update of the rows beyond a pair (p, b) of
+// consecutive blocks is one GEMM with K = K_p + K_b, run after b's diagonal step:
+//   C := 2^(d_p + d_b) C - U(., I_p) (2^d_b X_p) - U(., I_b) X_b,
+// the same sum Alg. 5 forms with two GEMMs, 2^d_b (2^d_p C - U(., I_p) X_p) - U(., I_b) X_b, to
+// rounding.  So when column j rescales in b's step (d_b = d < 0), X_p's rows (and its X+ rows)
+// are scaled by 2^d in place -- exact powers of two -- and Etab(p, j) moves to b's frame e_j (the
+// a.6 fix-up then scales them by 2^(e - E_bj) like b's rows), and dblk[j] (the merged update's
+// factor) becomes d_p + d.  Called by the nl lanes of column j's group (lane < nl) after the
+// step's e_j / dblk writes, for an active column.
+template <typename T>
+__device__ __forceinline__ void pair_fix(const DiagArgs<T> &a, int64_t j, int d, int ej, int lane, int nl) {
+    if (!a.dprev) return;
+    const bool inp = j >= a.c0prev;                  // (columns before p's range: X_p = 0, d_p = 0)
+    if (lane == 0) a.dblk[j] = d + (inp ? a.dprev[j] : 0);
+    if (d == 0 || !inp) return;
+    T *x = a.B + j * a.ldb;
+    for (int64_t r = a.plo + lane; r < a.phi; r += nl) x[r] = mulp2n(x[r], -d);
+    if (a.xsprev) {
+        double *xs = a.xsprev + j * a.ldxs;
+        for (int64_t r = lane; r < a.phi - a.plo; r += nl) xs[r] = mulp2n(xs[r], -d);
+    }
+    if (lane == 0) a.Etab[a.bprev * a.n + j] = ej;
+}
 // y := 2^-k y for a whole register array (one scale factor for all elements); k <= 1022 when
 // SMALL, any k >= 0 otherwise.
 template <bool SMALL, typename T, int N>
@@ -188,22 +217,33 @@ __device__ __forceinline__ int minpow2_bits(double a, double L) {
 //   complex: 1/d from an exactly prescaled conj(d)/|d|^2; x = y * (1/d) differs from the
 //            oracle's Smith quotient by a few ulps (R24).
 template <typename T> struct Piv;
+// Real pivots: y / d correctly rounded, as q0 = y r, one residual correction (exact when q and d
+// are well inside the normal range), else the IEEE division.  The range tests are integer tests of
+// the biased exponents (FP64 compares issue on the FP64 pipe the row loop needs): |d| in
+// [2^-999, 2^999) once per pivot, |q| in [2^-959, 2^999) per quotient -- inside the ranges the
+// correction is exact on, so both branches give the same correctly rounded quotient.
 template <> struct Piv<double> {
     double d, r;
-    __device__ __forceinline__ void make(double dd) { d = dd; r = __drcp_rn(dd); }
+    bool dok;
+    __device__ __forceinline__ void make(double dd) {
+        d = dd;
+        r = __drcp_rn(dd);
+        dok = unsigned(((__double2hiint(dd) >> 20) & 0x7ff) - 24) <= 1997u;
+    }
     __device__ __forceinline__ double apply(double y) const {
         double q0 = __dmul_rn(y, r);
         double rem = fma(-q0, d, y);
         double q = fma(rem, r, q0);
-        double aq = fabs(q), ad = fabs(d);
-        bool ok = (aq < 0x1p+1000 && aq > 0x1p-960 && ad < 0x1p+1000 && ad > 0x1p-1000) || y == 0.0;
-        return ok ? q : __ddiv_rn(y, d);
+        const bool qok = unsigned(((__double2hiint(q) >> 20) & 0x7ff) - 64) <= 1957u;
+        const bool yzero = ((unsigned(__double2hiint(y)) << 1) | unsigned(__double2loint(y))) == 0u;
+        return (dok && qok) || yzero ? q : __ddiv_rn(y, d);
     }
     __device__ __forceinline__ double absd() const { return fabs(d); }
     template <int W> __device__ __forceinline__ Piv shfl(int src) const {
         Piv o;
         o.d = __shfl_sync(0xffffffffu, d, src, W);
         o.r = __shfl_sync(0xffffffffu, r, src, W);
+        o.dok = __shfl_sync(0xffffffffu, int(dok), src, W) != 0;
         return o;
     }
 };

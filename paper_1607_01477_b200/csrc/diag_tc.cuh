@@ -437,6 +437,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                     a.dblk[j] = -(kt + k3);
                     a.Etab[a.b * a.n + j] = ej;
                 }
+                if (active && !failed) pair_fix(a, j, -(kt + k3), ej, tq, 4);
             }
             const int sfin = F - kt - k3;
             if (valid && !failed) {
@@ -512,6 +513,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                     a.dblk[jf] = -(ktf + k3);
                     a.Etab[a.b * a.n + jf] = ej;
                 }
+                pair_fix(a, jf, -(ktf + k3), ej, lane, 32);
                 double *xsum = nullptr;
                 if constexpr (ST::cplx_) xsum = a.Xsum ? a.Xsum + jf * a.ldxs : nullptr;
 #pragma unroll

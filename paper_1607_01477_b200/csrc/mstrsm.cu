@@ -126,12 +126,15 @@ int norm_pass(int op, const T *U, int64_t ldu, int64_t m, int nb, Work &w, bool 
         CK_LAUNCH("rowsum_reduce_kernel");
         ws_free(part2, g_stream);
     } else {
-        norm_rows_c_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
-        CK_LAUNCH("norm_rows_c_kernel");
+        CK(cudaMemsetAsync(w.cnl, 0, size_t(m) * 8, g_stream));
+        CK(cudaMemsetAsync(w.part, 0, size_t(m) * 8, g_stream));
+        norm_rows_c_chunk_kernel<T><<<dim3(unsigned(cdiv(m, 128)), unsigned(cdiv(m, kRowsumChunk))), 128, 0,
+                                      g_stream>>>(U, ldu, m, nb, w.cnl, w.part, g_flag);
+        CK_LAUNCH("norm_rows_c_chunk_kernel");
         panel_sum_kernel<<<int(cdiv(nblk, 128)), 128, 0, g_stream>>>(1, m, nb, nblk, w.part, w.P);
         CK_LAUNCH("panel_sum_kernel");
-        colsum_c_kernel<T><<<int(cdiv(m, 128)), 128, 0, g_stream>>>(U, ldu, m, w.part);
-        CK_LAUNCH("colsum_c_kernel");
+        colsum_c_tiled_kernel<T><<<int(cdiv(m, 32)), 256, 0, g_stream>>>(U, ldu, m, w.part);
+        CK_LAUNCH("colsum_c_tiled_kernel");
     }
     delta_kernel<<<1, 1024, 0, g_stream>>>(m, w.part, w.delta);
     CK_LAUNCH("delta_kernel");
@@ -191,6 +194,31 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
                      Work &w, const double *Usum, double *Xsum, int64_t ldus, int ldxs);
 
 // ---------------------------------------------------------------- the blocked solve
+// Paired blocks (pair_blocks below): blocks 2q and 2q+1 (solve order) form a pair.
+// After the first block's diagonal step only the second block's rows are updated (a GEMM with
+// M = K = n_b); after the second's, the rows beyond both are updated by one GEMM with K = 2 n_b
+// (pair_fix in diag_kernel.cuh keeps the exponent bookkeeping of Alg. 5 exact).  The long update
+// GEMMs then run at twice the K: at K = n_b = 64 (c4) the per-tile epilogue and pipeline fill weigh
+// on the DMMA rate.  The X+ plane holds both blocks of a pair (ld = 2 x n_b rounded).
+// Measured (profiles/r02/exp_pair_r02.txt, single vs paired): complex n_b = 64 pays (c4 87.7 ->
+// 83.2 ms, c4d 74.1 -> 71.1: its K = 64 updates become K = 128 ones); at n_b = 128 the K = 128
+// update is already efficient and the extra launch per pair costs what K = 256 saves (c5 155.7 vs
+// 156.3, the 8-GPU shard 25.6 vs 26.0); real data loses (c2 1.30 vs 1.46: the diagonal step
+// dominates and the update is one more latency-bound launch).  So: complex with n_b <= 64.
+// MSTRSM_PAIR=0 never, =2 always (tests), default by that rule; even n_b only.
+template <typename T>
+bool pair_blocks(int nb) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_PAIR");
+        const char *o = getenv("MSTRSM_DIAG_OLD");              // (round 1's kernel has no pair_fix)
+        v = (o && o[0] == '1') ? 0 : (e && (e[0] == '0' || e[0] == '2') && !e[1]) ? e[0] - '0' : 1;
+    }
+    // (even n_b: the two blocks' X+ rows must be contiguous in the plane, and every block's first
+    // X+ row 16-byte aligned for the tensor maps)
+    return nb % 2 == 0 && (v == 2 || (v == 1 && S<T>::cplx_ && nb <= 64));
+}
+
 // State (G, e) must be initialised by the caller (init kernels).  active_from(b) gives the first
 // active column of block b when row ends are known on the host and sorted.
 template <typename T, bool SAFE>
@@ -198,76 +226,153 @@ int blocked_solve(int op, const T *U, int64_t ldu, int64_t m, const T *shifts, i
                   T *B, int64_t ldb, int64_t n, const int64_t *rowend_dev,
                   const std::vector<int64_t> *rowend_sorted_host, int nb, Work &w,
                   const double *Usum = nullptr, double *Xsum = nullptr, int64_t ldus = 0, int ldxs = 0) {
+    int64_t nblk = cdiv(m, nb);
+    const bool pair = pair_blocks<T>(nb) && nblk >= 2;
     if constexpr (SAFE) {
         // (small solves: stream/event overhead; real data: the update is cheap next to the diagonal
         // step, which the split would confine to a few SMs -- c2 1.36 ms with, 1.30 ms without)
-        if (op == 0 && m >= 1024 && S<T>::cplx_ && lookahead_enabled())
+        if (!pair && op == 0 && m >= 1024 && S<T>::cplx_ && lookahead_enabled())
             return blocked_solve_la<T>(U, ldu, m, shifts, sstride, B, ldb, n, rowend_dev, rowend_sorted_host, nb, w,
                                        Usum, Xsum, ldus, ldxs);
     }
-    int64_t nblk = cdiv(m, nb);
     if (SAFE) CK(cudaMemsetAsync(w.fb_count, 0, nblk * 4, g_stream));   // diag fallback counts
+    auto c0_of = [&](const Blk &bl) -> int64_t {
+        if (op != 0 || !rowend_sorted_host) return 0;
+        const auto &re = *rowend_sorted_host;
+        return std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();   // first r > lo
+    };
+    const int64_t ldxh = ldxs / 2;             // X+ rows per block of a pair
+    // X+ rows of block b within its pair's plane: op N, the second block (above) ends where the
+    // first begins (offset ldxh); op C, the first block (above) at 0, the second after it
+    auto xs_off = [&](int64_t b, bool second) -> int64_t {
+        if (!pair) return 0;
+        const Blk bl = block_rows(op, m, nb, b);
+        if (op == 0) return second ? ldxh - (bl.hi - bl.lo) : ldxh;
+        return second ? ldxh : 0;
+    };
+    auto after_diag = [&](int64_t b) -> int { return t_after_diag ? (*t_after_diag)(b) : 0; };
+    auto debug = [&](int64_t b, const char *what) {
+        if (!g_debug_sync) return;
+        cudaError_t e = cudaStreamSynchronize(g_stream);
+        fprintf(stderr, "[mstrsm debug] block %lld %s done (%s)\n", (long long)b, what, cudaGetErrorString(e));
+    };
     int early = 0;                             // U / cnl ready: later launches stage before the wait
+    bool first_ran = false;                    // pair: the first block of the current pair ran its step
+    int64_t c0_first = 0;
     for (int64_t b = 0; b < nblk; b++) {
         if (t_pre_block) {
             if (int rc = (*t_pre_block)(b)) return rc;
         }
         const T *Ub = t_blk_U ? static_cast<const T *>(t_blk_U) : U;   // this block's view of U
         const int64_t ldub = t_blk_U ? t_blk_ld : ldu;
-        Blk bl = block_rows(op, m, nb, b);
-        int64_t c0 = 0;
-        if (op == 0 && rowend_sorted_host) {
-            const auto &re = *rowend_sorted_host;
-            c0 = std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();   // first r > lo
-        }
-        int64_t ncols = n - c0;
+        // (the pairing depends on the block index only, never on which columns are active, so a
+        // column's arithmetic is the same in every column subset: multi-GPU shards reproduce the
+        // single-GPU solve bit for bit.  A first block without active columns has X = 0 and no
+        // exponent deltas; its pair's second block still runs the merged update.)
+        const bool is_first = pair && (b % 2 == 0) && b + 1 < nblk;
+        const bool is_second = pair && (b % 2 == 1);
+        const Blk bl = block_rows(op, m, nb, b);
+        const int64_t c0 = c0_of(bl);
+        const int64_t ncols = n - c0;
         if (ncols <= 0) {                      // (the after-diag hook's collectives run on every rank)
-            if (t_after_diag) {
-                if (int rc = (*t_after_diag)(b)) return rc;
+            if (is_first) { first_ran = false; c0_first = n; }
+            if (is_second && first_ran) {
+                // (not reached with sorted row ends: a block's active columns include those of the
+                // block solved before it) the first block's update of the rows beyond the pair alone
+                first_ran = false;
+                if (int rc = after_diag(b - 1)) return rc;
+                const Blk bp = block_rows(op, m, nb, b - 1);
+                GemmArgs<T> g{};
+                g.U = Ub; g.ldu = ldub; g.B = B; g.ldb = ldb; g.X = B; g.ldx = ldb;
+                g.dblk = SAFE ? w.dblk : nullptr;
+                g.M = op == 0 ? bl.lo : m - bl.hi; g.N = n - c0_first; g.K = int(bp.hi - bp.lo);
+                if (op == 0) { g.a_r0 = 0; g.a_c0 = bp.lo; g.c_r0 = 0; }
+                else { g.a_r0 = bp.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
+                g.x_r0 = bp.lo; g.col0 = c0_first;
+                if (Usum && Xsum) { g.As = Usum; g.ldas = ldus; g.Xsum = Xsum + xs_off(b - 1, false); g.ldxs = ldxs; }
+                if (g.M > 0 && g.N > 0) {
+                    if (int rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g)) return rc;
+                }
             }
+            if (int rc = after_diag(b)) return rc;
             continue;
         }
+        double *xs = Xsum ? Xsum + xs_off(b, is_second) : nullptr;
         DiagArgs<T> a{};
         a.U = Ub; a.ldu = ldub; a.m = m; a.shifts = shifts; a.sstride = sstride;
         a.B = B; a.ldb = ldb; a.c0 = c0; a.ncols = ncols; a.n = n;
         a.rowend = op == 0 ? rowend_dev : nullptr;
         a.lo = bl.lo; a.hi = bl.hi; a.b = b;
         a.cnl = w.cnl; a.P = w.P; a.delta = w.delta;
-        a.G = w.G; a.e = w.e; a.dblk = w.dblk; a.Etab = w.Etab;
+        a.G = w.G; a.e = w.e; a.dblk = is_second ? w.dblk2 : w.dblk; a.Etab = w.Etab;
         a.fb_list = w.fb_list; a.fb_count = w.fb_count + b;
         a.force_fb = g_diag_force_fb;
         a.early = early;
         a.Xscr = static_cast<T *>(w.xscr); a.ldscr = w.ldscr;
         a.Ppart = t_panel_part;
-        a.Xsum = Xsum; a.ldxs = ldxs;
-        if (Xsum && rowend_dev && !rowend_sorted_host)        // inactive columns in range: zero rows
-            CK(cudaMemsetAsync(Xsum + c0 * ldxs, 0, size_t(ncols) * ldxs * 8, g_stream));
+        a.Xsum = xs; a.ldxs = ldxs;
+        if (SAFE && is_second && first_ran) {
+            const Blk bp = block_rows(op, m, nb, b - 1);
+            a.dprev = w.dblk; a.c0prev = c0_first; a.plo = bp.lo; a.phi = bp.hi; a.bprev = b - 1;
+            a.xsprev = Xsum ? Xsum + xs_off(b - 1, false) : nullptr;
+        }
+        if (xs && rowend_dev && !rowend_sorted_host)          // inactive columns in range: zero rows
+            CK(cudaMemset2DAsync(xs + c0 * ldxs, size_t(ldxs) * 8, 0, size_t(bl.hi - bl.lo) * 8, size_t(ncols),
+                                 g_stream));
         int rc = op == 0 ? launch_diag<T, SAFE, 0>(a, nb) : launch_diag<T, SAFE, 1>(a, nb);
         early = t_pre_block ? 0 : 1;           // (a per-block prepass writes cnl right before the diag)
         if (rc) return rc;
-        if (t_after_diag) {
-            if ((rc = (*t_after_diag)(b))) return rc;
+        // the after-diag hook sees final rows only: a pair's first block's rows may still be
+        // rescaled by the second block's step
+        if (!is_first) {
+            if (is_second && first_ran && (rc = after_diag(b - 1))) return rc;
+            if ((rc = after_diag(b))) return rc;
         }
-        if (g_debug_sync) {
-            cudaError_t e = cudaStreamSynchronize(g_stream);
-            fprintf(stderr, "[mstrsm debug] block %lld diag done (%s)\n", (long long)b, cudaGetErrorString(e));
-        }
-        int64_t M = op == 0 ? bl.lo : m - bl.hi;
-        if (M <= 0) continue;
+        debug(b, "diag");
         GemmArgs<T> g{};
         g.U = Ub; g.ldu = ldub; g.B = B; g.ldb = ldb;
-        g.M = M; g.N = ncols; g.K = int(bl.hi - bl.lo);
-        if (op == 0) { g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0; }
-        else { g.a_r0 = bl.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
-        g.x_r0 = bl.lo; g.col0 = c0;
         g.X = B; g.ldx = ldb;
-        if (Usum && Xsum) { g.As = Usum; g.ldas = ldus; g.Xsum = Xsum; g.ldxs = ldxs; }
-        g.dblk = SAFE ? w.dblk : nullptr;
-        rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g);
-        if (rc) return rc;
-        if (g_debug_sync) {
-            cudaError_t e = cudaStreamSynchronize(g_stream);
-            fprintf(stderr, "[mstrsm debug] block %lld gemm done (%s)\n", (long long)b, cudaGetErrorString(e));
+        g.dblk = SAFE ? a.dblk : nullptr;
+        if (is_first) {
+            // the second block's rows only, K = K_b
+            const Blk bn = block_rows(op, m, nb, b + 1);
+            g.M = bn.hi - bn.lo; g.N = ncols; g.K = int(bl.hi - bl.lo);
+            if (op == 0) { g.a_r0 = bn.lo; g.a_c0 = bl.lo; g.c_r0 = bn.lo; }
+            else { g.a_r0 = bl.lo; g.a_c0 = bn.lo; g.c_r0 = bn.lo; }
+            g.x_r0 = bl.lo; g.col0 = c0;
+            if (Usum && xs) { g.As = Usum; g.ldas = ldus; g.Xsum = xs; g.ldxs = ldxs; }
+            first_ran = true;
+            c0_first = c0;
+        } else if (is_second) {
+            // the rows beyond both blocks, K = K_p + K_b over rows [lo, hi) of the pair
+            const Blk bp = block_rows(op, m, nb, b - 1);
+            const int64_t plo = std::min(bl.lo, bp.lo), phi = std::max(bl.hi, bp.hi);
+            g.M = op == 0 ? plo : m - phi; g.N = ncols; g.K = int(phi - plo);
+            if (op == 0) { g.a_r0 = 0; g.a_c0 = plo; g.c_r0 = 0; }
+            else { g.a_r0 = plo; g.a_c0 = phi; g.c_r0 = phi; }
+            g.x_r0 = plo; g.col0 = c0;
+            first_ran = false;
+            if (g.M <= 0) continue;
+            if (Usum && Xsum) {
+                double *xsp = Xsum + (op == 0 ? xs_off(b, true) : 0);
+                // the first block's X+ rows of the columns its step did not cover (X = 0 there)
+                if (c0_first > c0)
+                    CK(cudaMemset2DAsync(Xsum + xs_off(b - 1, false) + c0 * ldxs, size_t(ldxs) * 8, 0,
+                                         size_t(bp.hi - bp.lo) * 8, size_t(c0_first - c0), g_stream));
+                g.As = Usum; g.ldas = ldus; g.Xsum = xsp; g.ldxs = ldxs;
+            }
+        } else {
+            g.M = op == 0 ? bl.lo : m - bl.hi; g.N = ncols; g.K = int(bl.hi - bl.lo);
+            if (g.M <= 0) continue;
+            if (op == 0) { g.a_r0 = 0; g.a_c0 = bl.lo; g.c_r0 = 0; }
+            else { g.a_r0 = bl.lo; g.a_c0 = bl.hi; g.c_r0 = bl.hi; }
+            g.x_r0 = bl.lo; g.col0 = c0;
+            if (Usum && xs) { g.As = Usum; g.ldas = ldus; g.Xsum = xs; g.ldxs = ldxs; }
+        }
+        if (g.M > 0) {
+            rc = op == 0 ? launch_gemm<T, false>(g) : launch_gemm<T, true>(g);
+            if (rc) return rc;
+            debug(b, "gemm");
         }
     }
     return 0;
@@ -409,7 +514,7 @@ int make_sum_planes(SumPlanes &sp, int op, const T *U, int64_t ldu, int64_t m, i
         // even leading dimensions (16-byte aligned bulk copies), ldu > m so that a copy rounded
         // up to 16 bytes past the last row of a column stays inside that column
         sp.ldu = (m + 2) & ~int64_t(1);
-        sp.ldx = (nb + 1) & ~1;
+        sp.ldx = 2 * ((nb + 1) & ~1);              // both blocks of a pair (blocked_solve)
         CK(ws_malloc((void **)&sp.U, size_t(sp.ldu) * m * 8));
         CK(ws_malloc((void **)&sp.X, size_t(sp.ldx) * std::max<int64_t>(n, 1) * 8));
         if (!fill) return 0;                        // the caller's kernel writes the plane
@@ -439,9 +544,34 @@ bool is_sorted_nondecreasing(const int64_t *v, int64_t n) {
     return true;
 }
 
+// row_end (a device array; host memory accepted too).  The values are needed on the host
+// to skip inactive columns per block when they are non-decreasing, so a device row_end is read back
+// with one copy on the caller's stream (which waits for the work already enqueued on it).  The
+// clamped values go to w.rowend.  Returns 0 or 1 (CUDA error).
+int load_row_end(const int64_t *row_end, int64_t n, int64_t m, int64_t *rowend_dev,
+                 std::vector<int64_t> &re_host, bool &sorted) {
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, row_end);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        at.type = cudaMemoryTypeUnregistered;
+    }
+    re_host.resize(size_t(n));
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+        CK(cudaMemcpyAsync(re_host.data(), row_end, size_t(n) * 8, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+    } else {
+        std::copy(row_end, row_end + n, re_host.begin());
+    }
+    for (auto &v : re_host) v = v < 0 ? 0 : (v > m ? m : v);
+    sorted = is_sorted_nondecreasing(re_host.data(), n);
+    CK(cudaMemcpyAsync(rowend_dev, re_host.data(), size_t(n) * 8, cudaMemcpyHostToDevice, g_stream));
+    return 0;  // (a copy from pageable memory has consumed its source when it returns)
+}
+
 template <typename T>
 int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *shifts,
-                   int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                   int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *row_end,
                    double *scales, int32_t *scale_exp, int nb) {
     if (safe != 0 && safe != 1) return -1;
     if (op != 0 && op != 1) return -2;
@@ -452,7 +582,7 @@ int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T
     if (n < 0) return -10;
     if (nb == 0) nb = 64;
     if (nb < 1 || nb > 128) return -14;
-    if (op == 1 && row_end_host) return -11;
+    if (op == 1 && row_end) return -11;
     if (m == 0 || n == 0) return 0;
     if (!U) return -3;
     if (!shifts) return -6;
@@ -461,15 +591,11 @@ int mstrsm_ex_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T
     if (int rc = ensure_init()) return rc;
 
     Work w;
-    if (int rc = alloc_work<T>(w, m, n, nb, row_end_host != nullptr, false)) return rc;
+    if (int rc = alloc_work<T>(w, m, n, nb, row_end != nullptr, false)) return rc;
     std::vector<int64_t> re_host;
     bool sorted = false;
-    if (row_end_host) {
-        re_host.assign(row_end_host, row_end_host + n);
-        for (auto &v : re_host) v = v < 0 ? 0 : (v > m ? m : v);
-        sorted = is_sorted_nondecreasing(re_host.data(), n);
-        CK(cudaMemcpyAsync(w.rowend, re_host.data(), n * 8, cudaMemcpyHostToDevice, g_stream));
-    }
+    if (row_end)
+        if (int rc = load_row_end(row_end, n, m, w.rowend, re_host, sorted)) return rc;
     int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
     if (safe) {
         if (int rc = norm_pass<T>(op, U, ldu, m, nb, w)) return rc;
@@ -830,7 +956,7 @@ int blocked_solve_gen(const T *U, int64_t ldu, const T *V, int64_t ldv, int64_t 
 
 template <typename T>
 int mstrsm_gen_impl(int safe, const T *U, int64_t ldu, const T *V, int64_t ldv, int64_t m, const T *shifts,
-                    int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                    int64_t sstride, T *B, int64_t ldb, int64_t n, const int64_t *row_end,
                     double *scales, int32_t *scale_exp, int nb) {
     if (safe != 0 && safe != 1) return -1;
     if (m < 0) return -6;
@@ -849,16 +975,12 @@ int mstrsm_gen_impl(int safe, const T *U, int64_t ldu, const T *V, int64_t ldv, 
     if (safe && !scales) return -13;
     if (int rc = ensure_init()) return rc;
     Work w, wv;
-    if (int rc = alloc_work<T>(w, m, n, nb, row_end_host != nullptr, false)) return rc;
+    if (int rc = alloc_work<T>(w, m, n, nb, row_end != nullptr, false)) return rc;
     if (int rc = alloc_work<T>(wv, m, 1, nb, false, false)) return rc;
     std::vector<int64_t> re_host;
     bool sorted = false;
-    if (row_end_host) {
-        re_host.assign(row_end_host, row_end_host + n);
-        for (auto &v : re_host) v = v < 0 ? 0 : (v > m ? m : v);
-        sorted = is_sorted_nondecreasing(re_host.data(), n);
-        CK(cudaMemcpyAsync(w.rowend, re_host.data(), n * 8, cudaMemcpyHostToDevice, g_stream));
-    }
+    if (row_end)
+        if (int rc = load_row_end(row_end, n, m, w.rowend, re_host, sorted)) return rc;
     T *Cbuf = nullptr;
     CK(cudaMallocAsync(&Cbuf, size_t(nb) * n * sizeof(T), g_stream));
     int blocks = int(std::min<int64_t>(cdiv(n, 8), int64_t(g_num_sms) * 16));
@@ -869,7 +991,7 @@ int mstrsm_gen_impl(int safe, const T *U, int64_t ldu, const T *V, int64_t ldv, 
             init_rhs_kernel<T><<<blocks, 256, 0, g_stream>>>(B, ldb, m, n, w.rowend, shifts, sstride, w.G, w.e, g_flag);
             CK_LAUNCH("init_rhs_kernel");
             rc = blocked_solve_gen<T, true>(U, ldu, V, ldv, m, shifts, sstride, B, ldb, n, w.rowend,
-                                            sorted ? &re_host : nullptr, row_end_host && !sorted, nb, w, wv, Cbuf);
+                                            sorted ? &re_host : nullptr, row_end && !sorted, nb, w, wv, Cbuf);
         }
     } else {
         if (w.rowend) {
@@ -877,7 +999,7 @@ int mstrsm_gen_impl(int safe, const T *U, int64_t ldu, const T *V, int64_t ldv, 
             CK_LAUNCH("init_rhs_kernel");
         }
         rc = blocked_solve_gen<T, false>(U, ldu, V, ldv, m, shifts, sstride, B, ldb, n, w.rowend,
-                                         sorted ? &re_host : nullptr, row_end_host && !sorted, nb, w, wv, Cbuf);
+                                         sorted ? &re_host : nullptr, row_end && !sorted, nb, w, wv, Cbuf);
     }
     if (!rc && (scales || scale_exp || safe))
         rc = finalize<T>(0, safe, B, ldb, m, n, nb, w.rowend, scales, scale_exp, nullptr, w);
@@ -1132,20 +1254,33 @@ static int short_pos(int rc) {
 
 template <typename T>
 int ex_ws_impl(int safe, int op, const T *U, int64_t ldu, int64_t m, const T *shifts, int64_t sstride, T *B,
-               int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb,
+               int64_t ldb, int64_t n, const int64_t *row_end, double *scales, int32_t *scale_exp, int nb,
                void *workspace, size_t workspace_bytes) {
     if (!workspace)                                  // NULL: the library allocates (as mstrsm_*_ex)
-        return mstrsm_ex_impl<T>(safe, op, U, ldu, m, shifts, sstride, B, ldb, n, row_end_host, scales,
+        return mstrsm_ex_impl<T>(safe, op, U, ldu, m, shifts, sstride, B, ldb, n, row_end, scales,
                                  scale_exp, nb);
     if (reinterpret_cast<uintptr_t>(workspace) % 256) return -15;
     g_arena.base = static_cast<char *>(workspace);
     g_arena.size = workspace_bytes;
     g_arena.off = 0;
     g_arena.active = true;
-    int rc = mstrsm_ex_impl<T>(safe, op, U, ldu, m, shifts, sstride, B, ldb, n, row_end_host, scales, scale_exp, nb);
+    int rc = mstrsm_ex_impl<T>(safe, op, U, ldu, m, shifts, sstride, B, ldb, n, row_end, scales, scale_exp, nb);
     g_arena.active = false;
     if (rc == 1 && last_cuda_error() == cudaErrorMemoryAllocation) rc = -16;   // workspace too small
     return rc;
+}
+
+// mstrsm_set_sync_status(1): the calls that can see a non-finite input synchronise the caller's
+// stream before returning and report code 2 themselves (the flag is then cleared, as mstrsm_status
+// does).  Per calling thread; off by default (the calls stay asynchronous).
+static thread_local bool t_sync_status = false;
+static int sync_status(int rc) {
+    if (rc != 0 || !t_sync_status) return rc;
+    CK(cudaStreamSynchronize(g_stream));
+    int h = 0;
+    CK(cudaMemcpy(&h, g_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h) CK(cudaMemset(g_flag, 0, sizeof(int)));
+    return h ? 2 : 0;
 }
 
 extern "C" {
@@ -1161,24 +1296,24 @@ int mstrsm_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcom
 }
 int mstrsm_d_safe(const double *U, int64_t ldu, int64_t m, const double *shifts, double *B,
                   int64_t ldb, int64_t n, double *scales, int nb) {
-    return short_pos(mstrsm_ex_impl<double>(1, 0, U, ldu, m, shifts, 1, B, ldb, n, nullptr, scales, nullptr, nb));
+    return sync_status(short_pos(mstrsm_ex_impl<double>(1, 0, U, ldu, m, shifts, 1, B, ldb, n, nullptr, scales, nullptr, nb)));
 }
 int mstrsm_z_safe(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts, mstrsm_dcomplex *B,
                   int64_t ldb, int64_t n, double *scales, int nb) {
-    return short_pos(mstrsm_ex_impl<cplx>(1, 0, (const cplx *)U, ldu, m, (const cplx *)shifts, 1, (cplx *)B, ldb, n,
-                                nullptr, scales, nullptr, nb));
+    return sync_status(short_pos(mstrsm_ex_impl<cplx>(1, 0, (const cplx *)U, ldu, m, (const cplx *)shifts, 1, (cplx *)B, ldb, n,
+                                nullptr, scales, nullptr, nb)));
 }
 int mstrsm_d_ex(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
-                int64_t shift_stride, double *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                int64_t shift_stride, double *B, int64_t ldb, int64_t n, const int64_t *row_end,
                 double *scales, int32_t *scale_exp, int nb) {
-    return mstrsm_ex_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host,
-                                  scales, scale_exp, nb);
+    return sync_status(mstrsm_ex_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, row_end,
+                                  scales, scale_exp, nb));
 }
 int mstrsm_z_ex(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *shifts,
-                int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n, const int64_t *row_end,
                 double *scales, int32_t *scale_exp, int nb) {
-    return mstrsm_ex_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride,
-                                (cplx *)B, ldb, n, row_end_host, scales, scale_exp, nb);
+    return sync_status(mstrsm_ex_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride,
+                                (cplx *)B, ldb, n, row_end, scales, scale_exp, nb));
 }
 
 size_t mstrsm_workspace_size(int64_t m, int64_t n, int nb, int is_complex, int safe) {
@@ -1192,41 +1327,41 @@ size_t mstrsm_workspace_size(int64_t m, int64_t n, int nb, int is_complex, int s
     size_t total = work + 256;
     if (safe) total += size_t(cdiv(m, kRowsumChunk)) * m * 8 + 256;              // norm pass partials
     if (is_complex && gemm_variant() == 0 && gemm_presum_enabled())            // 3M operand-sum planes
-        total += size_t((m + 2) & ~int64_t(1)) * m * 8 + 2 * size_t((nb + 1) & ~1) * n * 8 + 768;
+        total += size_t((m + 2) & ~int64_t(1)) * m * 8 + 4 * size_t((nb + 1) & ~1) * n * 8 + 768;
     return total;
 }
 
 int mstrsm_d_ex_ws(int safe, mstrsm_op op, const double *U, int64_t ldu, int64_t m, const double *shifts,
-                   int64_t shift_stride, double *B, int64_t ldb, int64_t n, const int64_t *row_end_host,
+                   int64_t shift_stride, double *B, int64_t ldb, int64_t n, const int64_t *row_end,
                    double *scales, int32_t *scale_exp, int nb, void *workspace, size_t workspace_bytes) {
-    return ex_ws_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, row_end_host, scales,
-                              scale_exp, nb, workspace, workspace_bytes);
+    return sync_status(ex_ws_impl<double>(safe, int(op), U, ldu, m, shifts, shift_stride, B, ldb, n, row_end, scales,
+                              scale_exp, nb, workspace, workspace_bytes));
 }
 int mstrsm_z_ex_ws(int safe, mstrsm_op op, const mstrsm_dcomplex *U, int64_t ldu, int64_t m,
                    const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n,
-                   const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb, void *workspace,
+                   const int64_t *row_end, double *scales, int32_t *scale_exp, int nb, void *workspace,
                    size_t workspace_bytes) {
-    return ex_ws_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride, (cplx *)B,
-                            ldb, n, row_end_host, scales, scale_exp, nb, workspace, workspace_bytes);
+    return sync_status(ex_ws_impl<cplx>(safe, int(op), (const cplx *)U, ldu, m, (const cplx *)shifts, shift_stride, (cplx *)B,
+                            ldb, n, row_end, scales, scale_exp, nb, workspace, workspace_bytes));
 }
 
 int trevc_d(const double *T, int64_t ldt, int64_t m, double *Z, int64_t ldz, double *scales,
             int32_t *scale_exp, int nb) {
     int rc = trevc_impl<double>(T, ldt, m, nullptr, m, Z, ldz, scales, scale_exp, nb);
-    return rc < 0 ? (rc == -4 ? -1 : (rc <= -6 ? rc + 2 : rc)) : rc;
+    return rc < 0 ? (rc == -4 ? -1 : (rc <= -6 ? rc + 2 : rc)) : sync_status(rc);
 }
 int trevc_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, mstrsm_dcomplex *Z, int64_t ldz, double *scales,
             int32_t *scale_exp, int nb) {
     int rc = trevc_impl<cplx>((const cplx *)T, ldt, m, nullptr, m, (cplx *)Z, ldz, scales, scale_exp, nb);
-    return rc < 0 ? (rc == -4 ? -1 : (rc <= -6 ? rc + 2 : rc)) : rc;
+    return rc < 0 ? (rc == -4 ? -1 : (rc <= -6 ? rc + 2 : rc)) : sync_status(rc);
 }
 int trevc_d_cols(const double *T, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
                  double *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
-    return trevc_impl<double>(T, ldt, m, cols_host, ncols, Z, ldz, scales, scale_exp, nb);
+    return sync_status(trevc_impl<double>(T, ldt, m, cols_host, ncols, Z, ldz, scales, scale_exp, nb));
 }
 int trevc_z_cols(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const int64_t *cols_host, int64_t ncols,
                  mstrsm_dcomplex *Z, int64_t ldz, double *scales, int32_t *scale_exp, int nb) {
-    return trevc_impl<cplx>((const cplx *)T, ldt, m, cols_host, ncols, (cplx *)Z, ldz, scales, scale_exp, nb);
+    return sync_status(trevc_impl<cplx>((const cplx *)T, ldt, m, cols_host, ncols, (cplx *)Z, ldz, scales, scale_exp, nb));
 }
 
 int spectral_cloud_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z, int64_t npts,
@@ -1266,14 +1401,14 @@ int spectral_portrait_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, int64_
 int mstrsm_d_side(int safe, mstrsm_side side, mstrsm_uplo uplo, const double *A, int64_t lda, int64_t m,
                   const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n, double *scales,
                   int32_t *scale_exp, int nb) {
-    return side_impl<double>(safe, int(side), int(uplo), A, lda, m, shifts, shift_stride, B, ldb, n, scales,
-                             scale_exp, nb);
+    return sync_status(side_impl<double>(safe, int(side), int(uplo), A, lda, m, shifts, shift_stride, B, ldb, n, scales,
+                             scale_exp, nb));
 }
 int mstrsm_z_side(int safe, mstrsm_side side, mstrsm_uplo uplo, const mstrsm_dcomplex *A, int64_t lda, int64_t m,
                   const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B, int64_t ldb, int64_t n,
                   double *scales, int32_t *scale_exp, int nb) {
-    return side_impl<cplx>(safe, int(side), int(uplo), (const cplx *)A, lda, m, (const cplx *)shifts, shift_stride,
-                           (cplx *)B, ldb, n, scales, scale_exp, nb);
+    return sync_status(side_impl<cplx>(safe, int(side), int(uplo), (const cplx *)A, lda, m, (const cplx *)shifts, shift_stride,
+                           (cplx *)B, ldb, n, scales, scale_exp, nb));
 }
 
 int eig_backtransform_d(const double *Q, int64_t ldq, int64_t m, const double *Z, int64_t ldz, int64_t n,
@@ -1286,11 +1421,11 @@ int eig_backtransform_z(const mstrsm_dcomplex *Q, int64_t ldq, int64_t m, const 
 }
 int trevc_qz_d(const double *T, int64_t ldt, int64_t m, const double *Q, int64_t ldq, double *X, int64_t ldx,
                double *scales, int32_t *scale_exp, int nb) {
-    return trevc_qz_impl<double>(T, ldt, m, Q, ldq, X, ldx, scales, scale_exp, nb);
+    return sync_status(trevc_qz_impl<double>(T, ldt, m, Q, ldq, X, ldx, scales, scale_exp, nb));
 }
 int trevc_qz_z(const mstrsm_dcomplex *T, int64_t ldt, int64_t m, const mstrsm_dcomplex *Q, int64_t ldq,
                mstrsm_dcomplex *X, int64_t ldx, double *scales, int32_t *scale_exp, int nb) {
-    return trevc_qz_impl<cplx>((const cplx *)T, ldt, m, (const cplx *)Q, ldq, (cplx *)X, ldx, scales, scale_exp, nb);
+    return sync_status(trevc_qz_impl<cplx>((const cplx *)T, ldt, m, (const cplx *)Q, ldq, (cplx *)X, ldx, scales, scale_exp, nb));
 }
 
 // Host <-> device copies of the triangles the TriangEig path reads and writes: only the upper
@@ -1421,26 +1556,26 @@ int trevc_z_host_batch(const mstrsm_dcomplex *const *T_host, int64_t ldt, int64_
 
 int mstrsm_d_gen(int safe, const double *U, int64_t ldu, const double *V, int64_t ldv, int64_t m,
                  const double *shifts, int64_t shift_stride, double *B, int64_t ldb, int64_t n,
-                 const int64_t *row_end_host, double *scales, int32_t *scale_exp, int nb) {
-    return mstrsm_gen_impl<double>(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end_host,
-                                   scales, scale_exp, nb);
+                 const int64_t *row_end, double *scales, int32_t *scale_exp, int nb) {
+    return sync_status(mstrsm_gen_impl<double>(safe, U, ldu, V, ldv, m, shifts, shift_stride, B, ldb, n, row_end,
+                                   scales, scale_exp, nb));
 }
 int mstrsm_z_gen(int safe, const mstrsm_dcomplex *U, int64_t ldu, const mstrsm_dcomplex *V, int64_t ldv,
                  int64_t m, const mstrsm_dcomplex *shifts, int64_t shift_stride, mstrsm_dcomplex *B,
-                 int64_t ldb, int64_t n, const int64_t *row_end_host, double *scales, int32_t *scale_exp,
+                 int64_t ldb, int64_t n, const int64_t *row_end, double *scales, int32_t *scale_exp,
                  int nb) {
-    return mstrsm_gen_impl<cplx>(safe, (const cplx *)U, ldu, (const cplx *)V, ldv, m, (const cplx *)shifts,
-                                 shift_stride, (cplx *)B, ldb, n, row_end_host, scales, scale_exp, nb);
+    return sync_status(mstrsm_gen_impl<cplx>(safe, (const cplx *)U, ldu, (const cplx *)V, ldv, m, (const cplx *)shifts,
+                                 shift_stride, (cplx *)B, ldb, n, row_end, scales, scale_exp, nb));
 }
 int tgevc_d(const double *T, int64_t ldt, const double *S, int64_t lds, int64_t m, double *Z, int64_t ldz,
             double *lambda, double *scales, int32_t *scale_exp, int nb) {
-    return tgevc_impl<double>(T, ldt, S, lds, m, Z, ldz, lambda, scales, scale_exp, nb);
+    return sync_status(tgevc_impl<double>(T, ldt, S, lds, m, Z, ldz, lambda, scales, scale_exp, nb));
 }
 int tgevc_z(const mstrsm_dcomplex *T, int64_t ldt, const mstrsm_dcomplex *S, int64_t lds, int64_t m,
             mstrsm_dcomplex *Z, int64_t ldz, mstrsm_dcomplex *lambda, double *scales, int32_t *scale_exp,
             int nb) {
-    return tgevc_impl<cplx>((const cplx *)T, ldt, (const cplx *)S, lds, m, (cplx *)Z, ldz, (cplx *)lambda,
-                            scales, scale_exp, nb);
+    return sync_status(tgevc_impl<cplx>((const cplx *)T, ldt, (const cplx *)S, lds, m, (cplx *)Z, ldz, (cplx *)lambda,
+                            scales, scale_exp, nb));
 }
 
 int pseudospectra_z(const mstrsm_dcomplex *U, int64_t ldu, int64_t m, const mstrsm_dcomplex *z, int64_t npts, int iters,
@@ -1472,6 +1607,11 @@ int mstrsm_status(void) {
     CK(cudaMemcpy(&h, g_flag, sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemset(g_flag, 0, sizeof(int)));
     return h ? 2 : 0;
+}
+
+int mstrsm_set_sync_status(int on) {
+    t_sync_status = on != 0;
+    return 0;
 }
 
 int64_t mstrsm_launch_count(int reset) {
@@ -1797,13 +1937,23 @@ int stream_upper(const T *Tm, int64_t ldt, int64_t m, int nb, int root, cudaStre
     const size_t es = sizeof(T), ndbl = es / 8;
     const int r = g_comm_r;
     const int64_t nblk = cdiv(m, nb);
-    std::vector<size_t> offs(size_t(nblk) + 1, 0);
-    for (int64_t b = 0; b < nblk; b++) {
-        const Blk bl = block_rows(0, m, nb, b);
-        offs[b + 1] = offs[b] + size_t(bl.hi) * size_t(bl.hi - bl.lo);
+    // One region per pair of blocks (2q, 2q+1) as blocked_solve pairs them: columns [lo_{2q+1},
+    // hi_{2q}), rows 0 .. hi_{2q} (ld = hi_{2q}), so that the pair's merged update sees both panels
+    // through one leading dimension; an unpaired last block has its own (ld = hi_b).  Panel b is
+    // columns [lo_b, hi_b) of its region: contiguous, sent as whole columns of ld rows (rows
+    // hi_b .. ld of the pair's upper panel lie below T's diagonal: never written, never read).
+    const int64_t nreg = (nblk + 1) / 2;
+    std::vector<size_t> roff(static_cast<size_t>(nreg) + 1, 0);
+    std::vector<int64_t> rld(static_cast<size_t>(nreg), 0), rc0(static_cast<size_t>(nreg), 0);
+    for (int64_t q = 0; q < nreg; q++) {
+        const Blk lo_blk = block_rows(0, m, nb, 2 * q);
+        const Blk hi_blk = block_rows(0, m, nb, 2 * q + 1 < nblk ? 2 * q + 1 : 2 * q);
+        rld[q] = lo_blk.hi;
+        rc0[q] = hi_blk.lo;
+        roff[q + 1] = roff[q] + size_t(rld[q]) * size_t(lo_blk.hi - hi_blk.lo);
     }
     T *pack = nullptr;
-    CK(cudaMallocAsync(&pack, offs[nblk] * es, g_stream));
+    CK(cudaMallocAsync(&pack, roff[nreg] * es, g_stream));
     *pack_out = pack;
     // MSTRSM_DIST_TEST_UNPACK=1 (testing on one GPU): root also solves from the broadcast buffer, so
     // the non-root path runs at nranks = 1
@@ -1825,21 +1975,22 @@ int stream_upper(const T *Tm, int64_t ldt, int64_t m, int nb, int root, cudaStre
     feed.delta = dbuf;
     feed.enqueue = [=](int64_t b) -> int {
         const Blk bl = block_rows(0, m, nb, b);
-        const int64_t rows = bl.hi, w = bl.hi - bl.lo;
+        const int64_t q = b / 2, ld = rld[q], w = bl.hi - bl.lo;
+        T *dst = pack + roff[q] + (bl.lo - rc0[q]) * ld;
         if (r == root)
-            CK(cudaMemcpy2DAsync(pack + offs[b], rows * es, Tm + bl.lo * ldt, ldt * es, rows * es, w,
-                                 cudaMemcpyDeviceToDevice, cs));
-        NCK(ncclBroadcast(pack + offs[b], pack + offs[b], size_t(rows) * w * ndbl, ncclDouble, root, g_comm, cs));
+            CK(cudaMemcpy2DAsync(dst, ld * es, Tm + bl.lo * ldt, ldt * es, bl.hi * es, w, cudaMemcpyDeviceToDevice,
+                                 cs));
+        NCK(ncclBroadcast(dst, dst, size_t(ld) * w * ndbl, ncclDouble, root, g_comm, cs));
         return 0;
     };
-    // every block reads only its own panel: a non-root rank solves straight from the broadcast
-    // buffer, panel b seen as a column-major matrix with leading dimension hi_b whose column lo_b
-    // is its first (no unpack, no second copy of T)
+    // a non-root rank solves straight from the broadcast buffer: block b sees its pair's region as
+    // a column-major matrix with leading dimension ld whose column rc0 is its first (no unpack, no
+    // second copy of T); a block reads only its own panel, a pair's merged update both of its panels
     if (from_pack)
         feed.view = [=](int64_t b, const void **ptr, int64_t *ld) {
-            const Blk bl = block_rows(0, m, nb, b);
-            *ptr = static_cast<const void *>(pack + offs[b] - bl.lo * bl.hi);
-            *ld = bl.hi;
+            const int64_t q = b / 2;
+            *ptr = static_cast<const void *>(pack + roff[q] - rc0[q] * rld[q]);
+            *ld = rld[q];
         };
     return 0;
 }

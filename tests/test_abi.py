@@ -133,3 +133,9 @@ def test_no_cpu_fallback_without_cuda():
     U = torch.from_numpy(np.eye(4))
     with pytest.raises(ms.MstrsmError):
         ms.solve(U, torch.zeros(1, dtype=torch.float64), torch.ones(4, 1, dtype=torch.float64))
+
+
+def test_sync_status_switch_needs_no_gpu():
+    lib = ctypes.CDLL(ms.LIB_PATH)
+    assert lib.mstrsm_set_sync_status(1) == 0
+    assert lib.mstrsm_set_sync_status(0) == 0

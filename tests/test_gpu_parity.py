@@ -163,6 +163,26 @@ def test_gpu_row_end(ms, sorted_):
         assert np.all(Xg[r[j]:, j] == 0)
 
 
+@pytest.mark.parametrize("sorted_", [True, False])
+def test_gpu_row_end_device_pointer(ms, sorted_):
+    """row_end as a device array (include/mstrsm.h): the same result, bit for bit, as
+    the host array, and parity with the oracle; out-of-range values are clamped to [0, m]."""
+    import torch
+    m, n, nb = 300, 70, 64
+    U = _well_conditioned(m, True, 9)
+    s = inputs.random_shifts(n, True, 10, radius=0.3)
+    B = inputs.random_rhs(m, n, True, 11)
+    r = np.random.default_rng(12).integers(-5, m + 20, n)
+    if sorted_:
+        r = np.sort(r)
+    Xh, _, eh = gpu_solve(ms, U, s, B, nb=nb, row_end=r)
+    Xd, _, ed = gpu_solve(ms, U, s, B, nb=nb, row_end=torch.from_numpy(r).cuda())
+    assert np.array_equal(Xh, Xd) and np.array_equal(eh, ed)
+    rc = np.clip(r, 0, m)
+    Xo, eo = oracle.mstrsm(U, s, B, nb=nb, row_end=rc)
+    assert_parity(Xd, ed, Xo, eo, what="row_end device")
+
+
 # ------------------------------------------------------------------------------- safety
 def test_gpu_adversarial_safety(ms):
     """finite, c in [0,1], ||x|| < Omega, backward error <= 64 m 2^-53 on the adversarial
@@ -191,6 +211,26 @@ def test_gpu_nonfinite_input_status(ms):
     gpu_solve(ms, U, np.zeros(2), np.ones((30, 2)), nb=8)
     assert ms.status() == 2
     assert ms.status() == 0          # cleared
+
+
+def test_gpu_nonfinite_input_sync_status(ms):
+    """mstrsm_set_sync_status(1): the call itself synchronises and returns code 2."""
+    U = _well_conditioned(30, True, 2)
+    U[4, 20] = complex(np.inf, 0)
+    ms.mstrsm_set_sync_status(1)
+    try:
+        with pytest.raises(ms.MstrsmError, match="returned 2"):
+            gpu_solve(ms, U, np.zeros(2, complex), np.ones((30, 2), complex), nb=8)
+        assert ms.status() == 0      # the call cleared the flag
+        gpu_solve(ms, _well_conditioned(30, True, 3), np.zeros(2, complex), np.ones((30, 2), complex), nb=8)
+        T = _well_conditioned(40, False, 4)
+        T[1, 30] = np.nan
+        with pytest.raises(ms.MstrsmError, match="returned 2"):
+            gpu_trevc(ms, T, 16)
+    finally:
+        ms.mstrsm_set_sync_status(0)
+    gpu_solve(ms, U, np.zeros(2, complex), np.ones((30, 2), complex), nb=8)   # asynchronous again
+    assert ms.status() == 2
 
 
 # ------------------------------------------------------------------------------- eigenvectors
