@@ -387,9 +387,13 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
             if constexpr (ST::cplx_) gub = __dmul_ru(gub, 1.4142135623730951);
             guarded = active && !(okM && carry < kOmega);
             if (__any_sync(0xffffffffu, guarded)) {                        // g := ||y(I1)||_inf
+                if constexpr (ST::cplx_) {
+                    g0 = modv_max(y, RPL);                                 // (rows >= nrow hold 0)
+                } else {
 #pragma unroll
-                for (int t = 0; t < RPL; t++)
-                    if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
+                    for (int t = 0; t < RPL; t++)
+                        if (rl + LPC * t < nrow) g0 = fmax(g0, modv(y[t]));
+                }
                 g0 = group_max<LPC>(g0);
             }
             if (rl == 0) {                                                 // the replay's inputs
@@ -420,8 +424,12 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
                     Gj = mulp2n(Gj, kt);
                 }
                 double xm = 0.0;
+                if constexpr (ST::cplx_) {
+                    xm = modv_max(y, RPL);
+                } else {
 #pragma unroll
-                for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
+                    for (int t = 0; t < RPL; t++) xm = fmax(xm, modv(y[t]));
+                }
                 xm = group_max<LPC>(xm);
                 Gj = __dadd_rn(Gj, __dmul_rn(Pb, xm));
                 int k3 = 0;

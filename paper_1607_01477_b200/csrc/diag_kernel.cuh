@@ -190,6 +190,30 @@ __device__ __forceinline__ double modv(cplx a) {
     y = __dmul_rn(y, s);
     return __dmul_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y))), si);
 }
+// max_t modv(y[t]) (t < n, the others ignored), bit for bit, with one square root: for components
+// in [2^-500, 2^500) modv is sqrt_rn(x^2 + y^2) (no prescale), a monotone function of the rounded
+// sum, so the largest sum gives the largest modulus (non-negative doubles order like their bits);
+// zeros add nothing; any other element takes modv itself.
+template <int N>
+__device__ __forceinline__ double modv_max(const cplx (&y)[N], int n_live) {
+    long long qb = -1;
+    double other = 0.0;
+#pragma unroll
+    for (int t = 0; t < N; t++) {
+        if (t < n_live) {
+            const unsigned hx = unsigned(__double2hiint(y[t].x)) & 0x7fffffffu;
+            const unsigned hy = unsigned(__double2hiint(y[t].y)) & 0x7fffffffu;
+            const unsigned hb = max(hx, hy);
+            if ((hb >> 20) - 523u <= 999u) {
+                const double q = __dadd_rn(__dmul_rn(y[t].x, y[t].x), __dmul_rn(y[t].y, y[t].y));
+                qb = max(qb, __double_as_longlong(q));
+            } else if ((hb | unsigned(__double2loint(y[t].x)) | unsigned(__double2loint(y[t].y))) != 0u) {
+                other = fmax(other, modv(y[t]));
+            }
+        }
+    }
+    return qb >= 0 ? fmax(__dsqrt_rn(__longlong_as_double(qb)), other) : other;
+}
 
 // R2's minpow2(a, L) (smallest k >= 1 with 2^-k a < L) for positive a >= L from the exponent and
 // mantissa bits: 2^-k a < L  <=>  k > e_a - e_L, or k = e_a - e_L with mant(a) < mant(L).
@@ -250,20 +274,22 @@ template <> struct Piv<double> {
 template <> struct Piv<cplx> {
     cplx r;
     __device__ __forceinline__ void make(cplx dd) {
-        double big = fmax(fabs(dd.x), fabs(dd.y));
-        if (!(big > 0.0 && big <= 1.7976931348623157e308)) {          // 0 or non-finite pivot
+        // (range tests on the exponent bits: FP64 compares would issue on the FP64 pipe)
+        const unsigned hx = unsigned(__double2hiint(dd.x)) & 0x7fffffffu, hy = unsigned(__double2hiint(dd.y)) & 0x7fffffffu;
+        const bool zx = (hx | unsigned(__double2loint(dd.x))) == 0u, zy = (hy | unsigned(__double2loint(dd.y))) == 0u;
+        if ((zx && zy) || max(hx, hy) >= 0x7ff00000u) {               // 0 or non-finite pivot
             r = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
             return;
         }
-        // Fast path: components 0 or in [2^-250, 2^250] keep every intermediate below normal --
+        // Fast path: components 0 or in [2^-250, 2^250) keep every intermediate below normal --
         // scaling by a power of two commutes with each rounded step, so this is bit for bit the
         // prescaled computation below
-        const double ax = fabs(dd.x), ay = fabs(dd.y);
-        if ((ax == 0.0 || (ax >= 0x1p-250 && ax <= 0x1p+250)) && (ay == 0.0 || (ay >= 0x1p-250 && ay <= 0x1p+250))) {
+        if ((zx || (hx >> 20) - 773u <= 499u) && (zy || (hy >> 20) - 773u <= 499u)) {
             const double inv = __drcp_rn(fma(dd.x, dd.x, __dmul_rn(dd.y, dd.y)));
             r = make_double2(__dmul_rn(dd.x, inv), -__dmul_rn(dd.y, inv));
             return;
         }
+        const double big = fmax(fabs(dd.x), fabs(dd.y));
         int e;
         long long mnt;
         exp_mant(big, e, mnt);

@@ -71,14 +71,16 @@ static int gemm_3p_phase() {
 // (c4, the generalized solve: per-tile overheads of the smaller 32-row tiles) and at large K (the
 // back-transformation: the 48-row tile re-reads X less); DESIGN.md §7.2.
 // MSTRSM_3M_GROUPS=2|3 forces one.
-static int gemm_3m_groups(int K) {
+// A short update (M <= 64 rows: the next block's rows in the paired-block solve) takes the three
+// groups' 32-row tiles whatever K: 48-row tiles would pad M = 64 to 96.
+static int gemm_3m_groups(int K, int64_t M) {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MSTRSM_3M_GROUPS");
         v = (e && !strcmp(e, "2")) ? 2 : (e && !strcmp(e, "3")) ? 3 : 0;
     }
     if (v) return v;
-    return (K >= 96 && K <= 256) ? 3 : 2;
+    return ((K >= 96 && K <= 256) || M <= 64) ? 3 : 2;
 }
 
 static bool use_classic() { return gemm_variant() == 1; }
@@ -109,7 +111,7 @@ int launch_gemm(const GemmArgs<T> &g) {
                 !encode_2d(&tmXs, g.Xsum + g.col0 * g.ldxs, uint64_t(g.K), uint64_t(g.N), uint64_t(g.ldxs), k3mBK,
                            k3mBN, CU_TENSOR_MAP_SWIZZLE_64B))
                 return set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (3M update operands)");
-            const bool q3 = gemm_3m_groups(g.K) == 3;
+            const bool q3 = gemm_3m_groups(g.K, g.M) == 3;
             const uint32_t bm = q3 ? k3qBM : k3mBM;
             if (OPC) {
                 if (!encode_2d(&tmA, g.U + g.a_r0 + g.a_c0 * g.ldu, uint64_t(2 * g.K), uint64_t(g.M),
