@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
     // ---- stage U(I1,I1) as the padded triangle (solve coordinates), its diagonal and cnl.  U and
     //      cnl are never written during a solve, so a launch after the solve's first one stages
     //      them before waiting for the preceding grid (a.early) ----
+    pdl_trigger();
     if (!a.early) pdl_wait();
     for (int cq = tid >> 5; cq < nfull; cq += nth >> 5) {                 // a warp per column of U,
         for (int r = tid & 31; r < cq; r += 32) {                           // lanes down its rows

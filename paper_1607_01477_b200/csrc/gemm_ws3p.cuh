@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws3p_kernel(GemmArgs<cplx>
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    pdl_trigger();
     pdl_wait();
 
     if (warp < 4) {

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
         s_go = (phase && nk > 0) ? 0 : NG;    // (K = 0: no k-tile would release the others)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    pdl_trigger();
     __syncthreads();
     pdl_wait();
 
