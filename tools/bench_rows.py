@@ -12,6 +12,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -125,14 +126,35 @@ def main():
                          "f2: back-transformation X = Q Z alone, complex m=8192 (SURVEY §8f f2)")
         work["f2"] = (lambda: ms.trevc_qz(Tq, Qq, nb=128), eig_flops(mq, True) + bt_flops, mq, "eigvecs/s",
                       "f2: TriangEig + back-transformation (Eig's last two steps), complex m=8192, n_b=128")
+    if "graph" in a.only:
+        # the same c1 / c2 calls captured once into a CUDA graph and replayed (launch overhead and
+        # inter-kernel gaps on the device side; the library's launches are stream-capturable)
+        for nm in ("c1", "c2"):
+            if nm not in work:
+                continue
+            fn0, flops0, units0, uname0, desc0 = work[nm]
+            for _ in range(2):
+                fn0()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s_cap = torch.cuda.Stream()
+            s_cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_cap):
+                with torch.cuda.graph(g, stream=s_cap):
+                    fn0()
+            torch.cuda.current_stream().wait_stream(s_cap)
+            torch.cuda.synchronize()
+            work[nm + "_graph"] = (lambda g_=g: g_.replay(), flops0, units0, uname0, desc0 + " (CUDA graph replay)")
     for name, (fn, flops, units, uname, desc) in work.items():
         for _ in range(a.warmup):
             fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        t0 = time.perf_counter()
         for _ in range(a.steps):
             fn()
+        t_host = (time.perf_counter() - t0) * 1e3 / a.steps    # host time to enqueue one step
         e1.record()
         torch.cuda.synchronize()
         ms_step = e0.elapsed_time(e1) / a.steps
@@ -146,8 +168,11 @@ def main():
                           "gflops_algorithmic": flops / (ms_step * 1e-3) / 1e9,
                           uname: units / (ms_step * 1e-3), "steps": a.steps, "warmup": a.warmup,
                           "gemm_ms_profiled_step": gm, "diag_ms_profiled_step": dm,
+                          "host_enqueue_ms_per_step": t_host,
                           "timing": "CUDA events around the timed steps (no per-launch events); the "
-                                    "per-kind split comes from one extra step with per-launch events"}),
+                                    "per-kind split comes from one extra step with per-launch events; "
+                                    "host_enqueue_ms_per_step = wall time of the host calls alone (below "
+                                    "ms_per_step: the host stays ahead, launch overhead is hidden)"}),
               flush=True)
 
 
