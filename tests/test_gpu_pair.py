@@ -111,3 +111,49 @@ print(json.dumps({{"worst": worst}}))
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert json.loads(out.stdout.strip().splitlines()[-1])["worst"] <= 1e-9
+
+
+def test_adversarial_suite_with_paired_blocks():
+    """S:228 safety properties (finite, e <= 0, ||x|| < Omega, c in [0,1], backward error <=
+    64 m 2^-53) on the adversarial suite (Jordan blocks, exact zero pivots, graded 10^+-300,
+    repeated eigenvalues, tiny pivots with strong coupling) with paired blocks forced
+    (MSTRSM_PAIR=2, even n_b), real and complex (the suite's matrices rotated by a unit phase)."""
+    script = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1607_01477_b200 as ms
+from tests.test_oracle_pins import _adversarial_suite
+from tests import refmath as R
+worst, bad = 0.0, []
+for i, (U, s, B, nb) in enumerate(_adversarial_suite()):
+    nb = 2 * ((nb + 1) // 2)                                 # even: paired
+    for cp in (False, True):
+        Uc, sc_, Bc = (U, s, B) if not cp else (U * np.exp(0.3j), s * np.exp(0.3j), B * (1 + 0.5j))
+        m = Uc.shape[0]
+        X, sc, e = ms.solve(torch.from_numpy(np.asfortranarray(Uc)).cuda(),
+                            torch.from_numpy(np.ascontiguousarray(sc_)).cuda(),
+                            torch.from_numpy(np.asfortranarray(Bc)).cuda(), safe=True, nb=nb)
+        torch.cuda.synchronize()
+        X, sc, e = X.cpu().numpy(), sc.cpu().numpy(), e.cpu().numpy()
+        ok = np.all(np.isfinite(X)) and np.all(e <= 0) and np.max(np.abs(X)) < R.OMEGA and np.all((sc >= 0) & (sc <= 1))
+        unorm = np.max(np.sum(np.abs(np.triu(Uc)), axis=1))
+        delta = np.ldexp(unorm, -52) if unorm > 0 else np.finfo(float).tiny
+        for j in range(len(sc_)):
+            dd = np.diag(Uc) - sc_[j]
+            if np.any((dd == 0) & (delta + sc_[j] - sc_[j] != delta)):
+                continue
+            Ud = np.triu(Uc).copy()
+            Ud[np.arange(m), np.arange(m)] = np.where(dd == 0, delta + sc_[j], np.diag(Uc))
+            rr = float(R.residual_ratio(Ud, sc_[j], X[:, j], e[j], Bc[:, j]))
+            worst = max(worst, rr / (64 * m * 2.0 ** -53))
+        if not ok:
+            bad.append((i, cp))
+print(json.dumps({{"worst": worst, "bad": bad}}))
+"""
+    env = dict(os.environ, MSTRSM_PAIR="2")
+    out = subprocess.run([sys.executable, "-c", script.format(root=ROOT)], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert not r["bad"] and r["worst"] <= 1.0, r
