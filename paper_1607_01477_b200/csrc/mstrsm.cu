@@ -173,7 +173,10 @@ thread_local const std::function<int(int64_t)> *t_after_diag = nullptr;
 thread_local const double *t_panel_part = nullptr;
 
 // ---------------------------------------------------------------- look-ahead (op N, safe)
-// Look-ahead (default; MSTRSM_LOOKAHEAD=0 disables): block b's update is split into its top n_b rows (the next diagonal block,
+// Look-ahead (MSTRSM_LOOKAHEAD=1 enables; off by default since round 2's diagonal kernels: c3 22.2
+// ms without vs 22.3 with, the 8-GPU shard 25.2 vs 25.6, c5 equal -- profiles/r02/exp_la_r02.txt,
+// the diagonal step is now short enough that confining it to a few SMs costs what the overlap
+// saves): block b's update is split into its top n_b rows (the next diagonal block,
 // on the library stream) and the rest (on a side stream, on fewer SMs), so that the next
 // diagonal step -- latency-bound, and the per-block floor of a multi-GPU shard -- runs on the
 // SMs the rest leaves free.  dblk and the X+ plane are double-buffered by block
@@ -184,7 +187,7 @@ bool lookahead_enabled() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MSTRSM_LOOKAHEAD");
-        v = (e && !strcmp(e, "0")) ? 0 : 1;
+        v = (e && !strcmp(e, "1")) ? 1 : 0;
     }
     return v == 1;
 }
@@ -396,7 +399,9 @@ int blocked_solve_la(const T *U, int64_t ldu, int64_t m, const T *shifts, int64_
         const auto &re = *rowend_sorted_host;
         return std::upper_bound(re.begin(), re.end(), bl.lo) - re.begin();
     };
-    constexpr int kColsPerCta = 48;            // RPL = 16 layout: 12 warps x 4 columns
+    // columns one CTA of the next diagonal step covers in one pass: the n_b > 64 complex layout
+    // (16, 8) has 15 substitution warps of 2 columns (diag_launch.cuh); MSTRSM_LA_COLS overrides
+    static const int kColsPerCta = [] { const char *e = getenv("MSTRSM_LA_COLS"); const int v = e ? atoi(e) : 0; return v > 0 ? v : 30; }();
     const int cap_max = g_num_sms / 3;
     bool rest_pending = false;
     int diag_cap = 0;                          // CTAs the next diagonal step may use (0: all)

@@ -59,7 +59,7 @@ VARIANTS = {
     "three_groups_no_stagger": {"MSTRSM_3M_GROUPS": "3", "MSTRSM_3P_PHASE": "0"},
     "three_groups_stagger1": {"MSTRSM_3M_GROUPS": "3", "MSTRSM_3P_PHASE": "1"},
     "diag_unbalanced": {"MSTRSM_DIAG_BALANCE": "0"},
-    "no_lookahead": {"MSTRSM_LOOKAHEAD": "0"},
+    "lookahead": {"MSTRSM_LOOKAHEAD": "1"},
 }
 
 
