@@ -147,6 +147,22 @@ __host__ __device__ __forceinline__ Blk block_rows(int op, int64_t m, int nb, in
 namespace mstrsm {
 // Programmatic dependent launch: wait for the preceding grid in the stream (a no-op when the
 // kernel was launched without the attribute).
+// Phase timing of the diagonal kernels (experiment builds only, -DMSTRSM_PHASE_TIMES,
+// tools/build_phase.sh): PT_MARK(pt, k) stores clock64() in slot k of this CTA's row of pt (16
+// slots per CTA, pass 0); slots 0 / 15 hold %globaltimer at entry / exit.
+#ifdef MSTRSM_PHASE_TIMES
+__device__ __forceinline__ long long pt_gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PT_MARK(pt, k, cond)                                                          \
+    do {                                                                              \
+        if ((pt) && (cond)) (pt)[blockIdx.x * 16 + (k)] = ((k) == 0 || (k) == 15) ? pt_gtime() : clock64(); \
+    } while (0)
+#else
+#define PT_MARK(pt, k, cond) do { } while (0)
+#endif
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 // ... and let the next grid in the stream launch now (onto the SMs this grid leaves free) rather
 // than when this one completes.  Its griddepcontrol.wait still waits for this grid's completion and

@@ -57,9 +57,9 @@ __host__ __device__ inline int diagw_nrep(int nsub, int lpc, bool safe) { return
 
 // Shared-memory carve-up (byte offsets, 16-aligned): padded triangle, diagonal, cnl, and for the
 // safe variants the replay records |x| (row-major: [sc][column slot]), the chunk frames, the
-// per-column g0 / live row count / K, and RPL + 1 mbarriers.
+// per-column g0 / live row count / K / G_j and e_j as read at the pass start, and RPL + 1 mbarriers.
 struct DiagWSmem {
-    int64_t pk, dg, cn, rec, fp, g0, lrows, kout, bar, total;
+    int64_t pk, dg, cn, rec, fp, g0, lrows, kout, gj, ej, bar, total;
 };
 __host__ __device__ inline DiagWSmem diagw_smem(int nfull, int lpc, int rpl, int esize, int ncol_cta, bool safe) {
     auto al = [](int64_t v) { return (v + 15) & ~int64_t(15); };
@@ -73,7 +73,9 @@ __host__ __device__ inline DiagWSmem diagw_smem(int nfull, int lpc, int rpl, int
     s.g0 = al(s.fp + int64_t(rpl) * ncol_cta * 4);
     s.lrows = al(s.g0 + int64_t(ncol_cta) * 8);
     s.kout = al(s.lrows + int64_t(ncol_cta) * 4);
-    s.bar = al(s.kout + int64_t(ncol_cta) * 4);
+    s.gj = al(s.kout + int64_t(ncol_cta) * 4);
+    s.ej = al(s.gj + int64_t(ncol_cta) * 8);
+    s.bar = al(s.ej + int64_t(ncol_cta) * 4);
     s.total = s.bar + int64_t(rpl + 1) * 8;
     return s;
 }
@@ -97,6 +99,61 @@ __device__ __forceinline__ void scale_pow2(T (&y)[N], int s) {
     } else {
         scale_all_any(y, s);
     }
+}
+
+// Alg. 4's decisions for one chunk of NR rows (solve rows sc0 + NR - 1 .. sc0) of one column: the
+// replay warps' per-row chain in the paper's frame |x_l| = ax 2^(Fp - K) (R27), with
+// ax = rec[sc * ldrec + c] recorded by the substitution warps.  Rows sc >= lrows are not live
+// (M = 0, k1 = k2 = 0: g * 1 + 0).  cn is read at sc (0 for sc >= ncn).
+template <int NR>
+__device__ __forceinline__ void replay_chunk(const double *rec, int ldrec, int c, int sc0, int lrows, int Fp,
+                                             const double *cn, int ncn, double &g, int &K) {
+    // Short form of the common row (no t1, frame offset dK = Fp - K in the normal range, so
+    // k1 = 0 and g 2^-k1 = g exactly): gn = g + (ax 2^dK) cnl, with 2^dK kept across rows; the
+    // general form below is the row as written out in full.  Both compute the same values.
+    int dK = Fp - K;
+    double p2 = pow2i(dK);
+    const double *rp = rec + (sc0 + NR - 1) * ldrec + c;
+#pragma unroll 4
+    for (int rr = NR - 1; rr >= 0; rr--, rp -= ldrec) {
+        const int sc = sc0 + rr;
+        const bool live = sc < lrows;
+        const double ax = live ? *rp : 0.0;
+        const double cr = cn[sc < ncn ? sc : 0];
+        const int ea = bexp(ax);
+        const int ep = ea + dK;                           // biased exponent, paper frame
+        const bool t1 = live && ea != 0 && ep >= 1993;    // |x_l| >= 2^970
+        double gn;
+        if (!t1 && unsigned(dK + 1022) <= 2045u) {
+            gn = __dadd_rn(g, __dmul_rn(live ? __dmul_rn(ax, p2) : 0.0, cr));
+        } else {
+            const int k1 = t1 ? ep - 1992 : 0;
+            double M, gs;
+            if (unsigned(dK + 1022) <= 2045u && k1 <= 1022) {
+                M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
+                gs = __dmul_rn(g, pow2i(-k1));                // P:287 applied to g
+            } else {                                          // extreme frames (rare)
+                M = t1 ? with_bexp(ax, 1992) : mulp2_any(ax, dK);
+                gs = mulp2n(g, k1);
+            }
+            M = live ? M : 0.0;
+            gn = __dadd_rn(gs, __dmul_rn(M, cr));
+            K += k1;
+        }
+        const bool t2 = live && gn >= kOmega;
+        const int k2 = t2 ? bexp(gn) - 1992 : 0;
+        g = __dmul_rn(gn, pow2i(-k2));
+        K += k2;
+        dK = Fp - K;
+        p2 = pow2i(dK);
+    }
+}
+
+// An upper bound of 1/v for the prechecks (v >= 0): the correctly rounded reciprocal raised by one
+// ulp and by the smallest subnormal (its error is below both), rounded up; inf for v = 0, NaN for
+// NaN.  Cheaper than __drcp_ru (no called slow path).
+__device__ __forceinline__ double rcp_up(double v) {
+    return __dadd_ru(__dmul_ru(__drcp_rn(v), 1.0 + 0x1p-52), 0x1p-1074);
 }
 
 template <int LPC>
@@ -231,6 +288,8 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
     double *s_g0 = reinterpret_cast<double *>(smem_raw + L.g0);
     int *s_lrows = reinterpret_cast<int *>(smem_raw + L.lrows);
     int *s_k = reinterpret_cast<int *>(smem_raw + L.kout);
+    double *s_gj = reinterpret_cast<double *>(smem_raw + L.gj);
+    int *s_ej = reinterpret_cast<int *>(smem_raw + L.ej);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar);   // [0, RPL): chunks, [RPL]: done
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -239,6 +298,8 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
     //      cnl are never written during a solve, so a launch after the solve's first one stages
     //      them before waiting for the preceding grid (a.early) ----
     pdl_trigger();
+    PT_MARK(a.pt, 0, tid == 0);
+    PT_MARK(a.pt, 1, tid == 0);
     if (!a.early) pdl_wait();
     for (int cq = tid >> 5; cq < nfull; cq += nth >> 5) {                 // a warp per column of U,
         for (int r = tid & 31; r < cq; r += 32) {                           // lanes down its rows
@@ -266,6 +327,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
     cp_async_commit();
     if (a.early) pdl_wait();
     __syncthreads();                                                       // diagonal, cnl, barriers
+    PT_MARK(a.pt, 2, tid == 0);
     bool staged = false;
     auto stage_wait = [&]() { cp_async_wait<0>(); __syncthreads(); staged = true; };
 
@@ -274,6 +336,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
         // =========================== replay warp: one lane per column slot ===========================
         if constexpr (SAFE) {
             stage_wait();
+            PT_MARK(a.pt, 10, warp == nsub && lane == 0);
             const int c = (warp - nsub) * 32 + lane;
             int pass = 0;
             for (int64_t cb = int64_t(blockIdx.x) * C; cb < ncols; cb += cstride, pass++) {
@@ -286,35 +349,10 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
                     if (t == RPL - 1 && c < C) { g = s_g0[c]; lrows = s_lrows[c]; }
                     if (!__any_sync(0xffffffffu, lrows > t * LPC)) continue;
                     const int Fp = lrows > t * LPC ? s_fp[t * C + c] : 0;
-#pragma unroll 4
-                    for (int rr = LPC - 1; rr >= 0; rr--) {
-                        const int sc = t * LPC + rr;
-                        const bool live = sc < lrows;
-                        const double ax = live ? s_rec[sc * C + c] : 0.0;
-                        // paper frame |x_l| = ax 2^(Fp - K); a row that is not live leaves g and K
-                        // unchanged exactly (M = 0, k1 = k2 = 0: g * 1 + 0)
-                        const int ea = bexp(ax);
-                        const int dK = Fp - K;
-                        const int ep = ea + dK;                           // biased exponent, paper frame
-                        const bool t1 = live && ea != 0 && ep >= 1993;    // |x_l| >= 2^970
-                        const int k1 = t1 ? ep - 1992 : 0;
-                        double M, gs;
-                        if (unsigned(dK + 1022) <= 2045u && k1 <= 1022) {
-                            M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
-                            gs = __dmul_rn(g, pow2i(-k1));                // P:287 applied to g
-                        } else {                                          // extreme frames (rare)
-                            M = t1 ? with_bexp(ax, 1992) : mulp2_any(ax, dK);
-                            gs = mulp2n(g, k1);
-                        }
-                        M = live ? M : 0.0;
-                        double gn = __dadd_rn(gs, __dmul_rn(M, cn[sc < nfull ? sc : 0]));
-                        const bool t2 = live && gn >= kOmega;
-                        const int k2 = t2 ? bexp(gn) - 1992 : 0;
-                        g = __dmul_rn(gn, pow2i(-k2));
-                        K += k1 + k2;
-                    }
+                    replay_chunk<LPC>(s_rec, C, c, t * LPC, lrows, Fp, cn, nfull, g, K);
                 }
                 if (c < C) s_k[c] = K;
+                PT_MARK(a.pt, 11, warp == nsub && lane == 0 && pass == 0);
                 dw_mbar_arrive(bars + RPL);
             }
         }
@@ -332,17 +370,24 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
         const int64_t q = cb + c;
         const bool valid = q < ncols;
         const int64_t j = a.c0 + (valid ? q : 0);
+        // the pass's column loads (shift, G_j, e_j) issue together, before the row end is known
+        T *x = a.B + j * a.ldb;
+        auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
+        T sh = valid ? a.shifts[j * a.sstride] : ST::zero();
+        const double Gj0 = (SAFE && valid) ? a.G[j] : 0.0;
         const int64_t r = valid ? ((OP == 0 && a.rowend) ? a.rowend[j] : a.m) : 0;
         const bool active = valid && r > a.lo;
         if (SAFE && valid && !active && rl == 0) a.dblk[j] = 0;           // inactive column: no rescale
+        if (SAFE && rl == 0) {                                             // (kept for the finish)
+            s_gj[c] = Gj0;
+            s_ej[c] = valid ? a.e[j] : 0;
+        }
         const int nrow = active ? (OP == 0 ? int((a.hi < r ? a.hi : r) - a.lo) : nfull) : 0;
         int nmax = nrow;
 #pragma unroll
         for (int o = LPC; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-        T sh = active ? a.shifts[j * a.sstride] : ST::zero();
+        if (!active) sh = ST::zero();
         if (OP == 1) sh = ST::conj(sh);
-        T *x = a.B + j * a.ldb;
-        auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
         auto pivot = [&](int sc) -> T {                                    // d_l = U(l,l) - s_j
             T dd = sc < nrow ? ST::sub(dg[sc], sh) : ST::real(1.0);
             if (SAFE && ST::is_zero(dd)) dd = ST::real(delta);
@@ -354,6 +399,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
             const int sc = rl + LPC * t;
             y[t] = sc < nrow ? x[rowof(sc)] : ST::zero();
         }
+        PT_MARK(a.pt, 3, tid == 0 && pass == 0);
 
         bool guarded = false;
         double g0 = 0.0, gub = 0.0;
@@ -367,7 +413,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
             for (int t = 0; t < RPL; t++) {
                 const int sc = rl + LPC * t;
                 if (sc < nrow) {
-                    const double inv = __drcp_ru(maxabs(pivot(sc)));       // >= 1/|d_l|
+                    const double inv = rcp_up(maxabs(pivot(sc)));         // >= 1/|d_l|
                     prod = __dmul_ru(prod, __dadd_ru(1.0, __dmul_ru(cn[sc], inv)));
                     minv = fmax(minv, inv);
                 }
@@ -377,7 +423,7 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
                 prod = __dmul_ru(prod, __shfl_xor_sync(0xffffffffu, prod, o, LPC));
                 minv = fmax(minv, __shfl_xor_sync(0xffffffffu, minv, o, LPC));
             }
-            const double gtop = active ? __dmul_ru(a.G[j], 1.0 + 0x1p-40) : 0.0;   // >= ||y(I1)||_inf
+            const double gtop = active ? __dmul_ru(Gj0, 1.0 + 0x1p-40) : 0.0;      // >= ||y(I1)||_inf
             const double carry = __dmul_ru(gtop, prod);
             const bool okM = __dmul_ru(carry, minv) < kOmega;
             // initial frame bound for the guarded loop: the registers' largest |y| (upper bound)
@@ -403,7 +449,9 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
             }
         }
 
+        PT_MARK(a.pt, 4, tid == 0 && pass == 0);
         if (!staged) stage_wait();
+        PT_MARK(a.pt, 5, tid == 0 && pass == 0);
         int F = 0;
         bool failed = false;
         if (SAFE && __any_sync(0xffffffffu, guarded)) {
@@ -414,12 +462,13 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
             diagw_rows<T, LPC, RPL, SAFE, false, OP == 1>(y, pivot, pk, rl, nmax, false, 0.0, s_rec + c, s_fp + c,
                                                           C, bars, F);
         }
+        PT_MARK(a.pt, 6, tid == 0 && pass == 0);
         // steps (ii) and (iii) of Alg. 5 and the stores, for the groups with `keep`
         auto finish = [&](int kt, bool keep) {
             if (SAFE) {
                 int ej = 0;
                 double Gj = 0.0;
-                if (active) { ej = a.e[j]; Gj = a.G[j]; }
+                if (active) { ej = s_ej[c]; Gj = s_gj[c]; }
                 if (kt > 0) {                                              // P:376-386, step (ii)
                     ej -= kt;
                     Gj = mulp2n(Gj, kt);
@@ -468,9 +517,11 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
         if (SAFE) {
             dw_mbar_wait(bars + RPL, pass & 1);                            // K from the replay warp
             kt = s_k[c];
+            PT_MARK(a.pt, 7, tid == 0 && pass == 0);
             if (!failed && F != kt) scale_pow2(y, F - kt);                 // to the paper's frame
         }
         finish(kt, !failed);
+        PT_MARK(a.pt, 8, tid == 0 && pass == 0);
         if (SAFE && __any_sync(0xffffffffu, failed)) {
             // a group whose values stopped being finite (tiny pivots: growth beyond the frame's
             // headroom inside one chunk) is rerun from its inputs by the synchronous guarded loop,
@@ -497,6 +548,8 @@ __global__ void __launch_bounds__(DiagW<T, LPC, RPL, SAFE>::kThreads, 1) diagw_k
         }
     }
     if (!staged) stage_wait();
+    PT_MARK(a.pt, 9, tid == 0);
+    PT_MARK(a.pt, 15, tid == 0);
 }
 
 }  // namespace mstrsm

@@ -61,6 +61,7 @@ struct DiagArgs {
     // exponent deltas to dprev; xsprev = p's X+ rows (ld ldxs, complex 3M only)
     const int *dprev; int64_t c0prev, plo, phi, bprev;
     double *xsprev;
+    long long *pt;                 // phase times (MSTRSM_PHASE_TIMES builds only; nullable)
 };
 
 template <typename T> struct DiagArgs;

@@ -143,6 +143,9 @@ int launch_diagf_k(const DiagArgs<T> &a0) {
     if (grid < 1) grid = 1;
     DiagArgs<T> a = a0;
     a.nsub = nsub;
+#ifdef MSTRSM_PHASE_TIMES
+    a.pt = phase_next();
+#endif
     const double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
     ProfScope ps(PK_DIAG, fl);
     CK(launch_k(kern, dim3(grid), dim3(threads), smem, g_stream, a));
@@ -218,6 +221,9 @@ int launch_diagl(const DiagArgs<T> &a0) {
     if (grid < 1) grid = 1;
     DiagArgs<T> a = a0;
     a.nsub = nsub;
+#ifdef MSTRSM_PHASE_TIMES
+    a.pt = phase_next();
+#endif
     const double fl = double(a.ncols) * nfull * (nfull - 1) / 2.0 * (S<T>::cplx_ ? 8.0 : 2.0);
     ProfScope ps(PK_DIAG, fl);
     CK(launch_k(kern, dim3(grid), dim3(threads), smem, g_stream, a));

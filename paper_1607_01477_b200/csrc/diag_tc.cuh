@@ -115,6 +115,8 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
     double *s_g0 = reinterpret_cast<double *>(smem_raw + L.g0);
     int *s_lrows = reinterpret_cast<int *>(smem_raw + L.lrows);
     int *s_k = reinterpret_cast<int *>(smem_raw + L.kout);
+    double *s_gj = reinterpret_cast<double *>(smem_raw + L.gj);
+    int *s_ej = reinterpret_cast<int *>(smem_raw + L.ej);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar);   // [0, NT): tiles, [NT]: done
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -122,6 +124,8 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
     // ---- stage U(I1,I1) as the padded triangle with 8-row chunks (solve coordinates; columns
     //      nfull .. npad-1 all zero), its diagonal (1 past nfull) and cnl (0 past nfull).  U and
     //      cnl are never written during a solve: launches after the first stage before the wait ----
+    PT_MARK(a.pt, 0, tid == 0);
+    PT_MARK(a.pt, 1, tid == 0);
     if (!a.early) pdl_wait();
     for (int cq = tid >> 5; cq < nfull; cq += nth >> 5) {                 // a warp per column of U,
         for (int r = tid & 31; r < cq; r += 32) {                           // lanes down its rows
@@ -158,6 +162,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
     cp_async_commit();
     if (a.early) pdl_wait();
     __syncthreads();                                                       // diagonal, cnl, barriers
+    PT_MARK(a.pt, 2, tid == 0);
     bool staged = false;
     auto stage_wait = [&]() { cp_async_wait<0>(); __syncthreads(); staged = true; };
 
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         // =========================== replay warp: one lane per column slot ===========================
         if constexpr (SAFE) {
             stage_wait();
+            PT_MARK(a.pt, 10, warp == nsub && lane == 0);
             const int c = (warp - nsub) * 32 + lane;
             int pass = 0;
             for (int64_t cb = int64_t(blockIdx.x) * C; cb < ncols; cb += cstride, pass++) {
@@ -178,35 +184,10 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                     if (t == NT - 1 && c < C) { g = s_g0[c]; lrows = s_lrows[c]; }
                     if (!__any_sync(0xffffffffu, lrows > t * TR)) continue;
                     const int Fp = lrows > t * TR ? s_fp[t * C + c] : 0;
-#pragma unroll 4
-                    for (int rr = TR - 1; rr >= 0; rr--) {
-                        const int sc = t * TR + rr;
-                        const bool live = sc < lrows;
-                        const double ax = live ? s_rec[sc * C + c] : 0.0;
-                        // paper frame |x_l| = ax 2^(Fp - K); a row that is not live leaves g and K
-                        // unchanged exactly (M = 0, k1 = k2 = 0: g * 1 + 0)
-                        const int ea = bexp(ax);
-                        const int dK = Fp - K;
-                        const int ep = ea + dK;                           // biased exponent, paper frame
-                        const bool t1 = live && ea != 0 && ep >= 1993;    // |x_l| >= 2^970
-                        const int k1 = t1 ? ep - 1992 : 0;
-                        double M, gs;
-                        if (unsigned(dK + 1022) <= 2045u && k1 <= 1022) {
-                            M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
-                            gs = __dmul_rn(g, pow2i(-k1));                // P:287 applied to g
-                        } else {                                          // extreme frames (rare)
-                            M = t1 ? with_bexp(ax, 1992) : mulp2_any(ax, dK);
-                            gs = mulp2n(g, k1);
-                        }
-                        M = live ? M : 0.0;
-                        double gn = __dadd_rn(gs, __dmul_rn(M, cn[sc]));
-                        const bool t2 = live && gn >= kOmega;
-                        const int k2 = t2 ? bexp(gn) - 1992 : 0;
-                        g = __dmul_rn(gn, pow2i(-k2));
-                        K += k1 + k2;
-                    }
+                    replay_chunk<TR>(s_rec, C, c, t * TR, lrows, Fp, cn, npad, g, K);
                 }
                 if (c < C) s_k[c] = K;
+                PT_MARK(a.pt, 11, warp == nsub && lane == 0 && pass == 0);
                 dw_mbar_arrive(bars + NT);
             }
         }
@@ -224,14 +205,20 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         const int64_t q = cb + c;
         const bool valid = q < ncols;
         const int64_t j = a.c0 + (valid ? q : 0);
+        T sh = valid ? a.shifts[j * a.sstride] : ST::zero();              // (the pass's loads together)
+        const double Gj0 = (SAFE && valid) ? a.G[j] : 0.0;
         const int64_t r = valid ? ((OP == 0 && a.rowend) ? a.rowend[j] : a.m) : 0;
         const bool active = valid && r > a.lo;
         if (SAFE && valid && !active && tq == 0) a.dblk[j] = 0;           // inactive column: no rescale
+        if (SAFE && tq == 0) {                                             // (kept for the finish)
+            s_gj[c] = Gj0;
+            s_ej[c] = valid ? a.e[j] : 0;
+        }
         const int nrow = active ? (OP == 0 ? int((a.hi < r ? a.hi : r) - a.lo) : nfull) : 0;
         int nmax = nrow;
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-        T sh = active ? a.shifts[j * a.sstride] : ST::zero();
+        if (!active) sh = ST::zero();
         if (OP == 1) sh = ST::conj(sh);
         T *x = a.B + j * a.ldb;
         T *xs = GSCR ? a.Xscr + j * a.ldscr
@@ -250,13 +237,13 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
             // ---- precheck with upper bounds (see the header) ----
             double prod = 1.0, minv = 0.0;
             for (int sc = tq; sc < nrow; sc += 4) {
-                const double inv = __drcp_ru(maxabs(pivot(sc)));           // >= 1/|d_l|
+                const double inv = rcp_up(maxabs(pivot(sc)));             // >= 1/|d_l|
                 prod = __dmul_ru(prod, __dadd_ru(1.0, __dmul_ru(cn[sc], inv)));
                 minv = fmax(minv, inv);
             }
             prod = dl_gprod_ru<4>(prod);
             minv = dl_gmax<4>(minv);
-            const double gtop = active ? __dmul_ru(a.G[j], 1.0 + 0x1p-40) : 0.0;   // >= ||y(I1)||_inf
+            const double gtop = active ? __dmul_ru(Gj0, 1.0 + 0x1p-40) : 0.0;      // >= ||y(I1)||_inf
             const double gfin = __dmul_ru(gtop, prod);
             guarded = active && !(gfin < kOmega && __dmul_ru(gfin, minv) < kOmega);
             if (__any_sync(0xffffffffu, guarded)) {                        // g := ||y(I1)||_inf
@@ -268,7 +255,9 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                 s_lrows[c] = guarded ? nrow : 0;
             }
         }
+        PT_MARK(a.pt, 4, tid == 0 && pass == 0);
         if (!staged) stage_wait();
+        PT_MARK(a.pt, 5, tid == 0 && pass == 0);
 
         const bool rec = SAFE && __any_sync(0xffffffffu, guarded);        // warp-uniform
         int F = 0;                                                         // this column's frame
@@ -404,6 +393,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
             __syncwarp();                                                  // scratch rows seen by the column's lanes
             if constexpr (SAFE) dw_mbar_arrive(bars + u);
         }
+        PT_MARK(a.pt, 6, tid == 0 && pass == 0);
         nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, 1, 4);
         nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, 2, 4);
         const bool failed = SAFE && guarded && (nonfinite || a.force_fb);
@@ -413,13 +403,14 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
             dw_mbar_wait(bars + NT, pass & 1);                             // K from the replay warp
             kt = s_k[c];
         }
+        PT_MARK(a.pt, 7, tid == 0 && pass == 0);
         // ---- steps (ii), (iii) and the output rows in the paper's frame 2^(F - K - k3) ----
         {
             int k3 = 0;
             if (SAFE) {
                 int ej = 0;
                 double Gj = 0.0;
-                if (active) { ej = a.e[j]; Gj = a.G[j]; }
+                if (active) { ej = s_ej[c]; Gj = s_gj[c]; }
                 if (kt > 0) {                                              // P:376-386, step (ii)
                     ej -= kt;
                     Gj = mulp2n(Gj, kt);
@@ -456,6 +447,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                 }
             }
         }
+        PT_MARK(a.pt, 8, tid == 0 && pass == 0);
         // ---- a column whose values stopped being finite (tiny pivots: growth beyond the frame's
         //      headroom inside one tile) is rerun from its inputs by the synchronous guarded loop,
         //      Alg. 4 step by step, one warp per column ----
@@ -528,6 +520,8 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         }
     }
     if (!staged) stage_wait();
+    PT_MARK(a.pt, 9, tid == 0);
+    PT_MARK(a.pt, 15, tid == 0);
 }
 
 }  // namespace mstrsm

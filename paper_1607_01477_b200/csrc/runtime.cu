@@ -97,3 +97,34 @@ cudaEvent_t ev_get() {
 
 }  // namespace rt
 }  // namespace mstrsm
+
+#ifdef MSTRSM_PHASE_TIMES
+// Phase-time buffer of the experiment build: 512 launches x 256 CTAs x 16 slots (ring).
+namespace mstrsm {
+namespace rt {
+static long long *g_pt = nullptr;
+static int g_pt_next = 0;
+long long *phase_next() {
+    if (!g_pt) {
+        if (cudaMalloc(&g_pt, size_t(512) * 256 * 16 * 8) != cudaSuccess) return nullptr;
+        cudaMemset(g_pt, 0, size_t(512) * 256 * 16 * 8);
+    }
+    long long *p = g_pt + size_t(g_pt_next % 512) * 256 * 16;
+    g_pt_next++;
+    return p;
+}
+}  // namespace rt
+}  // namespace mstrsm
+extern "C" int mstrsm_phase_read(long long *host, int64_t n_launches, int reset) {
+    using namespace mstrsm::rt;
+    cudaDeviceSynchronize();
+    if (g_pt && n_launches > 0)
+        cudaMemcpy(host, g_pt, size_t(n_launches < 512 ? n_launches : 512) * 256 * 16 * 8, cudaMemcpyDeviceToHost);
+    const int used = g_pt_next;
+    if (reset) {
+        g_pt_next = 0;
+        if (g_pt) cudaMemset(g_pt, 0, size_t(512) * 256 * 16 * 8);
+    }
+    return used;
+}
+#endif

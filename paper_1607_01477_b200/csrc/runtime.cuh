@@ -40,7 +40,10 @@ struct DevRes {
     cudaStream_t side = nullptr, h2d = nullptr, d2h = nullptr, comm = nullptr;
     cudaEvent_t ev_d = nullptr, ev_rest = nullptr;
 };
-DevRes *dev_res();           // nullptr (and the error recorded) if creation fails
+DevRes *dev_res();
+#ifdef MSTRSM_PHASE_TIMES
+long long *phase_next();     // the next diagonal launch's row block of the phase-time buffer
+#endif           // nullptr (and the error recorded) if creation fails
 // True the first time it is asked for the current device (per-device one-shot setup such as
 // cudaFuncSetAttribute; bit d of mask = device d done).
 inline bool first_on_device(std::atomic<uint64_t> &mask) {
