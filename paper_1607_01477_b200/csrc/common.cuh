@@ -149,7 +149,7 @@ namespace mstrsm {
 // kernel was launched without the attribute).
 // Phase timing of the diagonal kernels (experiment builds only, -DMSTRSM_PHASE_TIMES,
 // tools/build_phase.sh): PT_MARK(pt, k) stores clock64() in slot k of this CTA's row of pt (16
-// slots per CTA, pass 0); slots 0 / 15 hold %globaltimer at entry / exit.
+// slots per CTA, pass 0); slots 0 and 12-15 hold %globaltimer (entry, exits).
 #ifdef MSTRSM_PHASE_TIMES
 __device__ __forceinline__ long long pt_gtime() {
     long long t;
@@ -158,7 +158,7 @@ __device__ __forceinline__ long long pt_gtime() {
 }
 #define PT_MARK(pt, k, cond)                                                          \
     do {                                                                              \
-        if ((pt) && (cond)) (pt)[blockIdx.x * 16 + (k)] = ((k) == 0 || (k) == 15) ? pt_gtime() : clock64(); \
+        if ((pt) && (cond)) (pt)[blockIdx.x * 16 + (k)] = ((k) == 0 || (k) >= 12) ? pt_gtime() : clock64(); \
     } while (0)
 #else
 #define PT_MARK(pt, k, cond) do { } while (0)

@@ -108,44 +108,64 @@ __device__ __forceinline__ void scale_pow2(T (&y)[N], int s) {
 template <int NR>
 __device__ __forceinline__ void replay_chunk(const double *rec, int ldrec, int c, int sc0, int lrows, int Fp,
                                              const double *cn, int ncn, double &g, int &K) {
-    // Short form of the common row (no t1, frame offset dK = Fp - K in the normal range, so
-    // k1 = 0 and g 2^-k1 = g exactly): gn = g + (ax 2^dK) cnl, with 2^dK kept across rows; the
-    // general form below is the row as written out in full.  Both compute the same values.
-    int dK = Fp - K;
-    double p2 = pow2i(dK);
-    const double *rp = rec + (sc0 + NR - 1) * ldrec + c;
-#pragma unroll 4
-    for (int rr = NR - 1; rr >= 0; rr--, rp -= ldrec) {
+    // Branch-free form of the row for frame offsets dK = Fp - K in [-1022, 1023] and k1 <= 1022
+    // (the exact products below are then single multiplications by normal powers of two); a chunk
+    // in which any row leaves that range is replayed from its start by the general form.  Both
+    // evaluate the same expressions, so g and K are identical.
+    const double g_in = g;
+    const int K_in = K;
+    {
+        bool bad = false;
+        const double *rp = rec + (sc0 + NR - 1) * ldrec + c;
+        const double *cp = cn + (sc0 + NR - 1);
+#pragma unroll 8
+        for (int rr = NR - 1; rr >= 0; rr--, rp -= ldrec, cp--) {
+            const bool live = sc0 + rr < lrows;
+            const double ax = live ? *rp : 0.0;
+            const double cr = sc0 + rr < ncn ? *cp : cn[0];
+            const int ea = bexp(ax);
+            const int dK = Fp - K;
+            const int ep = ea + dK;                       // biased exponent, paper frame
+            const bool t1 = live && ea != 0 && ep >= 1993;    // |x_l| >= 2^970
+            const int k1 = t1 ? ep - 1992 : 0;
+            bad |= unsigned(dK + 1022) > 2045u || k1 > 1022;
+            double M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
+            M = live ? M : 0.0;
+            const double gs = __dmul_rn(g, pow2i(-k1));   // P:287 applied to g
+            const double gn = __dadd_rn(gs, __dmul_rn(M, cr));
+            const bool t2 = live && gn >= kOmega;
+            const int k2 = t2 ? bexp(gn) - 1992 : 0;
+            g = __dmul_rn(gn, pow2i(-k2));
+            K += k1 + k2;
+        }
+        if (!bad) return;
+    }
+    g = g_in;
+    K = K_in;
+#pragma unroll 1
+    for (int rr = NR - 1; rr >= 0; rr--) {
         const int sc = sc0 + rr;
         const bool live = sc < lrows;
-        const double ax = live ? *rp : 0.0;
-        const double cr = cn[sc < ncn ? sc : 0];
+        const double ax = live ? rec[sc * ldrec + c] : 0.0;
         const int ea = bexp(ax);
+        const int dK = Fp - K;
         const int ep = ea + dK;                           // biased exponent, paper frame
         const bool t1 = live && ea != 0 && ep >= 1993;    // |x_l| >= 2^970
-        double gn;
-        if (!t1 && unsigned(dK + 1022) <= 2045u) {
-            gn = __dadd_rn(g, __dmul_rn(live ? __dmul_rn(ax, p2) : 0.0, cr));
-        } else {
-            const int k1 = t1 ? ep - 1992 : 0;
-            double M, gs;
-            if (unsigned(dK + 1022) <= 2045u && k1 <= 1022) {
-                M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
-                gs = __dmul_rn(g, pow2i(-k1));                // P:287 applied to g
-            } else {                                          // extreme frames (rare)
-                M = t1 ? with_bexp(ax, 1992) : mulp2_any(ax, dK);
-                gs = mulp2n(g, k1);
-            }
-            M = live ? M : 0.0;
-            gn = __dadd_rn(gs, __dmul_rn(M, cr));
-            K += k1;
+        const int k1 = t1 ? ep - 1992 : 0;
+        double M, gs;
+        if (unsigned(dK + 1022) <= 2045u && k1 <= 1022) {
+            M = t1 ? with_bexp(ax, 1992) : __dmul_rn(ax, pow2i(dK));   // 2^-k1 |x_l|
+            gs = __dmul_rn(g, pow2i(-k1));                // P:287 applied to g
+        } else {                                          // extreme frames (rare)
+            M = t1 ? with_bexp(ax, 1992) : mulp2_any(ax, dK);
+            gs = mulp2n(g, k1);
         }
-        const bool t2 = live && gn >= kOmega;                 // P:301
+        M = live ? M : 0.0;
+        double gn = __dadd_rn(gs, __dmul_rn(M, cn[sc < ncn ? sc : 0]));
+        const bool t2 = live && gn >= kOmega;             // P:301
         const int k2 = t2 ? bexp(gn) - 1992 : 0;
         g = __dmul_rn(gn, pow2i(-k2));
-        K += k2;
-        dK = Fp - K;
-        p2 = pow2i(dK);
+        K += k1 + k2;
     }
 }
 

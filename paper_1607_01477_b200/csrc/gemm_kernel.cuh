@@ -42,6 +42,7 @@ struct GemmArgs {
     const double *Xsum; int64_t ldxs;
     int64_t col0;          // first column
     const int *dblk;       // per-column exponent delta (nullable)
+    long long *pt;         // phase times (MSTRSM_PHASE_TIMES builds only; nullable)
 };
 
 // Tile geometry.  Complex: CTA 64 (rows) x 64 (cols), warp 32x32, BK = 16.

@@ -130,6 +130,9 @@ int launch_gemm(const GemmArgs<T> &g) {
                 const int64_t tm = cdiv(g.M, k3qBM), tn = cdiv(g.N, k3qBN), nt = tm * tn;
                 const int grid = int(std::min<int64_t>(nt, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
                 ProfScope ps(PK_GEMM, flops);
+#ifdef MSTRSM_PHASE_TIMES
+                const_cast<GemmArgs<T> &>(g).pt = phase_next(1);
+#endif
                 CK(launch_k(kq, dim3(grid), dim3(k3qThreads), k3qSmemBytes, g_stream, g, int(tm), int(nt), tmX, tmXs, tmA,
                             tmAs, gemm_3p_phase()));
                 CK_LAUNCH("gemm_ws3q_kernel");

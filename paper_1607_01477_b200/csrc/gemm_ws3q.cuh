@@ -53,8 +53,11 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     pdl_trigger();
+    PT_MARK(g.pt, 0, tid == 0);
+    PT_MARK(g.pt, 1, tid == 0);
     __syncthreads();
     pdl_wait();
+    PT_MARK(g.pt, 2, tid == 0);
 
     if (warp < 4) {
         // ------------------------------------------------------------------ producers
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
         for (int kt = 0; kt < nk; kt++, gk++) {
             const int s = gk % RS, r = gk / RS;
             mbar_wait(&full_bar[grp][s], r & 1);
+            PT_MARK(g.pt, grp == 0 ? 3 : 5 + grp, kt == 0 && local == grp && wq == 0 && lane == 0);
             const unsigned char *st = smem_raw + (grp * RS + s) * k3qStage;
             const cplx *As = reinterpret_cast<const cplx *>(st + k3qOffA) + wm * 8 * MI + gq;
             const double *Ass = reinterpret_cast<const double *>(st + k3qOffAs) + wm * 8 * MI + gq;
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
             }
         }
 
+        PT_MARK(g.pt, 4, local == 0 && wq == 0 && lane == 0);
         // ---- epilogue: C = 2^d C - (P1 - P2, P3 - P1 - P2); warp (wm, wn) reads half wn ----
         const int s0 = gk % RS, s1 = (gk + 1) % RS;
         mbar_wait(&full_bar[grp][s0], (gk / RS) & 1);
@@ -254,6 +259,9 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[grp][wn ? s1 : s0]);
         gk += 2;
+        PT_MARK(g.pt, 5, local == 0 && wq == 0 && lane == 0);
+        PT_MARK(g.pt, 8 + grp, wq == 0 && lane == 0);
+        PT_MARK(g.pt, 12 + grp, wq == 0 && lane == 0);
     }
 }
 

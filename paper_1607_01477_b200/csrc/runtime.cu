@@ -99,32 +99,37 @@ cudaEvent_t ev_get() {
 }  // namespace mstrsm
 
 #ifdef MSTRSM_PHASE_TIMES
-// Phase-time buffer of the experiment build: 512 launches x 256 CTAs x 16 slots (ring).
+// Phase-time buffers of the experiment build (0: diagonal kernels, 1: update GEMM): 512 launches x
+// 256 CTAs x 16 slots each (rings).
 namespace mstrsm {
 namespace rt {
-static long long *g_pt = nullptr;
-static int g_pt_next = 0;
-long long *phase_next() {
-    if (!g_pt) {
-        if (cudaMalloc(&g_pt, size_t(512) * 256 * 16 * 8) != cudaSuccess) return nullptr;
-        cudaMemset(g_pt, 0, size_t(512) * 256 * 16 * 8);
+static long long *g_pt[2] = {nullptr, nullptr};
+static int g_pt_next[2] = {0, 0};
+static const size_t kPtBytes = size_t(512) * 256 * 16 * 8;
+long long *phase_next(int kind) {
+    if (!g_pt[kind]) {
+        if (cudaMalloc(&g_pt[kind], kPtBytes) != cudaSuccess) return nullptr;
+        cudaMemset(g_pt[kind], 0, kPtBytes);
     }
-    long long *p = g_pt + size_t(g_pt_next % 512) * 256 * 16;
-    g_pt_next++;
+    long long *p = g_pt[kind] + size_t(g_pt_next[kind] % 512) * 256 * 16;
+    g_pt_next[kind]++;
     return p;
 }
 }  // namespace rt
 }  // namespace mstrsm
-extern "C" int mstrsm_phase_read(long long *host, int64_t n_launches, int reset) {
+extern "C" int mstrsm_phase_read2(int kind, long long *host, int64_t n_launches, int reset) {
     using namespace mstrsm::rt;
     cudaDeviceSynchronize();
-    if (g_pt && n_launches > 0)
-        cudaMemcpy(host, g_pt, size_t(n_launches < 512 ? n_launches : 512) * 256 * 16 * 8, cudaMemcpyDeviceToHost);
-    const int used = g_pt_next;
+    if (g_pt[kind] && n_launches > 0)
+        cudaMemcpy(host, g_pt[kind], size_t(n_launches < 512 ? n_launches : 512) * 256 * 16 * 8, cudaMemcpyDeviceToHost);
+    const int used = g_pt_next[kind];
     if (reset) {
-        g_pt_next = 0;
-        if (g_pt) cudaMemset(g_pt, 0, size_t(512) * 256 * 16 * 8);
+        g_pt_next[kind] = 0;
+        if (g_pt[kind]) cudaMemset(g_pt[kind], 0, kPtBytes);
     }
     return used;
+}
+extern "C" int mstrsm_phase_read(long long *host, int64_t n_launches, int reset) {
+    return mstrsm_phase_read2(0, host, n_launches, reset);
 }
 #endif

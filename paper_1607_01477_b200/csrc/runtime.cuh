@@ -42,7 +42,7 @@ struct DevRes {
 };
 DevRes *dev_res();
 #ifdef MSTRSM_PHASE_TIMES
-long long *phase_next();     // the next diagonal launch's row block of the phase-time buffer
+long long *phase_next(int kind = 0);   // the next launch's row block of the phase-time buffer (0 diag, 1 GEMM)
 #endif           // nullptr (and the error recorded) if creation fails
 // True the first time it is asked for the current device (per-device one-shot setup such as
 // cudaFuncSetAttribute; bit d of mask = device d done).
