@@ -134,6 +134,100 @@ __global__ void lanczos_step_kernel(LanczosState st, int64_t m, int64_t nslots, 
     }
 }
 
+// The same step with one CTA per slot and the point's vectors in registers (m <= kLsThreads *
+// kLsR): one read of V, V_prev and W and one write of W, where the warp-per-point kernel above
+// passes over W three times (alpha, the update, the scaling) -- the step is HBM-bound.  Same
+// operations per element; alpha and ||w||^2 are summed in another order (a block reduction).
+constexpr int kLsThreads = 128, kLsR = 8;
+__device__ __forceinline__ double ls_block_sum(double v, double *red) {
+    v = warp_sum(v);
+    __syncthreads();                              // (red reused by the previous reduction)
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    return __dadd_rn(__dadd_rn(red[0], red[1]), __dadd_rn(red[2], red[3]));
+}
+__device__ __forceinline__ double ls_block_max(double v, double *red) {
+    v = warp_max(v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    return fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+}
+__global__ void __launch_bounds__(kLsThreads) lanczos_step_reg_kernel(LanczosState st, int64_t m, int64_t nslots,
+                                                                      int it, int iters) {
+    pdl_wait();
+    __shared__ double red[kLsThreads / 32];
+    const int tid = threadIdx.x;
+    for (int64_t sl = blockIdx.x; sl < nslots; sl += gridDim.x) {
+        const int64_t p = st.pid[sl];
+        if (!st.active[p]) continue;                                      // (uniform in the CTA)
+        const cplx *V = st.V + sl * m, *Vp = st.Vp + sl * m;
+        cplx *W = st.W + sl * m;
+        const cplx *Y = st.Y + sl * m;
+        const int e1 = st.e1[sl], e2 = st.e2[sl];
+        if (e1 < 0 || e2 < 0) {
+            // near-singular point (R25): sigma <= c1 / ||y||_2, scaled 2-norm
+            double s = 0.0;
+            for (int64_t i = tid; i < m; i += kLsThreads) s = fmax(s, fmax(fabs(Y[i].x), fabs(Y[i].y)));
+            s = ls_block_max(s, red);
+            double acc = 0.0;
+            if (s > 0.0)
+                for (int64_t i = tid; i < m; i += kLsThreads) {
+                    double a = Y[i].x / s, b = Y[i].y / s;
+                    acc += a * a + b * b;
+                }
+            acc = ls_block_sum(acc, red);
+            if (tid == 0) {
+                double ny = s * sqrt(acc);
+                st.sigma[p] = ldexp(1.0 / ny, e1);
+                st.flags[p] = 1;
+                st.active[p] = 0;
+            }
+            continue;
+        }
+        cplx vr[kLsR], wr[kLsR];
+#pragma unroll
+        for (int r = 0; r < kLsR; r++) {
+            const int64_t i = tid + int64_t(r) * kLsThreads;
+            vr[r] = i < m ? V[i] : make_double2(0.0, 0.0);
+            wr[r] = i < m ? W[i] : make_double2(0.0, 0.0);
+        }
+        double a = 0.0;                                                   // alpha = Re(v^H w)
+#pragma unroll
+        for (int r = 0; r < kLsR; r++) a += vr[r].x * wr[r].x + vr[r].y * wr[r].y;
+        a = ls_block_sum(a, red);
+        const double bp = st.beta_prev[p];
+        double bsq = 0.0;
+#pragma unroll
+        for (int r = 0; r < kLsR; r++) {                                  // w -= alpha v + beta v_prev
+            const int64_t i = tid + int64_t(r) * kLsThreads;
+            const cplx pi = i < m ? Vp[i] : make_double2(0.0, 0.0);
+            wr[r].x = (wr[r].x - a * vr[r].x) - bp * pi.x;
+            wr[r].y = (wr[r].y - a * vr[r].y) - bp * pi.y;
+            bsq += wr[r].x * wr[r].x + wr[r].y * wr[r].y;
+        }
+        bsq = ls_block_sum(bsq, red);
+        const double b = sqrt(bsq);
+        const int k = st.kdone[p];
+        const double amax = fmax(st.amax[p], a);
+        const bool brk = b <= double(m) * 0x1p-52 * amax;                 // Krylov space exhausted
+        const double binv = (!brk && it + 1 < iters) ? 1.0 / b : 1.0;     // v_next = w / beta in W
+#pragma unroll
+        for (int r = 0; r < kLsR; r++) {
+            const int64_t i = tid + int64_t(r) * kLsThreads;
+            if (i < m) W[i] = (!brk && it + 1 < iters) ? make_double2(wr[r].x * binv, wr[r].y * binv) : wr[r];
+        }
+        if (tid == 0) {
+            st.alpha[int64_t(k) * st.npts + p] = a;
+            st.beta[int64_t(k) * st.npts + p] = b;
+            st.kdone[p] = k + 1;
+            st.amax[p] = amax;
+            st.beta_prev[p] = b;
+            if (brk) st.active[p] = 0;
+        }
+    }
+}
+
 // lambda_max of the k x k tridiagonal (alpha, beta) by Sturm bisection (R14); sigma = 1/sqrt.
 __device__ inline int sturm_below_dev(const double *al, const double *be, int64_t stride, int k,
                                       double x, double pivmin) {

@@ -1123,8 +1123,14 @@ int spectral_cloud_impl(const cplx *U, int64_t ldu, int64_t m, const cplx *z, in
         rc = blocked_solve<cplx, true>(1, U, ldu, m, zc, 1, st.W, m, nact, nullptr, nullptr, nb, wC, spC.U, spC.X, spC.ldu, spC.ldx);
         if (!rc) rc = finalize<cplx>(1, 1, st.W, m, m, nact, nb, nullptr, nullptr, e2, nullptr, wC);
         if (rc) break;
-        CK(launch_k_lvl(2, lanczos_step_kernel, dim3(ab), dim3(256), 0, g_stream, st, m, nact, it, iters));
-        CK_LAUNCH("lanczos_step_kernel");
+        if (m <= int64_t(kLsThreads) * kLsR) {    // vectors in registers: one pass over memory
+            const int sb = int(std::min<int64_t>(nact, int64_t(g_num_sms) * 16));
+            CK(launch_k_lvl(2, lanczos_step_reg_kernel, dim3(sb), dim3(kLsThreads), 0, g_stream, st, m, nact, it, iters));
+            CK_LAUNCH("lanczos_step_reg_kernel");
+        } else {
+            CK(launch_k_lvl(2, lanczos_step_kernel, dim3(ab), dim3(256), 0, g_stream, st, m, nact, it, iters));
+            CK_LAUNCH("lanczos_step_kernel");
+        }
         if (it + 1 < iters) {           // the step left v_next in W: rotate (V, V_prev, W) <- (W, V, V_prev)
             cplx *t = st.Vp;
             st.Vp = st.V;
