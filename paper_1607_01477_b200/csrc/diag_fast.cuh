@@ -256,10 +256,14 @@ __device__ __forceinline__ bool diagw_rows(T (&y)[RPL], PivF pivot, const T *__r
 #pragma unroll 1
             for (int rr = rr_hi; rr >= 0; rr--, pc -= kStride) {
                 DW_CHECK(pc >= pk && pc + LPC * t < pk + padtri_off(t * LPC + rr + 1, LPC), "diagw row pointer");
+                T uc[RPL];                                                 // U(rows, l): loads first,
+#pragma unroll                                                                     // under the quotient's shuffle
+                for (int t2 = 0; t2 < RPL; t2++)
+                    if (t2 <= t) uc[t2] = uget(pc + LPC * t2);
                 const T xl = group_shfl<T, LPC>(pvt.apply(y[t]), rr);      // P:82 / P:297
-                y[t] = ST::fnms(y[t], xl, uget(pc + LPC * t));             // zero for rows >= l
+                y[t] = ST::fnms(y[t], xl, uc[t]);                          // zero for rows >= l
 #pragma unroll
-                for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xl, uget(pc + LPC * t2));
+                for (int t2 = t - 1; t2 >= 0; t2--) y[t2] = ST::fnms(y[t2], xl, uc[t2]);
             }
             const T xo = pvt.apply(y[t]);                                  // = the shuffled x_l
             y[t] = xo;

@@ -349,10 +349,10 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
                 const int tstride = TR * (u + 1);                          // padded column length
 #pragma unroll
                 for (int n = TR - 1; n >= 0; n--) {
+                    const T *cu = tb + n * tstride;                        // U(r0 + {0,1}, 8u + n), zero for row >= 8u + n
+                    const T u0 = CONJ ? ST::conj(cu[0]) : cu[0], u1 = CONJ ? ST::conj(cu[1]) : cu[1];   // (loads first)
                     const T qv = (n & 1) ? p1.apply(y1) : p0.apply(y0);
                     const T xl = group_shfl<T, 4>(qv, n >> 1);
-                    const T *cu = tb + n * tstride;                        // U(r0 + {0,1}, 8u + n), zero for row >= 8u + n
-                    const T u0 = CONJ ? ST::conj(cu[0]) : cu[0], u1 = CONJ ? ST::conj(cu[1]) : cu[1];
                     y0 = ST::fnms(y0, xl, u0);
                     y1 = ST::fnms(y1, xl, u1);
                 }
