@@ -28,4 +28,15 @@ timeout 600 ncu --set full --clock-control none --import-source on --profile-fro
     -o gpurun_out/prof_diag_c5_$TAG python tools/profile_run.py --config c5 > gpurun_out/ncu_diag_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:diagl -s 16 -c 1 \
     -o gpurun_out/prof_diagl_c2_$TAG python tools/profile_run.py --config c2 > gpurun_out/ncu_diagl_$TAG.log 2>&1
+# summaries on the box (the reports themselves stay out of gpurun_out: size cap)
+for r in gemm diag diagl; do
+  f=$(ls gpurun_out/prof_${r}_*_$TAG.ncu-rep 2>/dev/null | head -1)
+  [ -n "$f" ] || continue
+  b=${f%.ncu-rep}
+  ncu -i $f --page details > ${b}_details.txt 2>&1
+  ncu -i $f --page raw --csv > ${b}_raw.csv 2>&1
+  mv $f /tmp/
+done
+bash tools/gpu_phase.sh > /dev/null 2>&1
+bash tools/gpu_phase_gemm.sh > /dev/null 2>&1
 tail -3 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log
