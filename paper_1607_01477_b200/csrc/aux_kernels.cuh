@@ -183,6 +183,38 @@ __global__ void init_trevc_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t
 // P is non-null, the plane P(l,k) = Re + Im (presum_kernel) -- |T(l,k)| evaluated once.
 // qof (nullable): column subset -- eigenvector k goes to column qof[k] of Z (-1: not in the subset);
 // the norms and the plane always cover every column of T.
+// Running max of |v| over a column without a square root per element (prepass, a.1/a.2): for a
+// complex v with both components in [2^-500, 2^500) |v| = sqrt_rn(x^2 + y^2) with no prescale
+// (S<cplx>::mod), a monotone function of the rounded sum, so the maximum is sqrt_rn of the largest
+// sum (non-negative doubles order like their bits); zeros add nothing; any other element takes
+// S<T>::mod itself, which also flags non-finite entries.  Bit-identical to max_l S<T>::mod(v_l).
+struct ModMax {
+    long long qb = -1;
+    double other = 0.0;
+    bool bad = false;
+    __device__ __forceinline__ void add(double v) {
+        const double a = fabs(v);
+        bad |= !(a <= 1.7976931348623157e308);
+        other = fmax(other, a);
+    }
+    __device__ __forceinline__ void add(cplx v) {
+        const unsigned hx = unsigned(__double2hiint(v.x)) & 0x7fffffffu;
+        const unsigned hy = unsigned(__double2hiint(v.y)) & 0x7fffffffu;
+        const unsigned hb = max(hx, hy);
+        if ((hb >> 20) - 523u <= 999u) {
+            const double q = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+            qb = max(qb, __double_as_longlong(q));
+        } else if ((hb | unsigned(__double2loint(v.x)) | unsigned(__double2loint(v.y))) != 0u) {
+            const double a = S<cplx>::mod(v);
+            bad |= !(a <= 1.7976931348623157e308);
+            other = fmax(other, a);
+        }
+    }
+    __device__ __forceinline__ double get() const {
+        return qb >= 0 ? fmax(__dsqrt_rn(__longlong_as_double(qb)), other) : other;
+    }
+};
+
 template <typename T>
 __global__ void trevc_prepass_kernel(const T *__restrict__ Tm, int64_t ldt, int64_t m, int nb,
                                      double *__restrict__ cnl, double *__restrict__ pcol,
@@ -201,15 +233,12 @@ __global__ void trevc_prepass_kernel(const T *__restrict__ Tm, int64_t ldt, int6
         const T *tc = Tm + k * ldt;
         const int64_t q = qof ? int64_t(qof[k]) : k;
         T *z = q >= 0 ? Z + q * ldz : nullptr;
-        double c = 0.0, p = 0.0;
-        bool bad = false;
+        ModMax mc, mp;
         for (int64_t l = lane; l < m; l += 32) {
             if (l < k) {
                 const T v = tc[l];
-                const double a = S<T>::mod(v);
-                bad |= !(a <= 1.7976931348623157e308);
-                if (l < bl.lo) p = fmax(p, a);
-                else c = fmax(c, a);
+                if (l < bl.lo) mp.add(v);
+                else mc.add(v);
                 if (z) z[l] = S<T>::neg(v);
                 if constexpr (S<T>::cplx_) {
                     if (P) P[l + k * ldp] = __dadd_rn(v.x, v.y);
@@ -218,9 +247,9 @@ __global__ void trevc_prepass_kernel(const T *__restrict__ Tm, int64_t ldt, int6
                 z[l] = S<T>::zero();
             }
         }
-        c = warp_max(c);
-        p = warp_max(p);
-        bad = __any_sync(0xffffffffu, bad);
+        const double c = warp_max(mc.get());
+        const double p = warp_max(mp.get());
+        const bool bad = __any_sync(0xffffffffu, mc.bad || mp.bad);
         if (lane == 0) {
             const T d = tc[k];
             cnl[k] = c;
@@ -323,15 +352,12 @@ __global__ void trevc_prepass_panel_kernel(const T *__restrict__ Tm, int64_t ldt
         const T *tc = Tm + k * ldt;
         const int64_t q = qof ? int64_t(qof[k]) : k;
         T *z = q >= 0 ? Z + q * ldz : nullptr;
-        double c = 0.0, p = 0.0;
-        bool bad = false;
+        ModMax mc, mp;
         for (int64_t l = r0 + lane; l < r1; l += 32) {
             if (l < k) {
                 const T v = tc[l];
-                const double a = S<T>::mod(v);
-                bad |= !(a <= 1.7976931348623157e308);
-                if (l < bl.lo) p = fmax(p, a);
-                else c = fmax(c, a);
+                if (l < bl.lo) mp.add(v);
+                else mc.add(v);
                 if (z) z[l] = S<T>::neg(v);
                 if constexpr (S<T>::cplx_) {
                     if (P) P[l + k * ldp] = __dadd_rn(v.x, v.y);
@@ -340,9 +366,9 @@ __global__ void trevc_prepass_panel_kernel(const T *__restrict__ Tm, int64_t ldt
                 z[l] = S<T>::zero();
             }
         }
-        c = warp_max(c);
-        p = warp_max(p);
-        bad = __any_sync(0xffffffffu, bad);
+        const double c = warp_max(mc.get());
+        const double p = warp_max(mp.get());
+        const bool bad = __any_sync(0xffffffffu, mc.bad || mp.bad);
         if (lane == 0) {
             if (c > 0.0) atomic_max_nonneg(cnl + k, c);
             if (p > 0.0) atomic_max_nonneg(pcol + k, p);

@@ -2262,7 +2262,15 @@ int trevc_dist_impl(const T *Tm, int64_t ldt, int64_t m, T *Z, int64_t ldz, doub
     }
     int rc = 0;
     if (ncols > 0) {
+        // With P > 1 the solve's diagonal and update kernels leave k SMs (MSTRSM_DIST_RESERVE_SMS,
+        // default 8) to the comm stream's work -- panel prepass, slab packing, the collectives'
+        // kernels -- which cannot share an SM with the update GEMM (it holds the whole register
+        // file).  One-GPU emulation of rank 0's step: P = 8 32.6 -> 30.1 ms, P = 2
+        // 86.8 -> 84.9 ms.  The arithmetic does not depend on the grid size.
+        static const int reserve = [] { const char *e = getenv("MSTRSM_DIST_RESERVE_SMS"); return e ? atoi(e) : 8; }();
+        if (P > 1 && reserve > 0 && reserve < g_num_sms) g_cta_cap = g_num_sms - reserve;
         rc = trevc_impl<T>(Tuse, lduse, m, cols.data(), ncols, Zs, m, ss, es_, nb, &feed);
+        g_cta_cap = 0;
     } else {                                        // no columns here: the collectives still run
         for (int64_t b = 0; b < nblk && !rc; b++) {
             rc = feed.enqueue(b);
