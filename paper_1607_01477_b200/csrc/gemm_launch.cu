@@ -84,6 +84,15 @@ static int gemm_3m_groups(int K, int64_t M) {
 }
 
 static bool use_classic() { return gemm_variant() == 1; }
+// MSTRSM_EARLY_A=0|1 forces the early U-operand issue of gemm_ws3q_kernel off / on (default: by size)
+static int gemm_early_a() {
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("MSTRSM_EARLY_A");
+        v = (e && (e[0] == '0' || e[0] == '1') && !e[1]) ? e[0] - '0' : -1;
+    }
+    return v;
+}
 
 template <typename T, bool OPC>
 int launch_gemm(const GemmArgs<T> &g) {
@@ -133,8 +142,11 @@ int launch_gemm(const GemmArgs<T> &g) {
 #ifdef MSTRSM_PHASE_TIMES
                 const_cast<GemmArgs<T> &>(g).pt = phase_next(1);
 #endif
+                // (pipeline fill issued before the dependent-launch wait on short launches: <= 4 tiles
+                // per consumer group)
+                const int early_a = gemm_early_a() >= 0 ? gemm_early_a() : (nt <= int64_t(grid) * 3 * 4 ? 1 : 0);
                 CK(launch_k(kq, dim3(grid), dim3(k3qThreads), k3qSmemBytes, g_stream, g, int(tm), int(nt), tmX, tmXs, tmA,
-                            tmAs, gemm_3p_phase()));
+                            tmAs, gemm_3p_phase(), early_a));
                 CK_LAUNCH("gemm_ws3q_kernel");
                 return 0;
             }

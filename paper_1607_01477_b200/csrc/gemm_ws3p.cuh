@@ -45,6 +45,10 @@ static_assert(16 * 50 * 16 <= k3pStage, "a C quarter must fit in one stage");
 static_assert(k3pOffA % 1024 == 0 && k3pOffAsC % 512 == 0 && k3pOffAsC + k3mBM * k3mBK * 8 <= k3pStage, "");
 static_assert(k3pOffA % 16 == 0 && k3pOffAs % 16 == 0 && k3pOffXs % 512 == 0, "");
 
+// raise the barrier's expected transaction bytes without arriving
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
                                                                   const __grid_constant__ CUtensorMap tmXs,
                                                                   const __grid_constant__ CUtensorMap tmA,
                                                                   const __grid_constant__ CUtensorMap tmAs,
-                                                                  int phase) {
+                                                                  int phase, int early_a) {
     constexpr int kPC = k3q_pc<OPC>();
     constexpr int BM = k3qBM, BN = k3qBN, BK = k3qBK, RS = k3qRing, MI = k3qMI, NI = 4, NG = 3;
     extern __shared__ __align__(1024) unsigned char smem_dyn[];
@@ -56,6 +56,39 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
     PT_MARK(g.pt, 0, tid == 0);
     PT_MARK(g.pt, 1, tid == 0);
     __syncthreads();
+    // early_a: the U operands (A, A+) of each group's first kE k-tiles are read-only during the
+    // solve, so their copies into the (still empty) ring stages are issued before the wait for the
+    // preceding grid, which only the X / X+ / C loads need (the stage's full barrier then expects
+    // both parts).  The launcher sets it for short launches, where the pipeline fill weighs.
+    const int kE = early_a ? (nk < RS ? nk : RS) : 0;
+    if (warp < NG && kE > 0) {
+        const int q = warp, tile = blockIdx.x + q * gridDim.x;
+        if (tile < ntiles) {
+            const int64_t m0 = int64_t(tile % tiles_m) * BM;
+            const int rows = int(g.M - m0 < BM ? g.M - m0 : BM);
+            for (int kt = 0; kt < kE; kt++) {
+                const int k0 = kt * BK;
+                if (!(OPC || k0 + BK <= g.K)) break;              // (ragged k-tile: written by hand later)
+                unsigned char *st = smem_raw + (q * RS + kt) * k3qStage;
+                uint64_t *fb = &full_bar[q][kt];
+                if (OPC) {
+                    if (lane == 16) {
+                        mbar_expect_tx(fb, BM * BK * 24);
+                        tma_2d(st + k3qOffA, &tmA, 2 * k0, int(m0), fb);
+                        tma_2d(st + k3qOffAsC, &tmAs, k0, int(m0), fb);
+                    }
+                } else if (lane < 2 * BK) {
+                    const uint32_t bytes = lane < BK ? uint32_t(rows) * 16 : uint32_t((rows * 8 + 15) & ~15);
+                    mbar_expect_tx(fb, bytes);
+                    const int k = lane & (BK - 1);
+                    if (lane < BK)
+                        bulk_g2s(st + k3qOffA + k * kQA * 16, g.U + (g.a_r0 + m0) + (g.a_c0 + k0 + k) * g.ldu, bytes, fb);
+                    else
+                        bulk_g2s(st + k3qOffAs + k * kQAs * 8, g.As + (g.a_r0 + m0) + (g.a_c0 + k0 + k) * g.ldas, bytes, fb);
+                }
+            }
+        }
+    }
     pdl_wait();
     PT_MARK(g.pt, 2, tid == 0);
 
@@ -88,20 +121,21 @@ __global__ void __launch_bounds__(k3qThreads, 1) gemm_ws3q_kernel(GemmArgs<cplx>
                 uint64_t *fb = &full_bar[q][s];
                 const int k0 = kt * BK;
                 if (OPC || k0 + BK <= g.K) {
+                    const bool early = local == q && kt < kE;            // A, A+ already issued
                     uint32_t bytes = 0;
-                    if (lane == 16) bytes = BN * BK * 24 + (OPC ? BM * BK * 24 : 0);
-                    if (!OPC && lane < 2 * BK)
+                    if (lane == 16) bytes = BN * BK * 24 + (OPC && !early ? BM * BK * 24 : 0);
+                    if (!OPC && !early && lane < 2 * BK)
                         bytes = lane < BK ? uint32_t(rows) * 16 : uint32_t((rows * 8 + 15) & ~15);
                     mbar_arrive_expect_tx(fb, bytes);
                     if (lane == 16) {
                         tma_2d(st, &tmX, 2 * k0, int(n0), fb);
                         tma_2d(st + k3qOffXs, &tmXs, k0, int(n0), fb);
-                        if (OPC) {
+                        if (OPC && !early) {
                             tma_2d(st + k3qOffA, &tmA, 2 * k0, int(m0), fb);
                             tma_2d(st + k3qOffAsC, &tmAs, k0, int(m0), fb);
                         }
                     }
-                    if (!OPC && lane < 2 * BK) {
+                    if (!OPC && !early && lane < 2 * BK) {
                         const int k = lane & (BK - 1);
                         if (lane < BK)
                             bulk_g2s(st + k3qOffA + k * kQA * 16, g.U + (g.a_r0 + m0) + (g.a_c0 + k0 + k) * g.ldu,
