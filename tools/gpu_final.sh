@@ -40,3 +40,4 @@ done
 bash tools/gpu_phase.sh > /dev/null 2>&1
 bash tools/gpu_phase_gemm.sh > /dev/null 2>&1
 tail -3 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log
+timeout 900 bash tools/gpu_emul_prof.sh > /dev/null 2>&1; cp gpurun_out/launch_emul_r02.csv gpurun_out/launch_emul_$TAG.csv 2>/dev/null
