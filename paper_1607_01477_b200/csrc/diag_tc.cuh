@@ -84,13 +84,17 @@ __device__ __forceinline__ double dl_gprod_ru(double v) {
 }
 
 // Shared-memory bytes of one launch: diag_fast.cuh's carve-up (tiles as chunks of 8 rows) plus
-// the solved rows' scratch (column stride npad + 1: the 8 columns of a k-step fall in distinct
-// banks).
+// the solved rows' scratch (column stride diagl_scr_ld).
+// Column stride of the scratch: a k-step's 32 lanes (8 columns x 4 rows) read word gq S + tq;
+// for 8-byte elements S = npad + 4 (= 4 or 12 mod 16: every 8-byte bank pair serves two lanes,
+// the 2-wavefront minimum; npad + 1 put up to 4 lanes on one pair), for 16-byte elements npad + 1
+// (each 16-byte bank group already serves 4 lanes, the minimum).
+__host__ __device__ inline int64_t diagl_scr_ld(int npad, int esize) { return npad + (esize == 8 ? 4 : 1); }
 __host__ __device__ inline int64_t diagl_scr_offset(int npad, int esize, int ncol, bool safe) {
     return (diagw_smem(npad, kDLTile, npad / kDLTile, esize, ncol, safe).total + 15) & ~int64_t(15);
 }
 __host__ __device__ inline int64_t diagl_smem_bytes(int npad, int esize, int ncol, bool safe, bool gscr = false) {
-    return diagl_scr_offset(npad, esize, ncol, safe) + (gscr ? 0 : int64_t(ncol) * (npad + 1) * esize);
+    return diagl_scr_offset(npad, esize, ncol, safe) + (gscr ? 0 : int64_t(ncol) * diagl_scr_ld(npad, esize) * esize);
 }
 
 // GSCR: the solved rows' scratch lives in global memory (a.Xscr, L2-resident; for blocks whose
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
         T *x = a.B + j * a.ldb;
         T *xs = GSCR ? a.Xscr + j * a.ldscr
                      : reinterpret_cast<T *>(smem_raw + diagl_scr_offset(npad, int(sizeof(T)), C, SAFE)) +
-                           c * (npad + 1);                                 // -x of the solved rows
+                           c * diagl_scr_ld(npad, int(sizeof(T)));         // -x of the solved rows
         auto rowof = [&](int sc) -> int64_t { return OP == 0 ? a.lo + sc : a.hi - 1 - sc; };
         auto pivot = [&](int sc) -> T {                                    // d_l = U(l,l) - s_j
             T dd = sc < nrow ? ST::sub(dg[sc], sh) : ST::real(1.0);
