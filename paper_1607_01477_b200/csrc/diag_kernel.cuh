@@ -62,6 +62,7 @@ struct DiagArgs {
     const int *dprev; int64_t c0prev, plo, phi, bprev;
     double *xsprev;
     long long *pt;                 // phase times (MSTRSM_PHASE_TIMES builds only; nullable)
+    int trig;                      // diagl_kernel: let the next grid launch at this one's start
 };
 
 template <typename T> struct DiagArgs;

@@ -189,6 +189,18 @@ bool diagl_fits(int nfull) {
     return diagl_smem_bytes(npad, int(sizeof(T)), 8 * 8, SAFE) <= 227 * 1024;
 }
 
+// MSTRSM_DIAGL_TRIGGER=0|1: diagl_kernel triggers its dependent launch at its start, so the
+// update GEMM after it becomes resident on the SMs the diagonal step leaves free and issues its
+// first A k-tiles (read-only U) during that step (gemm_ws_kernel's early_a).  Default off: c2
+// 1.252 ms without vs 1.274 with, c1 0.199 vs 0.198 (same box, profiles/r02/exp_trig_t1.txt).
+inline int diagl_trigger() {
+    static const int v = [] {
+        const char *e = getenv("MSTRSM_DIAGL_TRIGGER");
+        return (e && e[0] == '1' && !e[1]) ? 1 : 0;
+    }();
+    return v;
+}
+
 template <typename T, bool SAFE, int OP, bool GSCR = false>
 int launch_diagl(const DiagArgs<T> &a0) {
     auto kern = diagl_kernel<T, SAFE, OP, GSCR>;
@@ -221,6 +233,7 @@ int launch_diagl(const DiagArgs<T> &a0) {
     if (grid < 1) grid = 1;
     DiagArgs<T> a = a0;
     a.nsub = nsub;
+    a.trig = diagl_trigger();
 #ifdef MSTRSM_PHASE_TIMES
     a.pt = phase_next();
 #endif

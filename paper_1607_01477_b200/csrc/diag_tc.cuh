@@ -128,6 +128,7 @@ __global__ void __launch_bounds__((kDLMaxSub) * 32, 1) diagl_kernel(DiagArgs<T> 
     // ---- stage U(I1,I1) as the padded triangle with 8-row chunks (solve coordinates; columns
     //      nfull .. npad-1 all zero), its diagonal (1 past nfull) and cnl (0 past nfull).  U and
     //      cnl are never written during a solve: launches after the first stage before the wait ----
+    if (a.trig) pdl_trigger();                                             // (launcher's choice)
     PT_MARK(a.pt, 0, tid == 0);
     PT_MARK(a.pt, 1, tid == 0);
     if (!a.early) pdl_wait();

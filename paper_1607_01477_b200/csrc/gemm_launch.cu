@@ -84,7 +84,8 @@ static int gemm_3m_groups(int K, int64_t M) {
 }
 
 static bool use_classic() { return gemm_variant() == 1; }
-// MSTRSM_EARLY_A=0|1 forces the early U-operand issue of gemm_ws3q_kernel off / on (default: by size)
+// MSTRSM_EARLY_A=0|1 forces the early U-operand issue of gemm_ws3q_kernel / gemm_ws_kernel off / on
+// (default: by size)
 static int gemm_early_a() {
     static int v = -2;
     if (v == -2) {
@@ -180,7 +181,10 @@ int launch_gemm(const GemmArgs<T> &g) {
     const int64_t ntiles = tiles_m * tiles_n;
     const int grid = int(std::min<int64_t>(ntiles, g_cta_cap > 0 ? g_cta_cap : g_num_sms));
     ProfScope ps(PK_GEMM, flops);
-    CK(launch_k(kern, dim3(grid), dim3(kWsThreads), smem, g_stream, g, int(tiles_m), int(ntiles)));
+    // (first tile's A k-tiles issued before the dependent-launch wait on short launches: <= 4
+    // tiles per consumer group, as for gemm_ws3q_kernel)
+    const int early_a = gemm_early_a() >= 0 ? gemm_early_a() : (ntiles <= int64_t(grid) * 2 * 4 ? 1 : 0);
+    CK(launch_k(kern, dim3(grid), dim3(kWsThreads), smem, g_stream, g, int(tiles_m), int(ntiles), early_a));
     CK_LAUNCH("gemm_ws_kernel");
     return 0;
 }

@@ -81,7 +81,7 @@ template <typename T> __device__ __forceinline__ int ws_offC(int row, int colq) 
 }
 
 template <typename T, bool OPC>
-__global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, int tiles_m, int ntiles) {
+__global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, int tiles_m, int ntiles, int early_a) {
     constexpr int BM = GemmCfg<T>::BM, BN = GemmCfg<T>::BN, BK = kWsBK;
     constexpr int WM = GemmCfg<T>::WM, WN = GemmCfg<T>::WN;
     constexpr int MI = WM / 8, NI = WN / 8;
@@ -105,6 +105,54 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             }
     }
     __syncthreads();
+    // A(mm, k) tile of k-tile k0 into As (the A warp of a ring; fully predicated unless interior)
+    auto load_A = [&](T *As, int64_t m0, int k0, bool interior) {
+        const int kl = lane & 7, nl = lane >> 3;
+        const bool vm0 = m0 + lane < g.M, vm1 = m0 + lane + 32 < g.M;
+        if (!OPC) {                 // A(mm,k) = U(a_r0+m0+mm, a_c0+k0+k): rows contiguous
+            const T *ua = g.U + (g.a_r0 + m0 + lane) + (g.a_c0 + k0) * g.ldu;
+            if (interior) {
+#pragma unroll
+                for (int k = 0; k < BK; k++) {
+                    cp_async<ESZ>(As + ws_offA_km<T>(k, lane), ua + k * g.ldu, true);
+                    cp_async<ESZ>(As + ws_offA_km<T>(k, lane + 32), ua + k * g.ldu + 32, true);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < BK; k++) {
+                    const bool vk = k0 + k < g.K;
+                    const T *col = ua + k * g.ldu;
+                    cp_async<ESZ>(As + ws_offA_km<T>(k, lane), vk && vm0 ? col : g.U, vk && vm0);
+                    cp_async<ESZ>(As + ws_offA_km<T>(k, lane + 32), vk && vm1 ? col + 32 : g.U, vk && vm1);
+                }
+            }
+        } else {                    // A(mm,k) = conj(U(a_r0+k0+k, a_c0+m0+mm)): k contiguous
+            const bool vk = k0 + kl < g.K;
+            const T *ua = g.U + (g.a_r0 + k0 + kl) + (g.a_c0 + m0 + nl) * g.ldu;
+#pragma unroll 4
+            for (int it = 0; it < BM / 4; it++) {
+                const int mm = 4 * it + nl;
+                const bool v = vk && m0 + mm < g.M;
+                cp_async<ESZ>(As + ws_offRK<T>(mm, kl), v ? ua + (4 * it) * g.ldu : g.U, v);
+            }
+        }
+    };
+    // early_a: U is read-only during the solve, so the A warps copy the A tiles of their group's
+    // first kE k-tiles into the (still empty) ring stages and arrive on those stages' full
+    // barriers before the wait for the preceding grid, which only the X and C loads need (as in
+    // gemm_ws3q_kernel; the launcher sets it for short launches).
+    const int kE = early_a ? (nk < kWsRingStages ? nk : kWsRingStages) : 0;
+    if (warp < 4 && (warp & 1) == 0 && kE > 0) {
+        const int q = warp >> 1, tile = blockIdx.x + q * gridDim.x;
+        if (tile < ntiles) {
+            const int64_t m0 = int64_t(tile % tiles_m) * BM;
+            for (int kt = 0; kt < kE; kt++) {
+                load_A(smem + (q * kWsRingStages + kt) * SE, m0, kt * BK,
+                       m0 + BM <= g.M && kt * BK + BK <= g.K);
+                mbar_arrive_cpasync(&full_bar[q][kt]);
+            }
+        }
+    }
     pdl_wait();
 
     if (warp < 4) {
@@ -144,37 +192,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) gemm_ws_kernel(GemmArgs<T> g, i
             }
 #pragma unroll 1
             for (int kt = 0; kt < nk; kt++) {
+                if (half == 0 && local == q && kt < kE) { gk++; continue; }   // A issued and arrived early
                 T *As = next_slot(), *Xs = As + BM * BK;
                 const int k0 = kt * BK;
                 const bool interior = mn_in && k0 + BK <= g.K;
                 if (half == 0) {
-                    if (!OPC) {                 // A(mm,k) = U(a_r0+m0+mm, a_c0+k0+k): rows contiguous
-                        const T *ua = g.U + (g.a_r0 + m0 + lane) + (g.a_c0 + k0) * g.ldu;
-                        if (interior) {
-#pragma unroll
-                            for (int k = 0; k < BK; k++) {
-                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane), ua + k * g.ldu, true);
-                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane + 32), ua + k * g.ldu + 32, true);
-                            }
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < BK; k++) {
-                                const bool vk = k0 + k < g.K;
-                                const T *col = ua + k * g.ldu;
-                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane), vk && vm0 ? col : g.U, vk && vm0);
-                                cp_async<ESZ>(As + ws_offA_km<T>(k, lane + 32), vk && vm1 ? col + 32 : g.U, vk && vm1);
-                            }
-                        }
-                    } else {                    // A(mm,k) = conj(U(a_r0+k0+k, a_c0+m0+mm)): k contiguous
-                        const bool vk = k0 + kl < g.K;
-                        const T *ua = g.U + (g.a_r0 + k0 + kl) + (g.a_c0 + m0 + nl) * g.ldu;
-#pragma unroll 4
-                        for (int it = 0; it < BM / 4; it++) {
-                            const int mm = 4 * it + nl;
-                            const bool v = vk && m0 + mm < g.M;
-                            cp_async<ESZ>(As + ws_offRK<T>(mm, kl), v ? ua + (4 * it) * g.ldu : g.U, v);
-                        }
-                    }
+                    load_A(As, m0, k0, interior);
                 } else {                        // X(k,nn) = X(x_r0+k0+k, col0+n0+nn): k contiguous
                     const T *xb = g.X + (g.x_r0 + k0 + kl) + (g.col0 + n0 + nl) * g.ldx;
                     if (interior) {
