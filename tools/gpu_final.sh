@@ -37,7 +37,9 @@ for r in gemm diag diagl; do
   ncu -i $f --page raw --csv > ${b}_raw.csv 2>&1
   mv $f /tmp/
 done
-bash tools/gpu_phase.sh > /dev/null 2>&1
-bash tools/gpu_phase_gemm.sh > /dev/null 2>&1
+if [ -z "$SKIP_PHASE" ]; then
+  bash tools/gpu_phase.sh > /dev/null 2>&1
+  bash tools/gpu_phase_gemm.sh > /dev/null 2>&1
+fi
 tail -3 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log
 timeout 900 bash tools/gpu_emul_prof.sh > /dev/null 2>&1; cp gpurun_out/launch_emul_r02.csv gpurun_out/launch_emul_$TAG.csv 2>/dev/null
