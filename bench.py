@@ -451,9 +451,10 @@ def e2e_host(ms, T_host, m, nb, args):
     ep = torch.empty(m, dtype=torch.int32, pin_memory=True)
     Tn, Zn, sn, en = Tp.numpy(), Zp.numpy(), sp.numpy(), ep.numpy()
     fl = algorithmic_flops_cols(np.arange(m), True)
-    # the upper triangle of T is uploaded by 128-column panels (rows 0 .. panel end)
+    # the upper triangle of T is uploaded by 128-column panels (rows 0 .. panel end); Z comes back
+    # the same way (rows 0..k of eigenvector k, R37), plus the scales (8 B) and exponents (4 B)
     h2d = sum(min(m, c0 + 128) * (min(m, c0 + 128) - c0) for c0 in range(0, m, 128)) * 16
-    d2h = int(m) * m * 16 + m * 12
+    d2h = int(h2d) + m * 12
     ms.trevc_z_host(Tn, m, Zn, sn, en, nb)                              # warm-up
     single = []
     for _ in range(max(1, min(args.steps, 2))):

@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
     // from dblk once per CTA while the pipeline fills
     __shared__ double s_sc[BN];
     __shared__ int s_d[BN];
+    pdl_wait();                       // (launched as a programmatic dependent: before any global access)
     if (tid < BN) {
         const int64_t gj = n0 + tid;
         const int d = (g.dblk && gj < g.N) ? g.dblk[g.col0 + gj] : 0;
@@ -247,7 +248,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
     __syncthreads();
 
     // ---- epilogue: C = 2^d C - acc (C from shared memory); one FMA per element (2^0 = 1 is
-    //      exact), bounds checks only on edge tiles, ldexp only for d < -1022 (subnormal scale) ----
+    //      exact), bounds checks only on edge tiles; for d < -1022 (subnormal scale) 2^d in two exact
+    //      normal factors, as gemm_ws_kernel ----
     const T *Cs = smem + ((nk + wn) % kGemmStages) * gemm_stage_elems<T>();   // this warp's half
     const bool full = m0 + BM <= g.M && n0 + BN <= g.N;
 #pragma unroll
@@ -271,10 +273,16 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
                 } else {
                     nv = fma(old, sc, -accR[i][jn][c]);
                 }
-                if (tiny) {
-                    const int d = s_d[wn * WN + colh];
-                    if constexpr (CPX) { nv.x = ldexp(old.x, d) - accR[i][jn][c]; nv.y = ldexp(old.y, d) - accI[i][jn][c]; }
-                    else nv = ldexp(old, d) - accR[i][jn][c];
+                if (tiny) {     // 2^d as f1 * f2, both normal: the same roundings as gemm_ws_kernel
+                    const int d = max(s_d[wn * WN + colh], -2044);
+                    const double f1 = __longlong_as_double((long long)(1023 + d + 1022) << 52);
+                    const double f2 = 0x1p-1022;
+                    if constexpr (CPX) {
+                        nv.x = fma(__dmul_rn(old.x, f1), f2, -accR[i][jn][c]);
+                        nv.y = fma(__dmul_rn(old.y, f1), f2, -accI[i][jn][c]);
+                    } else {
+                        nv = fma(__dmul_rn(old, f1), f2, -accR[i][jn][c]);
+                    }
                 }
                 if (full || (gi < g.M && gj < g.N)) colp[gi] = nv;
             }

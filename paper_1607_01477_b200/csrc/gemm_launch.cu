@@ -2,7 +2,8 @@
 //   default: the persistent warp-specialised kernel -- complex operands with three real products
 //   (gemm_ws3m.cuh), real operands gemm_ws.cuh;
 //   MSTRSM_GEMM=4m: complex with four real products (gemm_ws.cuh);
-//   MSTRSM_GEMM=classic: the one-tile-per-CTA kernel (gemm_kernel.cuh).  (Comparison only.)
+//   MSTRSM_GEMM=classic: the one-tile-per-CTA kernel (gemm_kernel.cuh) for everything (comparison);
+//   real launches of at most one wave take it by default (gemm_real_mode below).
 #include <stdlib.h>
 #include <string.h>
 
@@ -84,6 +85,18 @@ static int gemm_3m_groups(int K, int64_t M) {
 }
 
 static bool use_classic() { return gemm_variant() == 1; }
+// Real operands: MSTRSM_GEMM_REAL=ws|classic forces the persistent warp-specialised kernel / the
+// one-tile-per-CTA kernel; default (auto): the one-tile-per-CTA kernel when the launch is at most
+// one wave of it (2 CTAs per SM) and no SM cap is in force -- the short updates of small real
+// solves (c1, c2), where the persistent kernel's producer/consumer hand-off is pure latency.
+static int gemm_real_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MSTRSM_GEMM_REAL");
+        v = (e && !strcmp(e, "ws")) ? 1 : (e && !strcmp(e, "classic")) ? 2 : 0;
+    }
+    return v;
+}
 // MSTRSM_EARLY_A=0|1 forces the early U-operand issue of gemm_ws3q_kernel / gemm_ws_kernel off / on
 // (default: by size)
 static int gemm_early_a() {
@@ -99,14 +112,17 @@ template <typename T, bool OPC>
 int launch_gemm(const GemmArgs<T> &g) {
     const double flops = double(g.M) * g.N * g.K * (S<T>::cplx_ ? 8.0 : 2.0);
     const int64_t tiles_m = cdiv(g.M, GemmCfg<T>::BM), tiles_n = cdiv(g.N, GemmCfg<T>::BN);
-    if (use_classic()) {
+    const bool real_classic = !S<T>::cplx_ && gemm_variant() == 0 &&
+                              (gemm_real_mode() == 2 ||
+                               (gemm_real_mode() == 0 && g_cta_cap == 0 && tiles_m * tiles_n <= 2 * int64_t(g_num_sms)));
+    if (use_classic() || real_classic) {
         auto kern = gemm_update_kernel<T, OPC>;
         static std::atomic<uint64_t> attr_set{0};
         constexpr int smem = gemm_smem_bytes<T>();
         if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         dim3 grid{unsigned(tiles_m), unsigned(tiles_n), 1u};
         ProfScope ps(PK_GEMM, flops);
-        kern<<<grid, kGemmThreads, smem, g_stream>>>(g);
+        CK(launch_k(kern, grid, dim3(kGemmThreads), smem, g_stream, g));
         CK_LAUNCH("gemm_update_kernel");
         return 0;
     }

@@ -1,7 +1,10 @@
 """GPU parity of the real path's launch switches (README "Runtime switches"): the
 update GEMM's early A issue (`gemm_ws_kernel`, first k-tiles copied before the dependent-launch
 wait) forced on for every launch (several tiles per consumer group after the early ones), forced
-off, and combined with the diagonal kernel's start trigger.  Shapes: real TriangEig m = 700 at
+off, and combined with the diagonal kernel's start trigger; the real update on the persistent
+kernel only / the one-tile-per-CTA kernel only (the default picks per launch), which must agree
+bit for bit (same k order, same epilogue roundings: a multi-GPU shard may take the other kernel
+than the full solve).  Shapes: real TriangEig m = 700 at
 n_b = 64 (K = 64: more k-tiles than ring stages) and n_b = 32 (K = 32: fewer), and real safe
 solves op N at n_b = 13 (ragged k-tiles in the early copies) and op C at n_b = 32.  The switches
 are read once per process, so each variant runs in a subprocess; the comparison against the
@@ -60,6 +63,8 @@ VARIANTS = {
     "early_a_always": {"MSTRSM_EARLY_A": "1"},
     "early_a_never": {"MSTRSM_EARLY_A": "0"},
     "early_a_with_diag_trigger": {"MSTRSM_EARLY_A": "1", "MSTRSM_DIAGL_TRIGGER": "1"},
+    "gemm_real_ws": {"MSTRSM_GEMM_REAL": "ws"},
+    "gemm_real_classic": {"MSTRSM_GEMM_REAL": "classic"},
 }
 
 
@@ -87,3 +92,18 @@ def test_gpu_real_launch_variant_parity(name, oracle_results, tmp_path):
     for op in ("N", "C"):
         Xo, eo = oracle_results[op]
         assert_parity(got["X" + op], got["e" + op], Xo, eo, what=f"{name} real op {op} solve")
+
+
+def _run(tmp_path, name, env_over):
+    path = str(tmp_path / f"{name}.npz")
+    r = subprocess.run([sys.executable, "-c", _SCRIPT, path, ROOT], env=dict(os.environ, **env_over), cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(path)
+
+
+def test_gpu_real_gemm_kernels_bit_identical(tmp_path):
+    a = _run(tmp_path, "ws", {"MSTRSM_GEMM_REAL": "ws"})
+    b = _run(tmp_path, "classic", {"MSTRSM_GEMM_REAL": "classic"})
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
