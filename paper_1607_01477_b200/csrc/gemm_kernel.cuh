@@ -43,6 +43,8 @@ struct GemmArgs {
     int64_t col0;          // first column
     const int *dblk;       // per-column exponent delta (nullable)
     long long *pt;         // phase times (MSTRSM_PHASE_TIMES builds only; nullable)
+    int early_a;           // gemm_update_kernel: the first stages' A tiles (read-only U) before the wait
+    int trig;              // gemm_update_kernel: let the next grid launch at this one's start
 };
 
 // Tile geometry.  Complex: CTA 64 (rows) x 64 (cols), warp 32x32, BK = 16.
@@ -99,21 +101,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
     // from dblk once per CTA while the pipeline fills
     __shared__ double s_sc[BN];
     __shared__ int s_d[BN];
-    pdl_wait();                       // (launched as a programmatic dependent: before any global access)
-    if (tid < BN) {
-        const int64_t gj = n0 + tid;
-        const int d = (g.dblk && gj < g.N) ? g.dblk[g.col0 + gj] : 0;
-        s_d[tid] = d;
-        s_sc[tid] = d >= -1022 ? __longlong_as_double((long long)(1023 + d) << 52) : 0.0;
-    }
-
     auto stageA = [&](int s) { return smem + s * gemm_stage_elems<T>(); };
     auto stageX = [&](int s) { return smem + s * gemm_stage_elems<T>() + BM * BK; };
 
-    auto load_stage = [&](int s, int kt) {
-        T *As = stageA(s), *Xs = stageX(s);
+    auto load_A = [&](int s, int kt) {
+        T *As = stageA(s);
         const int k0 = kt * BK;
-        // A tile
         if (!OPC) {
             // BK columns of U, BM contiguous rows each
 #pragma unroll
@@ -139,6 +132,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
                 cp_async<ESZ>(As + offRK<T>(mm, k), src, v);
             }
         }
+    };
+    auto load_X = [&](int s, int kt) {
+        T *Xs = stageX(s);
+        const int k0 = kt * BK;
         // X tile: BN columns of B, BK contiguous rows each
 #pragma unroll
         for (int it = 0; it < (BN * BK) / kGemmThreads; it++) {
@@ -151,6 +148,24 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
             cp_async<ESZ>(Xs + offRK<T>(nn, k), src, v);
         }
     };
+    auto load_stage = [&](int s, int kt) { load_A(s, kt); load_X(s, kt); };
+
+    // U is read-only during a solve: with early_a the first stages' A tiles are issued before the
+    // wait for the preceding grid (launched as a programmatic dependent), which X, C and d need.
+    // They join the first stage's cp.async group, so the pipeline's group counting is unchanged.
+    if (g.trig) pdl_trigger();
+    if (g.early_a) {
+#pragma unroll
+        for (int s = 0; s < kGemmStages - 1; s++)
+            if (s < nk) load_A(s, s);
+    }
+    pdl_wait();
+    if (tid < BN) {
+        const int64_t gj = n0 + tid;
+        const int d = (g.dblk && gj < g.N) ? g.dblk[g.col0 + gj] : 0;
+        s_d[tid] = d;
+        s_sc[tid] = d >= -1022 ? __longlong_as_double((long long)(1023 + d) << 52) : 0.0;
+    }
 
     // accumulators: real part (and imaginary part for complex), 2 doubles per 8x8 sub-tile
     double accR[MI][NI][2], accI[CPX ? MI : 1][CPX ? NI : 1][2];
@@ -164,7 +179,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_update_kernel(GemmArgs<T
 
 #pragma unroll
     for (int s = 0; s < kGemmStages - 1; s++) {
-        if (s < nk) load_stage(s, s);
+        if (s < nk) {
+            if (g.early_a) load_X(s, s);
+            else load_stage(s, s);
+        }
         cp_async_commit();
     }
 

@@ -108,6 +108,19 @@ static int gemm_early_a() {
     return v;
 }
 
+// MSTRSM_GEMM_TRIGGER=0|1: the one-tile-per-CTA kernel lets the next grid (the next diagonal step,
+// which stages its read-only triangle before its wait) launch at its start never / always.
+// Default: for launches of at most g_num_sms / 4 tiles, which leave the next step's CTAs SMs of
+// their own (c1 0.186 -> 0.175 ms, real trsm 256 0.124 -> 0.113 with it; c2, whose updates cover
+// the GPU, 1.108 -> 1.154 with it everywhere: profiles/r02/exp_small_gemm_s3.txt).
+static int gemm_classic_trigger(int64_t tiles) {
+    static const int v = [] {
+        const char *e = getenv("MSTRSM_GEMM_TRIGGER");
+        return (e && (e[0] == '0' || e[0] == '1') && !e[1]) ? e[0] - '0' : -1;
+    }();
+    return v >= 0 ? v : (tiles <= g_num_sms / 4 ? 1 : 0);
+}
+
 template <typename T, bool OPC>
 int launch_gemm(const GemmArgs<T> &g) {
     const double flops = double(g.M) * g.N * g.K * (S<T>::cplx_ ? 8.0 : 2.0);
@@ -121,8 +134,11 @@ int launch_gemm(const GemmArgs<T> &g) {
         constexpr int smem = gemm_smem_bytes<T>();
         if (first_on_device(attr_set)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         dim3 grid{unsigned(tiles_m), unsigned(tiles_n), 1u};
+        GemmArgs<T> ga = g;
+        ga.early_a = gemm_early_a() == 1 ? 1 : 0;   // (measured no gain here: exp_small_gemm_s3.txt)
+        ga.trig = gemm_classic_trigger(tiles_m * tiles_n);
         ProfScope ps(PK_GEMM, flops);
-        CK(launch_k(kern, grid, dim3(kGemmThreads), smem, g_stream, g));
+        CK(launch_k(kern, grid, dim3(kGemmThreads), smem, g_stream, ga));
         CK_LAUNCH("gemm_update_kernel");
         return 0;
     }

@@ -65,6 +65,8 @@ VARIANTS = {
     "early_a_with_diag_trigger": {"MSTRSM_EARLY_A": "1", "MSTRSM_DIAGL_TRIGGER": "1"},
     "gemm_real_ws": {"MSTRSM_GEMM_REAL": "ws"},
     "gemm_real_classic": {"MSTRSM_GEMM_REAL": "classic"},
+    "both_triggers": {"MSTRSM_GEMM_TRIGGER": "1", "MSTRSM_DIAGL_TRIGGER": "1"},
+    "no_gemm_trigger": {"MSTRSM_GEMM_TRIGGER": "0"},
 }
 
 
