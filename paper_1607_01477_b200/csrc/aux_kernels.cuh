@@ -523,13 +523,21 @@ __global__ void finalize_kernel(int op, T *__restrict__ B, int64_t ldb, int64_t 
         int64_t r = rowend ? rowend[j] : m;
         T *x = B + j * ldb;
         if (Etab) {
-            for (int64_t b = 0; b < nblk; b++) {
-                Blk bl = block_rows(op, m, nb, b);
-                if (bl.lo >= r) continue;
-                int d = ej - Etab[b * n + j];
-                if (d == 0) continue;
-                int64_t hh = bl.hi < r ? bl.hi : r;
-                for (int64_t l = bl.lo + lane; l < hh; l += 32) x[l] = S<T>::ldx(x[l], d);
+            // the frames of 32 blocks at a time, one per lane (one round of loads instead of a
+            // chain of nblk), then the blocks whose frame differs, in turn, by the whole warp
+            for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
+                const int64_t bq = b0 + lane;
+                int d = 0;
+                if (bq < nblk && block_rows(op, m, nb, bq).lo < r) d = ej - Etab[bq * n + j];
+                unsigned todo = __ballot_sync(0xffffffffu, d != 0);
+                while (todo) {
+                    const int s = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const int ds = __shfl_sync(0xffffffffu, d, s);
+                    const Blk bl = block_rows(op, m, nb, b0 + s);
+                    const int64_t hh = bl.hi < r ? bl.hi : r;
+                    for (int64_t l = bl.lo + lane; l < hh; l += 32) x[l] = S<T>::ldx(x[l], ds);
+                }
             }
         }
         if (lane == 0) {
